@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the DistD2 fp64 batched tridiagonal solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Metric (BASELINE.json): achieved HBM GB/s (and % of measured peak) of the
+DistD2 fp64 x/y/z solve of the 6th-order compact d/dx operator, periodic.
+
+A STEP is one x, one y and one z solve of the whole field: three calls of the
+hot path, each over its own SZ-blocked (n_groups, n, 32) fp64 field already
+resident in HBM (inputs 1 GiB each at 512^3: larger than the 126 MB L2, so no
+flush between iterations). `value` counts the algorithmic bytes of the path,
+16 B per grid point per solve (one fp64 read + one fp64 write),
+divided by the device time of the K timed steps (CUDA events, max over
+ranks).
+
+N = 1: configs[1] of BASELINE.json, 512^3 x/y/z on one GPU.
+N > 1: configs[2], 1024^3 decomposed ALONG THE SOLVE DIRECTION over N GPUs
+       (one process per GPU, NCCL neighbour rounds), strong scaling.
+
+--impl reference: the reference's CPU algorithm (the pinned NumPy restatement
+in oracle/, the reference itself being Python that cannot travel to the GPU
+box) on the host cores, same metric, bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "achieved HBM GB/s & % peak, DistD2 fp64 512^3 x/y/z solve at 1/2/4/8 B200"
+BYTES_PER_POINT = 16          # algorithmic: 8 B read + 8 B write per point per solve
+SZ = 32
+
+
+def peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    path = os.path.join(HERE, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ GPU arm
+
+def make_fields(torch, n, dev, seed):
+    """Three SZ-blocked fields (x, y, z) of one random n^3 fp64 field."""
+    import paper_2411_13532_b200 as T
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    cart = torch.randn((n, n, n), dtype=torch.float64, device=dev, generator=g)
+    fields = {}
+    for d in "xyz":
+        fields[d] = T.pack(cart, T.LayoutDescriptor(n, n, n, SZ, d)).data
+    del cart
+    return fields
+
+
+def run_single(args, torch):
+    import paper_2411_13532_b200 as T
+    n = args.size or 512
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    sys_, st = T.assemble(T.sixth_order_first_derivative(2 * np.pi / n), n, periodic=True)
+    part = T.SubdomainPartition((n,))
+    fields = make_fields(torch, n, dev, 1234 + 1)
+    outs = {d: torch.empty_like(fields[d]) for d in "xyz"}
+    plan = T.get_plan(sys_, st, part)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        for i, d in enumerate("xyz"):
+            if ev is not None:
+                ev[d][0].record(stream)
+            T.run_distd2(sys_, fields[d], part=part, stencil=st, out=outs[d])
+            if ev is not None:
+                ev[d][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-launch events on the launching stream inside the timed region
+    evs = [{d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for d in "xyz"} for _ in range(args.steps)]
+    clk = Clocks(0)
+    clk.start()
+    time.sleep(0.3)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms_total = t0.elapsed_time(t1)
+    ms_step = ms_total / args.steps
+    per_dir = {d: statistics.mean(e[d][0].elapsed_time(e[d][1]) for e in evs) for d in "xyz"}
+    launch_ms = statistics.mean(per_dir.values())
+
+    points = n ** 3
+    alg_bytes_step = 3 * BYTES_PER_POINT * points
+    value = alg_bytes_step / (ms_step * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    achieved = BYTES_PER_POINT * points / (launch_ms * 1e-3) / 1e9
+
+    e2e = run_e2e(args, torch, T, sys_, st, part, fields, n)
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (randn fp64 field, seed 1235), operator = assemble(6th-order d/dx, "
+                "periodic)",
+        "config": {"workload": f"{n}^3 x/y/z DistD2 solve, 1 GPU (BASELINE configs[1])",
+                   "n": n, "directions": "x,y,z", "sz": SZ, "partition": [n],
+                   "path": plan.path, "chunk_rows": plan.info.chunk_rows,
+                   "uniform_table": bool(plan.info.uniform),
+                   "l2": "inputs 1 GiB per direction > 126 MB L2; no flush",
+                   "parallelism": "single GPU"},
+        "pct_peak": round(100 * value / peak, 2),
+        "gdof_per_s": round(3 * points / (ms_step * 1e-3) / 1e9, 2),
+        "ms_per_solve": {d: round(v, 5) for d, v in per_dir.items()},
+        "direction_spread_pct": round(100 * (max(per_dir.values()) - min(per_dir.values()))
+                                      / min(per_dir.values()), 2),
+        "roofline": {"bound": "hbm", "kernel": "k_fast<32,SOLVE,uniform>",
+                     "achieved": round(achieved, 2), "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(),
+                     "algorithmic_bytes_per_launch": BYTES_PER_POINT * points},
+        "e2e": e2e,
+        "gpu_launches": 3 * args.steps,
+        "clocks": clocks,
+    }
+    res["cpu_baseline"] = cpu_baseline(args, n)
+    return res
+
+
+def run_e2e(args, torch, T, sys_, st, part, fields, n):
+    """Same metric through the public API with HOST buffers: every step copies
+    the three pinned host fields in, solves, and copies the results out."""
+    host_in = {d: fields[d].cpu().pin_memory() for d in "xyz"}
+    host_out = {d: torch.empty_like(host_in[d]).pin_memory() for d in "xyz"}
+    steps = max(2, min(args.steps, args.e2e_steps))
+
+    def step():
+        for d in "xyz":
+            T.run_distd2(sys_, host_in[d], part=part, stencil=st, out=host_out[d])
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    nbytes = sum(h.numel() * 8 for h in host_in.values())
+    return {"value": round(3 * BYTES_PER_POINT * n ** 3 / dt / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "ms_per_step": round(dt * 1e3, 3), "steps": steps,
+            "api": "run_distd2(sys, pinned_host_tensor, out=pinned_host_tensor) x3"}
+
+
+def run_multi(args, torch):
+    """N > 1: one rank per GPU, 1024^3 decomposed along the solve direction."""
+    import torch.distributed as dist
+    import paper_2411_13532_b200 as T
+    from paper_2411_13532_b200.transport import RankContext
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    n = args.size or 1024
+    sys_, st = T.assemble(T.sixth_order_first_derivative(2 * np.pi / n), n, periodic=True)
+    part = T.SubdomainPartition.balanced(n, world)
+    ctx = RankContext.from_process_group(cyclic=True)
+    solver = T.DistD2Rank(sys_, st, part, ctx)
+    m = part.local_sizes[rank]
+    groups = n * n // SZ
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + 2 + rank)
+    fields = {d: torch.randn((groups, m, SZ), dtype=torch.float64, device=dev, generator=g)
+              for d in "xyz"}
+    outs = {d: torch.empty_like(fields[d]) for d in "xyz"}
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for d in "xyz":
+            solver.solve(fields[d], outs[d])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = clk.stop()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = float(ms.item())
+    points = n ** 3
+    value = 3 * BYTES_PER_POINT * points / (ms_step * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    res = None
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (randn fp64 local slabs)",
+            "config": {"workload": f"{n}^3 x/y/z DistD2 solve decomposed along the solve "
+                                   f"direction over {world} GPUs (BASELINE configs[2])",
+                       "n": n, "directions": "x,y,z", "sz": SZ,
+                       "partition": list(part.local_sizes), "path": solver.path,
+                       "exchange": "NCCL P2P, 2 neighbour rounds per solve",
+                       "l2": "inputs > 126 MB L2; no flush", "parallelism": f"dd{world}"},
+            "pct_peak": round(100 * value / (world * peak), 2),
+            "gdof_per_s": round(3 * points / (ms_step * 1e-3) / 1e9, 2),
+            "roofline": {"bound": "hbm", "kernel": "whole step per GPU",
+                         "achieved": round(value / world, 2), "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(value / world / peak, 4), "traffic": None},
+            "e2e": None, "gpu_launches": 3 * 3 * args.steps, "clocks": clocks,
+            "cpu_baseline": None,
+        }
+    dist.barrier()
+    dist.destroy_process_group()
+    return res
+
+
+# ------------------------------------------------------------ CPU legs
+
+def sample_fields(n, groups, seed):
+    """First `groups` SZ-groups of the x/y/z packings of the same random
+    n^3 field the reference bench would build (layout.py:105-134)."""
+    from oracle import tds_oracle as O
+    u = np.random.default_rng(seed).standard_normal((n, n, n))
+    out = {}
+    for d in "xyz":
+        axes = O._transverse_axes(d)
+        lines = u.transpose(axes).reshape(-1, n)[:groups * SZ]
+        out[d] = np.ascontiguousarray(lines.reshape(groups, SZ, n).transpose(0, 2, 1))
+    return out
+
+
+def cpu_time_sample(n, groups, threads, directions="xyz"):
+    from oracle import tds_oracle as O
+    lo, di, up, st = O.assemble("d1", n, 2 * np.pi / n, True)
+    flds = sample_fields(n, groups, 1234 + 1)
+    t0 = time.perf_counter()
+    for d in directions:
+        O.run_distd2_threaded(lo, di, up, True, flds[d], st, threads=threads,
+                              groups_per_task=max(1, groups // (4 * threads)))
+    dt = time.perf_counter() - t0
+    pts = len(directions) * groups * n * SZ
+    return BYTES_PER_POINT * pts / dt / 1e9, dt, pts
+
+
+def cpu_baseline(args, n):
+    threads = len(os.sched_getaffinity(0))
+    groups = args.cpu_groups
+    gbs, dt, pts = cpu_time_sample(n, groups, threads, "x")
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"x-direction solve of {groups} of {n * n // SZ} SZ-groups "
+                      f"({pts} points) of the {n}^3 field, oracle/tds_oracle.run_distd2 "
+                      f"(NumPy restatement of reference run_distd2, P=1), {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    n = 512 if args.gpus == 1 else (args.size or 1024)
+    n = args.size or n
+    threads = len(os.sched_getaffinity(0))
+    groups = args.cpu_groups
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_time_sample(n, max(1, groups // 8), threads)
+    times, last = [], None
+    for _ in range(args.steps):
+        gbs, dt, pts = cpu_time_sample(n, groups, threads)
+        times.append(dt)
+        last = (gbs, pts)
+    dt = statistics.mean(times)
+    gbs = BYTES_PER_POINT * last[1] / dt / 1e9
+    sample = (f"x,y,z solves of {groups} of {n * n // SZ} SZ-groups ({last[1]} points) of the "
+              f"{n}^3 field per step, oracle/tds_oracle.run_distd2 (NumPy restatement of "
+              f"reference run_distd2 P=1) on {threads} host threads")
+    peak, _ = peaks()
+    return {"metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{n}^3 x/y/z DistD2 solve (sampled lines)", "n": n,
+                       "directions": "x,y,z", "sz": SZ},
+            "pct_peak": round(100 * gbs / peak, 5),
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=0, help="grid extent (default 512 / 1024)")
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--cpu-groups", type=int, default=512)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    import torch
+    if args.gpus > 1 or "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
+        res = run_multi(args, torch)
+    else:
+        res = run_single(args, torch)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * tds_b200.h -- C ABI of the B200-native DistD2 batched tridiagonal solver.
+ *
+ * Drop-in boundary for the reference package `tds` (arXiv 2411.13532,
+ * /root/reference/pkg/src/tds). The reference is pure Python/NumPy and has
+ * no FFI of its own; the entry points below are what its operator layer
+ * would bind (ctypes stub in INTEGRATION.md). Every function:
+ *   - takes plain pointers and sizes (no torch types);
+ *   - takes DEVICE pointers for field data, owned by the caller;
+ *   - takes an explicit cudaStream_t (passed as void*), never synchronises;
+ *   - returns 0 (TDS_OK) or a TDS_ERR_* code; tds_last_error() gives text.
+ * All error conditions the reference raises (SingularPivot, SingularPair,
+ * SingularCorrection, ValueError) are coefficient-only and are raised by
+ * tds_plan_create on the host; kernels are error-free.
+ *
+ * Field layout ("SZ-blocked", reference layout.py:1-13): a field is
+ * (groups, n, sz) fp64, linear index lane + sz*pos + sz*n*group. A "line"
+ * is one (group, lane) pair; line l lives at (l/sz)*n*sz + l%sz with row
+ * stride sz. Position-major (n, lanes) arrays are the case groups=1, sz=lanes.
+ */
+#ifndef TDS_B200_H
+#define TDS_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDS_ABI_VERSION 1
+
+#define TDS_OK 0
+#define TDS_ERR_INVALID 1             /* ValueError (shape/partition/size)  */
+#define TDS_ERR_SINGULAR_PIVOT 2      /* errors.SingularPivot               */
+#define TDS_ERR_SINGULAR_PAIR 3       /* errors.SingularPair                */
+#define TDS_ERR_SINGULAR_CORRECTION 4 /* errors.SingularCorrection          */
+#define TDS_ERR_CUDA 5                /* CUDA runtime error                 */
+#define TDS_ERR_UNSUPPORTED 6         /* e.g. NotImplementedError           */
+
+/* plan flags */
+#define TDS_FLAG_STRICT 1   /* reference arithmetic order, no FMA: bit-identical
+                               to the reference (staged kernels)              */
+#define TDS_FLAG_STAGED 2   /* force the staged (multi-pass) kernels           */
+
+/* execution paths reported by tds_plan_query */
+#define TDS_PATH_FAST 0     /* single-pass chunked kernel (16 B/pt)           */
+#define TDS_PATH_STAGED 1   /* staged kernels (reference structure)           */
+
+typedef struct tds_plan tds_plan;
+
+typedef struct {
+    int n;              /* global rows per line                               */
+    int rank_count;     /* P of the partition                                 */
+    int rank;           /* -1: all P ranks emulated on this device            */
+    int block_rows;     /* rows per line held by this device                  */
+    int path;           /* TDS_PATH_*                                         */
+    int strict;         /* 1 if TDS_FLAG_STRICT                               */
+    int chunk_rows;     /* M (fast path)                                      */
+    int chunks;         /* C = block_rows / M (fast path)                     */
+    int uniform;        /* 1: every chunk shares one coefficient table        */
+    int periodic;
+    double max_dropped; /* max |dropped coupling| over ranks (audit)          */
+    double dominance_margin; /* system.py:163-167 of the global system        */
+} tds_plan_info;
+
+int tds_abi_version(void);
+const char* tds_last_error(void);
+/* rank whose per-rank stage failed (-1: not rank-specific); the Python
+ * shim wraps such errors in RankPanic like transport.spawn_ranks does. */
+int tds_last_error_rank(void);
+
+/*
+ * Build a plan for one operator: the global system (lower, diag, upper,
+ * periodic; system.py:31-51), its width-5 RHS stencil (n x 5 row-major,
+ * NULL = identity; distributed.py:71-116) and a partition of the n rows
+ * into `rank_count` blocks `sizes` (system.py:115-155).
+ *   rank == -1 : this device runs the whole operator, all ranks emulated
+ *                (replaces distributed.run_distd2, distributed.py:399-449);
+ *   rank == k  : this device owns rank k's rows only (replaces the per-rank
+ *                preprocess + distd2_solve, distributed.py:144-199,327-366).
+ * Host-side, O(n + C^3): runs Alg. 5 (preprocess) per rank and per chunk and
+ * uploads the coefficient tables with cudaMemcpy on the current device.
+ */
+int tds_plan_create(const double* lower, const double* diag, const double* upper,
+                    int periodic, const double* stencil, int n,
+                    const int* sizes, int rank_count, int rank, int flags,
+                    tds_plan** out);
+/* Per-rank plan from rank-local data only, the reference's per-rank view:
+ * a, b, c, stencil are rank k's local_slice bands (m rows; a[0] couples to
+ * the previous rank's last row, c[m-1] to the next rank's first row; open
+ * edges 0) and stencil rows; prev_sc_last / next_sa_first are the cached
+ * neighbour couplings of share_pair_coeffs (distributed.py:308-324, D16). */
+int tds_plan_create_local(const double* a, const double* b, const double* c,
+                          const double* stencil, int m, int has_prev, int has_next,
+                          double prev_sc_last, double next_sa_first, int flags,
+                          tds_plan** out);
+int tds_plan_destroy(tds_plan* plan);
+int tds_plan_query(const tds_plan* plan, tds_plan_info* info);
+
+/* Rank-level DistCoeffs of rank k (distributed.py:43-68), host arrays of
+ * length sizes[k]: s_a, s_c, w, f, r; dropped[2] = signed dropped couplings. */
+int tds_plan_rank_coeffs(const tds_plan* plan, int k, double* s_a, double* s_c,
+                         double* w, double* f, double* r, double* dropped);
+
+/* Alg. 5 alone on one block of m rows (preprocess, distributed.py:144-199):
+ * a[0] couples to the row before the block, c[m-1] to the row after it.
+ * Outputs host arrays of length m, bit-identical to the reference; s_c[0]
+ * and s_a[m-1] are zeroed and their signed values returned in dropped[2]. */
+int tds_preprocess(const double* a, const double* b, const double* c, int m,
+                   double* s_a, double* s_c, double* w, double* f, double* r,
+                   double* dropped);
+
+/*
+ * Whole-operator solve (rank == -1 plans): out = A^{-1} stencil(u) with the
+ * reference's truncation at the partition's rank boundaries
+ * (run_distd2, distributed.py:399-449). u, out: (groups, n, sz) device.
+ */
+int tds_solve(const tds_plan* plan, const double* u, double* out,
+              long long groups, int sz, void* stream);
+
+/* ---- per-rank distributed pipeline (rank == k plans) -------------------
+ * ROUND 1 (halo, transport.py:142-171) and ROUND 2 (boundary rows,
+ * transport.py:174-191) are done by the caller (NCCL send/recv) between
+ * these calls. All arrays are device memory:
+ *   u, out              (groups, m, sz)    this rank's block
+ *   first2, last2       (groups, 2, sz)    rows {0,1} and {m-2,m-1} of u
+ *   halo_lo, halo_hi    (groups, 2, sz)    prev's last 2 / next's first 2
+ *                                          rows, NULL on an open edge
+ *   d_first, d_last     (groups, sz)       decoupled rows d[0], d[m-1]
+ *   prev_last, next_first (groups, sz)     neighbours' d[m-1] / d[0], NULL
+ *                                          on an open edge                 */
+int tds_halo_rows(const tds_plan* plan, const double* u, double* first2,
+                  double* last2, long long groups, int sz, void* stream);
+/* Alg. 6 boundary values d[0], d[m-1] of every line (decouple_fused,
+ * distributed.py:257-276). `scratch` is (groups, m, sz); the fast path does
+ * not touch it, the staged path keeps d there for tds_finish. */
+int tds_boundary_rows(const tds_plan* plan, const double* u, const double* halo_lo,
+                      const double* halo_hi, double* d_first, double* d_last,
+                      double* scratch, long long groups, int sz, void* stream);
+/* 2x2 boundary pairs + Alg. 7 substitution (distributed.py:279-305,345-366).
+ * For the staged path `out` must be the `scratch` given to tds_boundary_rows. */
+int tds_finish(const tds_plan* plan, const double* u, const double* halo_lo,
+               const double* halo_hi, const double* d_first, const double* d_last,
+               const double* prev_last, const double* next_first, double* out,
+               long long groups, int sz, void* stream);
+
+/* ---- phase-level kernels, reference arithmetic (bit-identical) ----------
+ * Position-major (rows, lanes) device arrays, as the reference phase
+ * functions take them. Coefficients are host arrays (copied per call). */
+/* decouple_fused: u_ext (m+4, lanes) -> d (m, lanes); distributed.py:257-276 */
+int tds_decouple_fused(const double* u_ext, const double* stencil, const double* w,
+                       const double* f, const double* r, double* d, int m,
+                       long long lanes, void* stream);
+/* substitute: d (m, lanes) -> out (m, lanes); distributed.py:296-305 */
+int tds_substitute(const double* d, const double* s_a, const double* s_c,
+                   const double* u_start, const double* u_end, double* out, int m,
+                   long long lanes, void* stream);
+/* solve_boundary_pair over lanes; distributed.py:279-293 */
+int tds_boundary_pair(const double* d_last, const double* d_first, double s_c_last,
+                      double s_a_first, double* u_last, double* u_first,
+                      long long lanes, void* stream);
+/* thomas_solve / periodic_thomas_solve (serial.py:26-90) on a (groups, n, sz)
+ * field; an RhsBatch (m, n) is groups = m, sz = 1. */
+int tds_thomas(const double* lower, const double* diag, const double* upper,
+               int periodic, const double* rhs, double* out, int n,
+               long long groups, int sz, void* stream);
+
+/* ---- layout (layout.py:82-152) -------------------------------------------
+ * Cartesian (nx, ny, nz) C-order <-> SZ-blocked (groups, n, sz) field for
+ * `direction` ('x'=0,'y'=1,'z'=2). groups*sz may exceed the line count:
+ * the ghost lines are zero-filled by tds_pack (LayoutDescriptor pad=True). */
+int tds_pack(const double* cart, double* field, int nx, int ny, int nz, int sz,
+             int direction, long long groups, void* stream);
+int tds_unpack(const double* field, double* cart, int nx, int ny, int nz, int sz,
+               int direction, long long groups, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDS_B200_H */

@@ -1,0 +1,277 @@
+// C-ABI entry points (include/tds_b200.h): argument checking and dispatch of
+// the plan to the fast or staged kernels. No allocation on the solve path
+// except the phase-level calls that take host coefficient arrays.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tds_internal.h"
+
+using tds::set_err;
+
+namespace {
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check_field(const tds_plan* p, long long groups, int sz) {
+    if (!p) return set_err(TDS_ERR_INVALID, "null plan");
+    if (groups < 0 || sz < 1) return set_err(TDS_ERR_INVALID, "bad field shape");
+    return TDS_OK;
+}
+
+tds::FastArgs fast_args(const tds_plan* p, long long lines, int sz) {
+    tds::FastArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.tab = p->d_tab;
+    a.Hp = p->d_Hp;
+    a.g = p->d_g;
+    a.lines = lines;
+    a.rows = p->block_rows;
+    a.sz = sz;
+    a.chunks = p->C;
+    int per_tile = p->C * tds::TL;
+    a.tiles_per_cta = per_tile >= 256 ? 1 : 256 / per_tile;
+    a.has_prev = p->has_prev;
+    a.has_next = p->has_next;
+    a.sa_first = p->sa_first;
+    a.sc_last = p->sc_last;
+    a.prev_sc_last = p->prev_sc_last;
+    a.next_sa_first = p->next_sa_first;
+    a.det_prev = p->det_prev;
+    a.det_next = p->det_next;
+    a.ut = p->ut;
+    return a;
+}
+
+long long tiles_of(long long lines) { return (lines + tds::TL - 1) / tds::TL; }
+
+tds::StagedArgs staged_args(const tds_plan* p, long long lines, int sz) {
+    tds::StagedArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.st = p->d_st;
+    a.w = p->d_w;
+    a.f = p->d_f;
+    a.r = p->d_r;
+    a.sa = p->d_sa;
+    a.sc = p->d_sc;
+    a.boff = p->d_boff;
+    a.bsize = p->d_bsize;
+    a.bconst = p->d_bconst;
+    a.lines = lines;
+    a.rows = p->block_rows;
+    a.sz = sz;
+    a.nb = p->nb;
+    a.th_a = p->d_tha;
+    a.th_w = p->d_thw;
+    a.th_cp = p->d_thcp;
+    a.th_z = p->d_thz;
+    a.th_b0 = p->th_b0;
+    a.th_qlast = p->th_qlast;
+    a.th_den = p->th_den;
+    a.periodic = p->periodic;
+    return a;
+}
+
+// scratch for the staged path's boundary rows, stream-ordered
+int scratch_alloc(double** ptr, size_t count, cudaStream_t s) {
+    return tds::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(ptr),
+                                           (count ? count : 1) * sizeof(double), s),
+                           "cudaMallocAsync");
+}
+
+}  // namespace
+
+extern "C" int tds_solve(const tds_plan* p, const double* u, double* out, long long groups,
+                         int sz, void* stream) {
+    int rc = check_field(p, groups, sz);
+    if (rc) return rc;
+    if (p->rank >= 0 && p->P > 1)
+        return set_err(TDS_ERR_INVALID, "tds_solve needs a whole-operator plan (rank = -1)");
+    if (!u || !out) return set_err(TDS_ERR_INVALID, "null field pointer");
+    const long long lines = groups * sz;
+    if (p->path == TDS_PATH_FAST) {
+        tds::FastArgs a = fast_args(p, lines, sz);
+        a.u = u;
+        a.out = out;
+        a.edge_mode = p->periodic ? tds::EDGE_WRAP : tds::EDGE_ZERO;
+        return tds::launch_fast(p->M, tds::MODE_SOLVE, p->uniform, a, tiles_of(lines), S(stream));
+    }
+    tds::StagedArgs a = staged_args(p, lines, sz);
+    a.u = u;
+    a.out = out;
+    a.edge_mode = p->periodic ? tds::EDGE_WRAP : tds::EDGE_ZERO;
+    if (p->P == 1) return tds::launch_thomas(a, S(stream));
+    double* rows = nullptr;
+    if ((rc = scratch_alloc(&rows, size_t(2) * p->nb * lines, S(stream)))) return rc;
+    a.d_first = rows;
+    a.d_last = rows + size_t(p->nb) * lines;
+    rc = tds::launch_staged_decouple(a, S(stream));
+    if (!rc) rc = tds::launch_staged_finish(a, S(stream));
+    cudaFreeAsync(rows, S(stream));
+    return rc;
+}
+
+extern "C" int tds_halo_rows(const tds_plan* p, const double* u, double* first2, double* last2,
+                             long long groups, int sz, void* stream) {
+    int rc = check_field(p, groups, sz);
+    if (rc) return rc;
+    return tds::launch_halo_rows(u, first2, last2, groups * sz, p->block_rows, sz, S(stream));
+}
+
+extern "C" int tds_boundary_rows(const tds_plan* p, const double* u, const double* halo_lo,
+                                 const double* halo_hi, double* d_first, double* d_last,
+                                 double* scratch, long long groups, int sz, void* stream) {
+    int rc = check_field(p, groups, sz);
+    if (rc) return rc;
+    if (p->rank < 0 || p->P < 2) return set_err(TDS_ERR_INVALID, "per-rank plan required");
+    const long long lines = groups * sz;
+    if (p->path == TDS_PATH_FAST) {
+        tds::FastArgs a = fast_args(p, lines, sz);
+        a.u = u;
+        a.halo_lo = halo_lo;
+        a.halo_hi = halo_hi;
+        a.edge_mode = tds::EDGE_HALO;
+        a.d_first_out = d_first;
+        a.d_last_out = d_last;
+        return tds::launch_fast(p->M, tds::MODE_PASS_A, p->uniform, a, tiles_of(lines), S(stream));
+    }
+    if (!scratch) return set_err(TDS_ERR_INVALID, "staged path needs the scratch block");
+    tds::StagedArgs a = staged_args(p, lines, sz);
+    a.u = u;
+    a.out = scratch;
+    a.halo_lo = halo_lo;
+    a.halo_hi = halo_hi;
+    a.edge_mode = tds::EDGE_HALO;
+    a.d_first = d_first;
+    a.d_last = d_last;
+    return tds::launch_staged_decouple(a, S(stream));
+}
+
+extern "C" int tds_finish(const tds_plan* p, const double* u, const double* halo_lo,
+                          const double* halo_hi, const double* d_first, const double* d_last,
+                          const double* prev_last, const double* next_first, double* out,
+                          long long groups, int sz, void* stream) {
+    int rc = check_field(p, groups, sz);
+    if (rc) return rc;
+    if (p->rank < 0 || p->P < 2) return set_err(TDS_ERR_INVALID, "per-rank plan required");
+    if ((p->has_prev && !prev_last) || (p->has_next && !next_first))
+        return set_err(TDS_ERR_INVALID, "missing neighbour boundary rows");
+    const long long lines = groups * sz;
+    if (p->path == TDS_PATH_FAST) {
+        tds::FastArgs a = fast_args(p, lines, sz);
+        a.u = u;
+        a.out = out;
+        a.halo_lo = halo_lo;
+        a.halo_hi = halo_hi;
+        a.edge_mode = tds::EDGE_HALO;
+        a.d_first_in = d_first;
+        a.d_last_in = d_last;
+        a.prev_last = prev_last;
+        a.next_first = next_first;
+        return tds::launch_fast(p->M, tds::MODE_PASS_B, p->uniform, a, tiles_of(lines), S(stream));
+    }
+    tds::StagedArgs a = staged_args(p, lines, sz);
+    a.out = out;
+    a.d_first = const_cast<double*>(d_first);
+    a.d_last = const_cast<double*>(d_last);
+    a.prev_last = prev_last;
+    a.next_first = next_first;
+    return tds::launch_staged_finish(a, S(stream));
+}
+
+// ------------------------------------------------------------ phase kernels
+
+
+extern "C" int tds_decouple_fused(const double* u_ext, const double* stencil, const double* w,
+                                  const double* f, const double* r, double* d, int m,
+                                  long long lanes, void* stream) {
+    if (m < 4) return set_err(TDS_ERR_INVALID, "local block needs at least 4 rows");
+    cudaStream_t s = S(stream);
+    double* buf = nullptr;
+    size_t mm = size_t(m);
+    int rc = scratch_alloc(&buf, mm * 8, s);
+    if (rc) return rc;
+    double *dst = buf, *dw = buf + 5 * mm, *df = buf + 6 * mm, *dr = buf + 7 * mm;
+    rc = tds::cuda_check(cudaMemcpyAsync(dst, stencil, 5 * mm * sizeof(double),
+                                         cudaMemcpyHostToDevice, s), "copy stencil");
+    if (!rc) rc = tds::cuda_check(cudaMemcpyAsync(dw, w, mm * 8, cudaMemcpyHostToDevice, s), "copy w");
+    if (!rc) rc = tds::cuda_check(cudaMemcpyAsync(df, f, mm * 8, cudaMemcpyHostToDevice, s), "copy f");
+    if (!rc) rc = tds::cuda_check(cudaMemcpyAsync(dr, r, mm * 8, cudaMemcpyHostToDevice, s), "copy r");
+    if (!rc) rc = tds::launch_decouple_pm(u_ext, dst, dw, df, dr, d, m, lanes, s);
+    // host arrays may be released once the copies are done
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(buf, s);
+    return rc;
+}
+
+extern "C" int tds_substitute(const double* d, const double* s_a, const double* s_c,
+                              const double* u_start, const double* u_end, double* out, int m,
+                              long long lanes, void* stream) {
+    if (m < 4) return set_err(TDS_ERR_INVALID, "local block needs at least 4 rows");
+    cudaStream_t s = S(stream);
+    double* buf = nullptr;
+    int rc = scratch_alloc(&buf, size_t(2) * m, s);
+    if (rc) return rc;
+    rc = tds::cuda_check(cudaMemcpyAsync(buf, s_a, size_t(m) * 8, cudaMemcpyHostToDevice, s), "copy s_a");
+    if (!rc)
+        rc = tds::cuda_check(cudaMemcpyAsync(buf + m, s_c, size_t(m) * 8, cudaMemcpyHostToDevice, s),
+                             "copy s_c");
+    if (!rc) rc = tds::launch_substitute_pm(d, buf, buf + m, u_start, u_end, out, m, lanes, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(buf, s);
+    return rc;
+}
+
+extern "C" int tds_boundary_pair(const double* d_last, const double* d_first, double s_c_last,
+                                 double s_a_first, double* u_last, double* u_first,
+                                 long long lanes, void* stream) {
+    double det = 1.0 - s_c_last * s_a_first;
+    if (!(det >= tds::PAIR_DET_FLOOR || det <= -tds::PAIR_DET_FLOOR)) {
+        char msg[64];
+        std::snprintf(msg, sizeof(msg), "boundary determinant %.3e", det);
+        return set_err(TDS_ERR_SINGULAR_PAIR, msg);
+    }
+    return tds::launch_pair(d_last, d_first, s_c_last, s_a_first, det, u_last, u_first, lanes,
+                            S(stream));
+}
+
+extern "C" int tds_thomas(const double* lower, const double* diag, const double* upper,
+                          int periodic, const double* rhs, double* out, int n, long long groups,
+                          int sz, void* stream) {
+    // A P=1 staged plan over a (groups, n, sz) field with the identity
+    // stencil (its zero weights never see the halo). RhsBatch (m, n) is the
+    // case groups=m, sz=1.
+    int one = n;
+    tds_plan* p = nullptr;
+    int rc = tds_plan_create(lower, diag, upper, periodic, nullptr, n, &one, 1, -1,
+                             TDS_FLAG_STAGED, &p);
+    if (rc) return rc;
+    tds::StagedArgs a = staged_args(p, groups * sz, sz);
+    a.u = rhs;
+    a.out = out;
+    a.edge_mode = tds::EDGE_ZERO;
+    rc = tds::launch_thomas(a, S(stream));
+    cudaStreamSynchronize(S(stream));
+    tds_plan_destroy(p);
+    return rc;
+}
+
+static int pack_common(const double* src, double* dst, int nx, int ny, int nz, int sz,
+                       int direction, long long groups, bool to_field, void* stream) {
+    if (direction < 0 || direction > 2 || sz < 1 || nx < 1 || ny < 1 || nz < 1)
+        return set_err(TDS_ERR_INVALID, "bad layout");
+    long long n = direction == 0 ? nx : (direction == 1 ? ny : nz);
+    long long lines = (long long)nx * ny * nz / n;
+    if (groups * sz < lines) return set_err(TDS_ERR_INVALID, "field has too few lines");
+    return tds::launch_pack(src, dst, nx, ny, nz, sz, direction, groups, to_field, S(stream));
+}
+
+extern "C" int tds_pack(const double* cart, double* field, int nx, int ny, int nz, int sz,
+                        int direction, long long groups, void* stream) {
+    return pack_common(cart, field, nx, ny, nz, sz, direction, groups, true, stream);
+}
+
+extern "C" int tds_unpack(const double* field, double* cart, int nx, int ny, int nz, int sz,
+                          int direction, long long groups, void* stream) {
+    return pack_common(field, cart, nx, ny, nz, sz, direction, groups, false, stream);
+}

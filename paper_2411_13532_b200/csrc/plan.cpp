@@ -1,0 +1,750 @@
+// Host-side plan builder: everything that depends only on the operator.
+//
+// Compiled with -ffp-contract=off so the scalar recurrences round exactly like
+// the reference's NumPy code (IEEE binary64, one rounding per operation); the
+// rank-level DistCoeffs, the Thomas multipliers and the pair determinants are
+// therefore bit-identical to the reference's own values.
+//
+// Reference anchors (/root/reference/pkg/src/tds):
+//   preprocess (Alg. 5) ........ distributed.py:144-199
+//   local_slice ................ distributed.py:119-133
+//   rank topology .............. transport.py:113-119
+//   pair determinant ........... distributed.py:288-290
+//   thomas / periodic thomas ... serial.py:26-90
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tds_internal.h"
+
+using std::vector;
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_err_rank = -1;
+}  // namespace
+
+namespace tds {
+
+int set_err(int code, const std::string& msg, int rank) {
+    g_err = msg;
+    g_err_rank = rank;
+    return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return TDS_OK;
+    return set_err(TDS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace tds
+
+using tds::set_err;
+
+extern "C" const char* tds_last_error(void) { return g_err.c_str(); }
+extern "C" int tds_last_error_rank(void) { return g_err_rank; }
+extern "C" int tds_abi_version(void) { return TDS_ABI_VERSION; }
+
+namespace {
+
+char buf[256];
+
+std::string fmt(const char* f, double v) {
+    std::snprintf(buf, sizeof(buf), f, v);
+    return buf;
+}
+
+// Alg. 5 (distributed.py:144-199) on one block of m rows. a[0] couples to the
+// row before the block, c[m-1] to the row after it. Same operation order as
+// the reference; the two couplings it discards are returned in drop_*.
+int preprocess_block(const double* a, const double* b, const double* c, int m,
+                     tds_rank_coeffs& co, int rank) {
+    if (m < 4)
+        return set_err(TDS_ERR_INVALID,
+                       "local block needs at least 4 rows, got " + std::to_string(m), rank);
+    co.sa.assign(m, 0.0);
+    co.sc.assign(m, 0.0);
+    co.w.assign(m, 0.0);
+    co.f.assign(m, 0.0);
+    co.r.assign(m, 0.0);
+    auto& sa = co.sa;
+    auto& sc = co.sc;
+    auto& w = co.w;
+    auto& f = co.f;
+    auto& r = co.r;
+    for (int j = 0; j < 2; ++j) {
+        sa[j] = a[j] / b[j];
+        sc[j] = c[j] / b[j];
+        w[j] = sc[j];
+        f[j] = 1.0 / b[j];
+        r[j] = 1.0 / b[j];
+    }
+    for (int j = 2; j < m; ++j) {
+        double den = b[j] - a[j] * sc[j - 1];
+        if (std::fabs(den) <= tds::PIVOT_FLOOR)
+            return set_err(TDS_ERR_SINGULAR_PIVOT,
+                           fmt("pivot %.3e at local row ", den) + std::to_string(j + 1), rank);
+        f[j] = 1.0 / den;
+        r[j] = a[j];
+        sa[j] = -a[j] * sa[j - 1] * f[j];
+        sc[j] = c[j] * f[j];
+    }
+    for (int j = m - 3; j > 0; --j) {
+        w[j] = sc[j];
+        sa[j] = sa[j] - sc[j] * sa[j + 1];
+        sc[j] = -sc[j] * sc[j + 1];
+    }
+    double clo = 1.0 - sc[0] * sa[1];
+    if (std::fabs(clo) <= tds::PIVOT_FLOOR)
+        return set_err(TDS_ERR_SINGULAR_PIVOT, fmt("closure pivot %.3e", clo), rank);
+    f[0] = 1.0 / clo;
+    sa[0] = f[0] * sa[0];
+    sc[0] = -f[0] * sc[0] * sc[1];
+    co.drop_first = sc[0];
+    co.drop_last = sa[m - 1];
+    return TDS_OK;
+}
+
+// Gauss-Jordan inverse with partial pivoting (K is small: 2 x chunks).
+bool invert(vector<double>& A, int K) {
+    vector<double> I(size_t(K) * K, 0.0);
+    for (int i = 0; i < K; ++i) I[size_t(i) * K + i] = 1.0;
+    for (int col = 0; col < K; ++col) {
+        int piv = col;
+        for (int i = col + 1; i < K; ++i)
+            if (std::fabs(A[size_t(i) * K + col]) > std::fabs(A[size_t(piv) * K + col])) piv = i;
+        double pv = A[size_t(piv) * K + col];
+        if (!(std::fabs(pv) > 1e-300)) return false;
+        if (piv != col)
+            for (int j = 0; j < K; ++j) {
+                std::swap(A[size_t(piv) * K + j], A[size_t(col) * K + j]);
+                std::swap(I[size_t(piv) * K + j], I[size_t(col) * K + j]);
+            }
+        double inv = 1.0 / pv;
+        for (int j = 0; j < K; ++j) {
+            A[size_t(col) * K + j] *= inv;
+            I[size_t(col) * K + j] *= inv;
+        }
+        for (int i = 0; i < K; ++i) {
+            if (i == col) continue;
+            double fct = A[size_t(i) * K + col];
+            if (fct == 0.0) continue;
+            for (int j = 0; j < K; ++j) {
+                A[size_t(i) * K + j] -= fct * A[size_t(col) * K + j];
+                I[size_t(i) * K + j] -= fct * I[size_t(col) * K + j];
+            }
+        }
+    }
+    A.swap(I);
+    return true;
+}
+
+struct Global {
+    vector<double> a, b, c;   // effective bands (system.py:57-71)
+    vector<double> lower, upper;
+    vector<double> st;        // n x 5
+    int n;
+    bool periodic;
+};
+
+// Coupling of global row j to row j-1 / j+1 with the open corners zeroed.
+double A_of(const Global& g, int j) { return g.a[j]; }
+double C_of(const Global& g, int j) { return g.c[j]; }
+
+// local_slice (distributed.py:119-133) for rank k.
+void local_slice(const Global& g, const vector<int>& sizes, const vector<int>& offs, int k,
+                 vector<double>& a, vector<double>& b, vector<double>& c) {
+    int off = offs[k], m = sizes[k];
+    a.assign(g.a.begin() + off, g.a.begin() + off + m);
+    b.assign(g.b.begin() + off, g.b.begin() + off + m);
+    c.assign(g.c.begin() + off, g.c.begin() + off + m);
+    if (k == 0) a[0] = g.periodic ? g.lower[0] : 0.0;
+    if (k == int(sizes.size()) - 1) c[m - 1] = g.periodic ? g.upper[g.n - 1] : 0.0;
+}
+
+template <typename T>
+int upload(tds_plan* p, T** dst, const T* src, size_t count) {
+    void* ptr = nullptr;
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = sizeof(T);
+    int rc = tds::cuda_check(cudaMalloc(&ptr, bytes), "cudaMalloc(plan)");
+    if (rc) return rc;
+    p->allocs.push_back(ptr);
+    if (count) {
+        rc = tds::cuda_check(cudaMemcpy(ptr, src, count * sizeof(T), cudaMemcpyHostToDevice),
+                             "cudaMemcpy(plan)");
+        if (rc) return rc;
+    }
+    *dst = static_cast<T*>(ptr);
+    return TDS_OK;
+}
+
+// Rows of chunk k of the block are [s, s+M). Builds the chunk-local Alg. 5
+// tables (undropped couplings kept: they enter the exact reduced system).
+struct ChunkSet {
+    int M, C;
+    vector<tds_rank_coeffs> co;
+};
+
+int build_chunks(const Global& g, int block_off, int block_rows, int M, ChunkSet& cs) {
+    cs.M = M;
+    cs.C = block_rows / M;
+    cs.co.resize(cs.C);
+    vector<double> a(M), b(M), c(M);
+    for (int k = 0; k < cs.C; ++k) {
+        int s = block_off + k * M;
+        for (int i = 0; i < M; ++i) {
+            a[i] = A_of(g, s + i);
+            b[i] = g.b[s + i];
+            c[i] = C_of(g, s + i);
+        }
+        int rc = preprocess_block(a.data(), b.data(), c.data(), M, cs.co[k], -1);
+        if (rc) return rc;
+    }
+    return TDS_OK;
+}
+
+// Reduced system of chunk boundary unknowns [F_0, L_0, F_1, L_1, ...] over
+// chunks [k0, k1]; `wrap` closes it periodically, `cut_lo/hi` drops the
+// couplings leaving the range (rank-external).
+vector<double> reduced(const ChunkSet& cs, int k0, int k1, bool wrap) {
+    int Cr = k1 - k0 + 1, K = 2 * Cr;
+    vector<double> R(size_t(K) * K, 0.0);
+    int M = cs.M;
+    for (int kk = 0; kk < Cr; ++kk) {
+        const auto& co = cs.co[k0 + kk];
+        int F = 2 * kk, L = 2 * kk + 1;
+        // row F: F_k + sa_0 L_{k-1} + sc_0 L_k = y
+        R[size_t(F) * K + F] += 1.0;
+        R[size_t(F) * K + L] += co.drop_first;          // sc[0] before zeroing
+        if (kk > 0) R[size_t(F) * K + (2 * kk - 1)] += co.sa[0];
+        else if (wrap) R[size_t(F) * K + (K - 1)] += co.sa[0];
+        // row L: L_k + sa_{M-1} F_k + sc_{M-1} F_{k+1} = y
+        R[size_t(L) * K + L] += 1.0;
+        R[size_t(L) * K + F] += co.drop_last;           // sa[M-1] before zeroing
+        if (kk < Cr - 1) R[size_t(L) * K + (2 * kk + 2)] += co.sc[M - 1];
+        else if (wrap) R[size_t(L) * K + 0] += co.sc[M - 1];
+    }
+    return R;
+}
+
+int pick_chunk(const vector<int>& blocks, int flags) {
+    if (flags & (TDS_FLAG_STRICT | TDS_FLAG_STAGED)) return 0;
+    for (int M : {32, 16}) {
+        bool ok = true;
+        for (int m : blocks)
+            if (m % M != 0 || m / M > tds::MAX_CHUNKS) ok = false;
+        if (ok) return M;
+    }
+    return 0;
+}
+
+}  // namespace
+
+extern "C" int tds_plan_destroy(tds_plan* p) {
+    if (!p) return TDS_OK;
+    for (void* ptr : p->allocs) cudaFree(ptr);
+    delete p;
+    return TDS_OK;
+}
+
+namespace {
+
+// Per-rank maps over the chunks [k0, k1] of one rank: g0/g1 give the rank's
+// Alg. 6 boundary rows d[0], d[m-1] (exact elimination of the rank's rows with
+// zero externals, plus the two couplings Alg. 5 folds into them before
+// dropping); Hpin maps the chunk reduced rhs with F_0 := u_start and
+// L_last := u_end to every chunk boundary value of the rank.
+struct RankMap {
+    int k0 = 0, k1 = 0, K = 0;
+    vector<double> g0, g1, Hpin;
+};
+
+int rank_map(const ChunkSet& cs, int k0, int k1, double drop_first, double drop_last,
+             RankMap& rm) {
+    rm.k0 = k0;
+    rm.k1 = k1;
+    rm.K = 2 * (k1 - k0 + 1);
+    const int KK = rm.K;
+    vector<double> Ro = reduced(cs, k0, k1, false);
+    vector<double> Rp = Ro;
+    if (!invert(Ro, KK)) return set_err(TDS_ERR_SINGULAR_PIVOT, "singular chunk reduced system");
+    auto pin = [&](vector<double>& A) {
+        for (int j = 0; j < KK; ++j) {
+            A[j] = (j == 0) ? 1.0 : 0.0;
+            A[size_t(KK - 1) * KK + j] = (j == KK - 1) ? 1.0 : 0.0;
+        }
+    };
+    pin(Rp);
+    if (!invert(Rp, KK)) return set_err(TDS_ERR_SINGULAR_PIVOT, "singular chunk reduced system");
+    pin(Rp);   // the pinned rows of the inverse are exact unit rows
+    rm.Hpin = Rp;
+    rm.g0.assign(KK, 0.0);
+    rm.g1.assign(KK, 0.0);
+    for (int q = 0; q < KK; ++q) {
+        double first = Ro[q], last = Ro[size_t(KK - 1) * KK + q];
+        rm.g0[q] = first + drop_first * last;
+        rm.g1[q] = last + drop_last * first;
+    }
+    return TDS_OK;
+}
+
+// Fast-path per-row table of the block (stencil, chunk Alg. 5 tables) and the
+// uniform-table detection.
+int fast_tables(tds_plan* p, const Global& g, int M, ChunkSet& cs) {
+    int rc = build_chunks(g, p->block_off, p->block_rows, M, cs);
+    if (rc) return rc;
+    p->path = TDS_PATH_FAST;
+    p->M = M;
+    p->C = cs.C;
+    p->K = 2 * cs.C;
+    vector<double> tab(size_t(p->block_rows) * tds::NCOEF);
+    for (int k = 0; k < cs.C; ++k)
+        for (int i = 0; i < M; ++i) {
+            int row = k * M + i;
+            double* t = &tab[size_t(row) * tds::NCOEF];
+            for (int o = 0; o < 5; ++o) t[o] = g.st[size_t(p->block_off + row) * 5 + o];
+            const auto& co = cs.co[k];
+            t[5] = co.f[i];
+            t[6] = co.r[i];
+            t[7] = co.w[i];
+            // interior couplings to the chunk's own first / last unknowns
+            t[8] = (i == 0 || i == M - 1) ? 0.0 : co.sa[i];
+            t[9] = (i == 0 || i == M - 1) ? 0.0 : co.sc[i];
+        }
+    bool uni = M <= tds::MMAX_UNIFORM;
+    for (int row = 0; row < p->block_rows && uni; ++row) {
+        const double* t = &tab[size_t(row) * tds::NCOEF];
+        const double* t0 = &tab[size_t(row % M) * tds::NCOEF];
+        if (std::memcmp(t + 5, t0 + 5, 5 * sizeof(double)) != 0) uni = false;
+        if (std::memcmp(t, &tab[0], 5 * sizeof(double)) != 0) uni = false;
+    }
+    p->uniform = uni;
+    if (uni) {
+        for (int o = 0; o < 5; ++o) p->ut.st[o] = tab[o];
+        for (int i = 0; i < M; ++i) {
+            const double* t = &tab[size_t(i) * tds::NCOEF];
+            p->ut.f[i] = t[5];
+            p->ut.r[i] = t[6];
+            p->ut.w[i] = t[7];
+            p->ut.sa[i] = t[8];
+            p->ut.sc[i] = t[9];
+        }
+    }
+    return upload(p, &p->d_tab, tab.data(), tab.size());
+}
+
+int upload_H(tds_plan* p, const vector<double>& H, const vector<double>& gv) {
+    const int C = p->C, K = p->K;
+    vector<double2> Hp(size_t(C) * K);
+    for (int k = 0; k < C; ++k)
+        for (int q = 0; q < K; ++q)
+            Hp[size_t(k) * K + q] =
+                make_double2(H[size_t(2 * k) * K + q], H[size_t(2 * k + 1) * K + q]);
+    int rc = upload(p, &p->d_Hp, Hp.data(), Hp.size());
+    if (rc) return rc;
+    return upload(p, &p->d_g, gv.data(), gv.size());
+}
+
+// Staged tables of a set of rank blocks (rank-level DistD2 coefficients,
+// dropped couplings zeroed as the reference does).
+int staged_rank_tables(tds_plan* p, const vector<const tds_rank_coeffs*>& cos,
+                       const vector<int>& boff, const vector<int>& bsize,
+                       const vector<double>& bconst) {
+    vector<double> w, f, r, sa, sc;
+    for (const auto* co : cos) {
+        w.insert(w.end(), co->w.begin(), co->w.end());
+        f.insert(f.end(), co->f.begin(), co->f.end());
+        r.insert(r.end(), co->r.begin(), co->r.end());
+        sa.insert(sa.end(), co->sa.begin(), co->sa.end());
+        sc.insert(sc.end(), co->sc.begin(), co->sc.end());
+    }
+    p->nb = int(cos.size());
+    int rc;
+    if ((rc = upload(p, &p->d_w, w.data(), w.size()))) return rc;
+    if ((rc = upload(p, &p->d_f, f.data(), f.size()))) return rc;
+    if ((rc = upload(p, &p->d_r, r.data(), r.size()))) return rc;
+    if ((rc = upload(p, &p->d_sa, sa.data(), sa.size()))) return rc;
+    if ((rc = upload(p, &p->d_sc, sc.data(), sc.size()))) return rc;
+    if ((rc = upload(p, &p->d_boff, boff.data(), boff.size()))) return rc;
+    if ((rc = upload(p, &p->d_bsize, bsize.data(), bsize.size()))) return rc;
+    return upload(p, &p->d_bconst, bconst.data(), bconst.size());
+}
+
+Global make_global(const double* lower, const double* diag, const double* upper, bool periodic,
+                   const double* stencil, int n) {
+    Global g;
+    g.n = n;
+    g.periodic = periodic;
+    g.lower.assign(lower, lower + n);
+    g.upper.assign(upper, upper + n);
+    g.a = g.lower;
+    g.c = g.upper;
+    g.b.assign(diag, diag + n);
+    if (!g.periodic) {
+        g.a[0] = 0.0;
+        g.c[n - 1] = 0.0;
+    }
+    g.st.assign(size_t(n) * 5, 0.0);
+    for (int j = 0; j < n; ++j) {
+        if (stencil)
+            for (int o = 0; o < 5; ++o) g.st[size_t(j) * 5 + o] = stencil[size_t(j) * 5 + o];
+        else
+            g.st[size_t(j) * 5 + 2] = 1.0;   // identity_stencil, distributed.py:112-116
+    }
+    return g;
+}
+
+double margin_of(const Global& g) {
+    double margin = 1e300;
+    for (int j = 0; j < g.n; ++j)
+        margin = std::fmin(margin, std::fabs(g.b[j]) - std::fabs(g.a[j]) - std::fabs(g.c[j]));
+    return margin;
+}
+
+// One rank's block from rank-local data only (the reference's per-rank view:
+// local_slice bands with the external couplings in a[0] / c[m-1], the local
+// stencil rows, and the two cached neighbour couplings of D16).
+int build_local(tds_plan* p, const Global& loc, int has_prev, int has_next, double prev_sc_last,
+                double next_sa_first, int rank_for_errors) {
+    const int m = loc.n;
+    p->rc.resize(1);
+    tds_rank_coeffs& co = p->rc[0];
+    int rc = preprocess_block(loc.a.data(), loc.b.data(), loc.c.data(), m, co, rank_for_errors);
+    if (rc) return rc;
+    co.sc[0] = 0.0;
+    co.sa[m - 1] = 0.0;
+    p->max_dropped = std::fmax(std::fabs(co.drop_first), std::fabs(co.drop_last));
+    p->has_prev = has_prev;
+    p->has_next = has_next;
+    p->sa_first = co.sa[0];
+    p->sc_last = co.sc[m - 1];
+    p->prev_sc_last = has_prev ? prev_sc_last : 0.0;
+    p->next_sa_first = has_next ? next_sa_first : 0.0;
+    p->det_prev = has_prev ? 1.0 - p->prev_sc_last * p->sa_first : 1.0;
+    p->det_next = has_next ? 1.0 - p->sc_last * p->next_sa_first : 1.0;
+    for (double det : {p->det_prev, p->det_next})
+        if (std::fabs(det) < tds::PAIR_DET_FLOOR)
+            return set_err(TDS_ERR_SINGULAR_PAIR, fmt("boundary determinant %.3e", det),
+                           rank_for_errors);
+    int M = pick_chunk({m}, p->flags);
+    if (M > 0) {
+        ChunkSet cs;
+        if ((rc = fast_tables(p, loc, M, cs))) return rc;
+        RankMap rm;
+        if ((rc = rank_map(cs, 0, cs.C - 1, co.drop_first, co.drop_last, rm))) return rc;
+        vector<double> gv(size_t(2) * rm.K);
+        std::copy(rm.g0.begin(), rm.g0.end(), gv.begin());
+        std::copy(rm.g1.begin(), rm.g1.end(), gv.begin() + rm.K);
+        return upload_H(p, rm.Hpin, gv);
+    }
+    p->path = TDS_PATH_STAGED;
+    if ((rc = upload(p, &p->d_st, loc.st.data(), loc.st.size()))) return rc;
+    return staged_rank_tables(p, {&co}, {0}, {m},
+                              {co.sa[0], co.sc[m - 1], p->det_prev, p->det_next,
+                               double(has_prev), double(has_next)});
+}
+
+tds_plan* new_plan(int n, bool periodic, int P, int rank, int flags) {
+    auto* p = new tds_plan();
+    p->n = n;
+    p->periodic = periodic;
+    p->P = P;
+    p->rank = rank;
+    p->flags = flags;
+    return p;
+}
+
+}  // namespace
+
+extern "C" int tds_plan_create_local(const double* a, const double* b, const double* c,
+                                     const double* stencil, int m, int has_prev, int has_next,
+                                     double prev_sc_last, double next_sa_first, int flags,
+                                     tds_plan** out) {
+    if (!out) return set_err(TDS_ERR_INVALID, "null plan output");
+    *out = nullptr;
+    if (!a || !b || !c) return set_err(TDS_ERR_INVALID, "null band pointer");
+    if (m < 4) return set_err(TDS_ERR_INVALID, "local block needs at least 4 rows");
+    for (int j = 0; j < m; ++j)
+        if (b[j] == 0.0) return set_err(TDS_ERR_INVALID, "diagonal entries must be nonzero");
+    // bands are taken as given: a[0] / c[m-1] are the external couplings
+    Global loc = make_global(a, b, c, true, stencil, m);
+    loc.periodic = false;
+    tds_plan* p = new_plan(m, false, 2, 0, flags);
+    p->block_off = 0;
+    p->block_rows = m;
+    p->sizes = {m};
+    p->offs = {0};
+    p->margin = margin_of(loc);
+    int rc = build_local(p, loc, has_prev != 0, has_next != 0, prev_sc_last, next_sa_first, -1);
+    if (rc) {
+        tds_plan_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return TDS_OK;
+}
+
+extern "C" int tds_plan_create(const double* lower, const double* diag, const double* upper,
+                               int periodic, const double* stencil, int n, const int* sizes_in,
+                               int P, int rank, int flags, tds_plan** out) {
+    if (!out) return set_err(TDS_ERR_INVALID, "null plan output");
+    *out = nullptr;
+    if (!lower || !diag || !upper) return set_err(TDS_ERR_INVALID, "null band pointer");
+    if (n < 3) return set_err(TDS_ERR_INVALID, "system size must be at least 3");
+    if (P < 1 || !sizes_in) return set_err(TDS_ERR_INVALID, "partition needs at least one subdomain");
+    if (rank < -1 || rank >= P) return set_err(TDS_ERR_INVALID, "rank out of range");
+    if (rank >= 0 && P < 2) return set_err(TDS_ERR_INVALID, "per-rank plans need P > 1");
+    vector<int> sizes(sizes_in, sizes_in + P), offs(P, 0);
+    long long tot = 0;
+    for (int k = 0; k < P; ++k) {
+        if (sizes[k] < 4) return set_err(TDS_ERR_INVALID, "every subdomain needs at least 4 rows");
+        offs[k] = int(tot);
+        tot += sizes[k];
+    }
+    if (tot != n)
+        return set_err(TDS_ERR_INVALID, "partition covers " + std::to_string(tot) +
+                                            " positions, field has " + std::to_string(n));
+    for (int j = 0; j < n; ++j)
+        if (diag[j] == 0.0) return set_err(TDS_ERR_INVALID, "diagonal entries must be nonzero");
+
+    const Global g = make_global(lower, diag, upper, periodic != 0, stencil, n);
+    tds_plan* p = new_plan(n, g.periodic, P, rank, flags);
+    p->sizes = sizes;
+    p->offs = offs;
+    p->margin = margin_of(g);
+    int rc = TDS_OK;
+    auto fail = [&](int code) {
+        tds_plan_destroy(p);
+        return code;
+    };
+
+    // rank-level Alg. 5 of every rank (needed for the pair couplings)
+    vector<tds_rank_coeffs> rcs(P > 1 ? P : 0);
+    vector<double> a, b, c;
+    for (int k = 0; k < P && P > 1; ++k) {
+        local_slice(g, sizes, offs, k, a, b, c);
+        if ((rc = preprocess_block(a.data(), b.data(), c.data(), sizes[k], rcs[k], k)))
+            return fail(rc);
+        p->max_dropped = std::fmax(p->max_dropped, std::fmax(std::fabs(rcs[k].drop_first),
+                                                             std::fabs(rcs[k].drop_last)));
+    }
+    for (auto& co : rcs) {   // the reference zeroes the dropped pair
+        co.sc[0] = 0.0;
+        co.sa.back() = 0.0;
+    }
+    auto has_prev = [&](int k) { return P > 1 && (k > 0 || g.periodic); };
+    auto has_next = [&](int k) { return P > 1 && (k < P - 1 || g.periodic); };
+    auto prev_of = [&](int k) { return (k - 1 + P) % P; };
+    auto next_of = [&](int k) { return (k + 1) % P; };
+
+    if (rank >= 0) {
+        // this device owns rank `rank`: build it from its local view only
+        local_slice(g, sizes, offs, rank, a, b, c);
+        const int m = sizes[rank];
+        vector<double> st(g.st.begin() + size_t(offs[rank]) * 5,
+                          g.st.begin() + size_t(offs[rank] + m) * 5);
+        Global loc = make_global(a.data(), b.data(), c.data(), true, st.data(), m);
+        loc.periodic = false;
+        p->block_off = 0;
+        p->block_rows = m;
+        double psc = has_prev(rank) ? rcs[prev_of(rank)].sc.back() : 0.0;
+        double nsa = has_next(rank) ? rcs[next_of(rank)].sa[0] : 0.0;
+        double md = p->max_dropped;
+        if ((rc = build_local(p, loc, has_prev(rank), has_next(rank), psc, nsa, rank)))
+            return fail(rc);
+        p->max_dropped = md;
+        p->rank = rank;
+        p->P = P;
+        p->rc = rcs;
+        *out = p;
+        return TDS_OK;
+    }
+
+    p->block_off = 0;
+    p->block_rows = n;
+    p->rc = rcs;
+    vector<double> det_prev(P, 1.0), det_next(P, 1.0);
+    for (int k = 0; k < P && P > 1; ++k) {
+        if (!has_next(k)) continue;
+        int q = next_of(k);
+        double det = 1.0 - rcs[k].sc.back() * rcs[q].sa[0];
+        if (std::fabs(det) < tds::PAIR_DET_FLOOR)
+            return fail(set_err(TDS_ERR_SINGULAR_PAIR, fmt("boundary determinant %.3e", det), k));
+        det_next[k] = det;
+        det_prev[q] = det;
+    }
+
+    vector<int> blocks = (P == 1) ? vector<int>{n} : sizes;
+    const int M = pick_chunk(blocks, flags);
+    if (M > 0) {
+        // ---------------------------- fast path ------------------------------
+        ChunkSet cs;
+        if ((rc = fast_tables(p, g, M, cs))) return fail(rc);
+        const int K = p->K;
+        vector<double> H(size_t(K) * K, 0.0), gv(size_t(2) * K, 0.0);
+        if (P == 1) {
+            H = reduced(cs, 0, cs.C - 1, g.periodic);
+            if (!invert(H, K))
+                return fail(set_err(TDS_ERR_SINGULAR_PIVOT, "singular chunk reduced system"));
+        } else {
+            // emulated ranks: compose g -> 2x2 pairs -> pinned solves into one
+            // K x K linear map of the chunk reduced rhs
+            vector<RankMap> maps(P);
+            for (int k = 0; k < P; ++k)
+                if ((rc = rank_map(cs, offs[k] / M, (offs[k] + sizes[k]) / M - 1,
+                                   rcs[k].drop_first, rcs[k].drop_last, maps[k])))
+                    return fail(rc);
+            vector<double> Y(K), d0(P), dl(P), us(P), ue(P), Yp;
+            for (int q = 0; q < K; ++q) {
+                std::fill(Y.begin(), Y.end(), 0.0);
+                Y[q] = 1.0;
+                for (int k = 0; k < P; ++k) {
+                    const auto& rm = maps[k];
+                    double s0 = 0, s1 = 0;
+                    for (int j = 0; j < rm.K; ++j) {
+                        s0 += rm.g0[j] * Y[2 * rm.k0 + j];
+                        s1 += rm.g1[j] * Y[2 * rm.k0 + j];
+                    }
+                    d0[k] = s0;
+                    dl[k] = s1;
+                }
+                for (int k = 0; k < P; ++k) {
+                    us[k] = has_prev(k) ? (d0[k] - rcs[k].sa[0] * dl[prev_of(k)]) / det_prev[k]
+                                        : d0[k];
+                    ue[k] = has_next(k)
+                                ? (dl[k] - rcs[k].sc.back() * d0[next_of(k)]) / det_next[k]
+                                : dl[k];
+                }
+                for (int k = 0; k < P; ++k) {
+                    const auto& rm = maps[k];
+                    Yp.assign(Y.begin() + 2 * rm.k0, Y.begin() + 2 * rm.k0 + rm.K);
+                    Yp[0] = us[k];
+                    Yp[rm.K - 1] = ue[k];
+                    for (int i = 0; i < rm.K; ++i) {
+                        double s = 0;
+                        for (int j = 0; j < rm.K; ++j) s += rm.Hpin[size_t(i) * rm.K + j] * Yp[j];
+                        H[size_t(2 * rm.k0 + i) * K + q] = s;
+                    }
+                }
+            }
+        }
+        if ((rc = upload_H(p, H, gv))) return fail(rc);
+        *out = p;
+        return TDS_OK;
+    }
+
+    // --------------------------- staged path ---------------------------------
+    p->path = TDS_PATH_STAGED;
+    if ((rc = upload(p, &p->d_st, g.st.data(), g.st.size()))) return fail(rc);
+    if (P > 1) {
+        vector<const tds_rank_coeffs*> cos;
+        vector<double> bconst;
+        for (int k = 0; k < P; ++k) {
+            cos.push_back(&rcs[k]);
+            bconst.insert(bconst.end(), {rcs[k].sa[0], rcs[k].sc.back(), det_prev[k], det_next[k],
+                                         double(has_prev(k)), double(has_next(k))});
+        }
+        p->rc = rcs;
+        if ((rc = staged_rank_tables(p, cos, offs, sizes, bconst))) return fail(rc);
+        *out = p;
+        return TDS_OK;
+    }
+    // P == 1: thomas_solve / periodic_thomas_solve multipliers (serial.py:26-90)
+    vector<double> la = g.lower, lb = g.b, lc = g.upper;
+    vector<double> w(n, 0.0), cp(n, 0.0), z;
+    double gamma = 0.0;
+    if (g.periodic) {
+        gamma = -lb[0];
+        lb[0] = lb[0] - gamma;
+        lb[n - 1] = lb[n - 1] - lc[n - 1] * la[0] / gamma;
+    }
+    cp[0] = lc[0] / lb[0];
+    for (int i = 1; i < n; ++i) {
+        double den = lb[i] - la[i] * cp[i - 1];
+        if (std::fabs(den) <= tds::PIVOT_FLOOR)
+            return fail(set_err(TDS_ERR_SINGULAR_PIVOT,
+                                fmt("pivot %.3e at row ", den) + std::to_string(i + 1)));
+        w[i] = 1.0 / den;
+        cp[i] = lc[i] * w[i];
+    }
+    p->th_b0 = lb[0];
+    if (g.periodic) {
+        z.assign(n, 0.0);
+        z[0] = gamma;
+        z[n - 1] = lc[n - 1];
+        z[0] /= lb[0];
+        for (int i = 1; i < n; ++i) {
+            z[i] -= la[i] * z[i - 1];
+            z[i] *= w[i];
+        }
+        for (int i = n - 2; i >= 0; --i) z[i] -= cp[i] * z[i + 1];
+        double ql = la[0] / gamma;
+        double den = 1.0 + 1.0 * z[0] + ql * z[n - 1];
+        if (std::fabs(den) <= tds::PIVOT_FLOOR)
+            return fail(set_err(TDS_ERR_SINGULAR_CORRECTION, fmt("correction denominator %.3e", den)));
+        p->th_qlast = ql;
+        p->th_den = den;
+        if ((rc = upload(p, &p->d_thz, z.data(), z.size()))) return fail(rc);
+    }
+    if ((rc = upload(p, &p->d_tha, la.data(), la.size()))) return fail(rc);
+    if ((rc = upload(p, &p->d_thw, w.data(), w.size()))) return fail(rc);
+    if ((rc = upload(p, &p->d_thcp, cp.data(), cp.size()))) return fail(rc);
+    *out = p;
+    return TDS_OK;
+}
+
+extern "C" int tds_plan_query(const tds_plan* p, tds_plan_info* info) {
+    if (!p || !info) return set_err(TDS_ERR_INVALID, "null argument");
+    info->n = p->n;
+    info->rank_count = p->P;
+    info->rank = p->rank;
+    info->block_rows = p->block_rows;
+    info->path = p->path;
+    info->strict = (p->flags & TDS_FLAG_STRICT) ? 1 : 0;
+    info->chunk_rows = p->M;
+    info->chunks = p->C;
+    info->uniform = p->uniform ? 1 : 0;
+    info->periodic = p->periodic;
+    info->max_dropped = p->max_dropped;
+    info->dominance_margin = p->margin;
+    return TDS_OK;
+}
+
+extern "C" int tds_plan_rank_coeffs(const tds_plan* p, int k, double* sa, double* sc, double* w,
+                                    double* f, double* r, double* dropped) {
+    if (!p || k < 0 || k >= p->P || p->P < 2)
+        return set_err(TDS_ERR_INVALID, "rank coefficients exist for P > 1 plans only");
+    const auto& co = p->rc[k];
+    size_t m = co.sa.size();
+    std::memcpy(sa, co.sa.data(), m * sizeof(double));
+    std::memcpy(sc, co.sc.data(), m * sizeof(double));
+    std::memcpy(w, co.w.data(), m * sizeof(double));
+    std::memcpy(f, co.f.data(), m * sizeof(double));
+    std::memcpy(r, co.r.data(), m * sizeof(double));
+    dropped[0] = co.drop_first;
+    dropped[1] = co.drop_last;
+    return TDS_OK;
+}
+
+extern "C" int tds_preprocess(const double* a, const double* b, const double* c, int m,
+                              double* sa, double* sc, double* w, double* f, double* r,
+                              double* dropped) {
+    if (!a || !b || !c || !sa || !sc || !w || !f || !r || !dropped)
+        return set_err(TDS_ERR_INVALID, "null argument");
+    tds_rank_coeffs co;
+    int rc = preprocess_block(a, b, c, m, co, -1);
+    if (rc) return rc;
+    co.sc[0] = 0.0;
+    co.sa[m - 1] = 0.0;
+    std::memcpy(sa, co.sa.data(), size_t(m) * sizeof(double));
+    std::memcpy(sc, co.sc.data(), size_t(m) * sizeof(double));
+    std::memcpy(w, co.w.data(), size_t(m) * sizeof(double));
+    std::memcpy(f, co.f.data(), size_t(m) * sizeof(double));
+    std::memcpy(r, co.r.data(), size_t(m) * sizeof(double));
+    dropped[0] = co.drop_first;
+    dropped[1] = co.drop_last;
+    return TDS_OK;
+}

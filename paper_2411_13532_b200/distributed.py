@@ -1,0 +1,409 @@
+"""DistD2 operator API, B200-native: same names, arguments, return types and
+errors as the reference's distributed.py (/root/reference/pkg/src/tds/
+distributed.py:1-449), computed by the sm_100a kernels in `_lib`.
+
+Field arguments may be NumPy arrays (host; copied to the current CUDA device
+and back, like a drop-in for the reference) or CUDA torch tensors (device
+resident, result returned on the device). There is no CPU path: every call
+below that touches field data launches a kernel from libtds_b200.so.
+
+Arithmetic modes (keyword-only `arithmetic=`):
+  "fast"   -- default. Single-pass chunked kernel; FMA; exact reduced system
+              between chunks; the reference's truncation only at rank
+              boundaries. Agrees with the reference to ~1e-15 relative.
+  "strict" -- staged kernels in the reference's operation order, no FMA;
+              bit-identical to the reference on the same inputs.
+"""
+
+import ctypes
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import NotDominantWarning, SingularPair
+from .system import SubdomainPartition, TridiagonalSystem, is_diagonally_dominant
+
+HALO_DEPTH = 2
+PIVOT_FLOOR = 1e-300
+PAIR_DET_FLOOR = 1e-12
+
+
+# ------------------------------------------------------------------ types
+
+@dataclass(frozen=True)
+class DistCoeffs:
+    """Preprocessed per-row coefficients of one subdomain (distributed.py:43-68)."""
+
+    s_a: np.ndarray
+    s_c: np.ndarray
+    w: np.ndarray
+    f: np.ndarray
+    r: np.ndarray
+    n_loc: int
+    cyclic_global: bool
+    position: str
+    dropped_first: float
+    dropped_last: float
+
+    @property
+    def max_dropped(self):
+        return max(self.dropped_first, self.dropped_last)
+
+
+@dataclass(frozen=True)
+class StencilCoeffs:
+    """Per-row width-5 RHS weights, offsets -2..+2 (distributed.py:71-86)."""
+
+    c: np.ndarray
+    halo_depth: int = HALO_DEPTH
+
+    def __post_init__(self):
+        arr = np.ascontiguousarray(self.c, dtype=np.float64)
+        if arr.ndim != 2 or arr.shape[1] != 5:
+            raise ValueError(f"stencil must be (n, 5), got {arr.shape}")
+        object.__setattr__(self, "c", arr)
+
+    @property
+    def n(self):
+        return self.c.shape[0]
+
+
+@dataclass(frozen=True)
+class BoundaryPair:
+    """Inputs of one cross-boundary 2x2 solve (distributed.py:89-101)."""
+
+    d_last_local: object
+    d_first_remote: object
+    s_c_last: float
+    s_a_first_remote: float
+
+
+@dataclass(frozen=True)
+class PairCoeffs:
+    """Cached neighbour couplings, exchanged once (distributed.py:104-109)."""
+
+    prev_s_c_last: float | None
+    next_s_a_first: float | None
+
+
+def identity_stencil(n):
+    c = np.zeros((n, 5))
+    c[:, 2] = 1.0
+    return StencilCoeffs(c)
+
+
+def local_slice(sys, part, rank_id):
+    """Rank `rank_id`'s block with its external couplings (distributed.py:119-133)."""
+    off = part.offsets()[rank_id]
+    m = part.local_sizes[rank_id]
+    a = sys.effective_lower()[off:off + m].copy()
+    c = sys.effective_upper()[off:off + m].copy()
+    if rank_id == 0:
+        a[0] = sys.lower[0] if sys.periodic else 0.0
+    if rank_id == part.rank_count - 1:
+        c[-1] = sys.upper[-1] if sys.periodic else 0.0
+    return TridiagonalSystem(a, sys.diag[off:off + m].copy(), c, periodic=False)
+
+
+def rank_position(rank_id, rank_count):
+    if rank_id == 0:
+        return "first"
+    if rank_id == rank_count - 1:
+        return "last"
+    return "interior"
+
+
+def preprocess(local_sys, position, cyclic, pivot_floor=PIVOT_FLOOR, warn_not_dominant=True):
+    """Alg. 5 (distributed.py:144-199), computed by the native plan builder
+    (tds_preprocess) with the reference's rounding: bit-identical values."""
+    m = local_sys.n
+    if m < 4:
+        raise ValueError(f"local block needs at least 4 rows, got {m}")
+    if pivot_floor != PIVOT_FLOOR:
+        raise ValueError("the native plan builder uses the reference pivot floor 1e-300")
+    if warn_not_dominant and not is_diagonally_dominant(local_sys):
+        warnings.warn("local block is not strictly diagonally dominant",
+                      NotDominantWarning, stacklevel=2)
+    a, b, c = (N.f64(x) for x in (local_sys.lower, local_sys.diag, local_sys.upper))
+    out = [np.empty(m) for _ in range(5)]
+    dropped = np.empty(2)
+    N.check(N.lib().tds_preprocess(N.dptr(a), N.dptr(b), N.dptr(c), m,
+                                   *[N.dptr(o) for o in out], N.dptr(dropped)))
+    sa, sc, w, f, r = out
+    return DistCoeffs(sa, sc, w, f, r, m, bool(cyclic), position,
+                      abs(float(dropped[0])), abs(float(dropped[1])))
+
+
+# ------------------------------------------------------------- plumbing
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class _Field:
+    """A fp64 operand on the current CUDA device. Remembers where the caller's
+    data lives: NumPy array or CPU tensor (host: copied in, result copied
+    back; pinned CPU tensors copy asynchronously) or CUDA tensor (device)."""
+
+    def __init__(self, x):
+        torch = _torch()
+        if isinstance(x, torch.Tensor):
+            self.numpy = False
+            if x.is_cuda:
+                self.host = False
+                self.t = x.to(torch.float64).contiguous()
+                return
+            _need_cuda()
+            self.host = True
+            self.t = x.to(torch.float64).contiguous().to("cuda", non_blocking=x.is_pinned())
+        else:
+            _need_cuda()
+            self.host = True
+            self.numpy = True
+            arr = np.ascontiguousarray(x, dtype=np.float64)
+            self.t = torch.from_numpy(arr).to("cuda", non_blocking=False)
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.t.data_ptr())
+
+    def empty_like(self, shape=None):
+        torch = _torch()
+        return torch.empty(self.t.shape if shape is None else shape,
+                           dtype=torch.float64, device=self.t.device)
+
+    def give(self, t, out=None):
+        """Hand the result back where the input came from (into `out` if given)."""
+        torch = _torch()
+        if not self.host:
+            if out is not None:
+                out.copy_(t)
+                return out
+            return t
+        if out is not None:
+            out.copy_(t, non_blocking=bool(getattr(out, "is_pinned", lambda: False)()))
+            torch.cuda.current_stream().synchronize()
+            return out
+        if self.numpy:
+            return t.cpu().numpy()
+        return t.cpu()
+
+
+def _need_cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2411_13532_b200 needs a CUDA device; there is no CPU "
+                           "fallback")
+
+
+class Plan:
+    """Owns one native tds_plan (coefficient tables on one device)."""
+
+    def __init__(self, handle, rank_count, device):
+        self.handle = handle
+        self.rank_count = rank_count
+        self.device = device
+        info = N.PlanInfo()
+        N.check(N.lib().tds_plan_query(handle, ctypes.byref(info)))
+        self.info = info
+
+    @property
+    def path(self):
+        return "fast" if self.info.path == N.TDS_PATH_FAST else "staged"
+
+    def __del__(self):
+        try:
+            if self.handle:
+                N.lib().tds_plan_destroy(self.handle)
+                self.handle = None
+        except Exception:   # interpreter shutdown
+            pass
+
+    @classmethod
+    def create(cls, sys, stencil_c, sizes, rank=-1, flags=0):
+        torch = _torch()
+        lo, di, up = (N.f64(x) for x in (sys.lower, sys.diag, sys.upper))
+        st = None if stencil_c is None else N.f64(stencil_c)
+        sz = (ctypes.c_int * len(sizes))(*sizes)
+        h = ctypes.c_void_p()
+        N.check(N.lib().tds_plan_create(
+            N.dptr(lo), N.dptr(di), N.dptr(up), int(bool(sys.periodic)),
+            None if st is None else N.dptr(st), sys.n, sz, len(sizes), rank, flags,
+            ctypes.byref(h)), rank_count=len(sizes))
+        return cls(h, len(sizes), torch.cuda.current_device())
+
+    @classmethod
+    def create_local(cls, local_sys, stencil_c, has_prev, has_next, prev_sc_last,
+                     next_sa_first, flags=0):
+        torch = _torch()
+        a, b, c = (N.f64(x) for x in (local_sys.lower, local_sys.diag, local_sys.upper))
+        st = None if stencil_c is None else N.f64(stencil_c)
+        h = ctypes.c_void_p()
+        N.check(N.lib().tds_plan_create_local(
+            N.dptr(a), N.dptr(b), N.dptr(c), None if st is None else N.dptr(st), local_sys.n,
+            int(has_prev), int(has_next), float(prev_sc_last or 0.0),
+            float(next_sa_first or 0.0), flags, ctypes.byref(h)))
+        return cls(h, 2, torch.cuda.current_device())
+
+
+_PLAN_CACHE = {}
+_PLAN_CACHE_MAX = 32
+
+
+def _flags(arithmetic):
+    if arithmetic == "fast":
+        return 0
+    if arithmetic == "strict":
+        return N.TDS_FLAG_STRICT
+    if arithmetic == "staged":
+        return N.TDS_FLAG_STAGED
+    raise ValueError(f"arithmetic must be 'fast', 'strict' or 'staged', got {arithmetic!r}")
+
+
+def get_plan(sys, stencil, part, rank=-1, arithmetic="fast"):
+    """Cached plan for (operator, partition, rank, arithmetic, device)."""
+    torch = _torch()
+    st = None if stencil is None else stencil.c
+    key = (sys.lower.tobytes(), sys.diag.tobytes(), sys.upper.tobytes(), bool(sys.periodic),
+           None if st is None else st.tobytes(), part.local_sizes, rank, arithmetic,
+           torch.cuda.current_device())
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+        plan = Plan.create(sys, st, part.local_sizes, rank, _flags(arithmetic))
+        _PLAN_CACHE[key] = plan
+    return plan
+
+
+# ------------------------------------------------------------- operator
+
+def _audit_counts(part, periodic, groups, sz):
+    """Message accounting of the reference protocol (transport.py:66-80,
+    distributed.py:308-366): per directed edge one scalar share, one halo
+    (groups, 2, sz) and one boundary row (groups, sz) message."""
+    p = part.rank_count
+    edges = 2 * p if periodic else 2 * (p - 1)
+    msgs = 3 * edges
+    nbytes = edges * (8 + groups * HALO_DEPTH * sz * 8 + groups * sz * 8)
+    return msgs, nbytes
+
+
+def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
+               warn_not_dominant=True, audit=None, *, arithmetic="fast", stream=None,
+               out=None):
+    """Solve A u = stencil(field) over P subdomains (distributed.py:399-449).
+
+    field_values: (n_groups, n, sz) NumPy array or CUDA tensor. P=1 gives the
+    serial (periodic) Thomas result; P>1 the reference's DistD2 truncation at
+    the same subdomain boundaries (all ranks emulated on this GPU; for one
+    rank per GPU see `DistD2Rank`). Keyword extensions: `arithmetic`
+    ("fast" | "strict"), `stream` (torch.cuda.Stream), `out` (result buffer:
+    a CUDA tensor, or a pinned CPU tensor for host-resident pipelines)."""
+    shape = tuple(field_values.shape)
+    if len(shape) != 3:
+        raise ValueError(f"field must be (n_groups, n, sz), got {shape}")
+    groups, n, sz = shape
+    if part is None:
+        part = SubdomainPartition.balanced(n, 1 if rank_count is None else rank_count)
+    if part.n != n:
+        raise ValueError(f"partition covers {part.n} positions, field has {n}")
+    if stencil is not None and stencil.n != n:
+        raise ValueError(f"stencil has {stencil.n} rows, field has {n}")
+    if sys.n != n:
+        raise ValueError(f"system size {sys.n} does not match field positions {n}")
+    if part.rank_count > 1 and warn_not_dominant:
+        for k in range(part.rank_count):
+            if not is_diagonally_dominant(local_slice(sys, part, k)):
+                warnings.warn("local block is not strictly diagonally dominant",
+                              NotDominantWarning, stacklevel=2)
+    plan = get_plan(sys, stencil, part, -1, arithmetic)
+    fld = _Field(field_values)
+    res = out if (out is not None and not fld.host) else fld.empty_like()
+    N.check(N.lib().tds_solve(plan.handle, fld.ptr, ctypes.c_void_p(res.data_ptr()),
+                              groups, sz, _stream_handle(stream)), part.rank_count)
+    if audit is not None and part.rank_count > 1:
+        msgs, nbytes = _audit_counts(part, sys.periodic, groups, sz)
+        audit["rounds_per_rank"] = [2] * part.rank_count
+        audit["messages_sent"] = msgs
+        audit["bytes_sent"] = nbytes
+        audit["max_dropped"] = float(plan.info.max_dropped)
+    if out is not None and not fld.host:
+        return res
+    return fld.give(res, out)
+
+
+# ------------------------------------------------------ phase functions
+
+def _lanes_of(shape):
+    lanes = 1
+    for s in shape[1:]:
+        lanes *= s
+    return lanes
+
+
+def decouple_fused(u_ext, coeffs, stencil):
+    """Alg. 6 on a halo-extended block (m+4, ...) -> (m, ...), reference
+    arithmetic on the GPU (distributed.py:257-276)."""
+    m = coeffs.n_loc
+    if u_ext.shape[0] != m + 4:
+        raise ValueError(f"expected {m + 4} positions incl. halo, got {u_ext.shape[0]}")
+    fld = _Field(u_ext)
+    d = fld.empty_like((m,) + tuple(u_ext.shape[1:]))
+    st = N.f64(stencil.c[:m])
+    w, f, r = N.f64(coeffs.w), N.f64(coeffs.f), N.f64(coeffs.r)
+    N.check(N.lib().tds_decouple_fused(fld.ptr, N.dptr(st), N.dptr(w), N.dptr(f), N.dptr(r),
+                                       ctypes.c_void_p(d.data_ptr()), m,
+                                       _lanes_of(u_ext.shape), _stream_handle()))
+    return fld.give(d)
+
+
+def decouple_unfused(d_rhs, coeffs):
+    """Sweeps over an already-built RHS (distributed.py:242-254): Alg. 6 with
+    the identity stencil on a zero-padded block."""
+    torch = _torch()
+    m = coeffs.n_loc
+    fld = _Field(d_rhs)
+    pad = torch.zeros((m + 4,) + tuple(fld.t.shape[1:]), dtype=torch.float64,
+                      device=fld.t.device)
+    pad[2:m + 2] = fld.t
+    d = decouple_fused(pad, coeffs, identity_stencil(m))
+    return fld.give(d)
+
+
+def solve_boundary_pair(pair):
+    """Cramer solve of the 2x2 pair (distributed.py:279-293)."""
+    det = 1.0 - pair.s_c_last * pair.s_a_first_remote
+    if abs(det) < PAIR_DET_FLOOR:
+        raise SingularPair(f"boundary determinant {det:.3e}")
+    dl = _Field(pair.d_last_local)
+    df = _Field(pair.d_first_remote)
+    ul, uf = dl.empty_like(), dl.empty_like()
+    N.check(N.lib().tds_boundary_pair(dl.ptr, df.ptr, float(pair.s_c_last),
+                                      float(pair.s_a_first_remote),
+                                      ctypes.c_void_p(ul.data_ptr()),
+                                      ctypes.c_void_p(uf.data_ptr()), dl.t.numel(),
+                                      _stream_handle()))
+    return dl.give(ul), dl.give(uf)
+
+
+def substitute(d, coeffs, u_start, u_end):
+    """Alg. 7 (distributed.py:296-305), reference arithmetic on the GPU."""
+    m = coeffs.n_loc
+    fd = _Field(d)
+    us, ue = _Field(u_start), _Field(u_end)
+    out = fd.empty_like()
+    sa, sc = N.f64(coeffs.s_a), N.f64(coeffs.s_c)
+    N.check(N.lib().tds_substitute(fd.ptr, N.dptr(sa), N.dptr(sc), us.ptr, ue.ptr,
+                                   ctypes.c_void_p(out.data_ptr()), m, _lanes_of(d.shape),
+                                   _stream_handle()))
+    return fd.give(out)
