@@ -145,6 +145,17 @@ def run_single(args, torch):
             if ev is not None:
                 ev[d][1].record(stream)
 
+    # context: a plain device copy of one field (same bytes moved as one solve)
+    copy_ms = []
+    for _ in range(12):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        outs["x"].copy_(fields["x"])
+        b.record(stream)
+        torch.cuda.synchronize()
+        copy_ms.append(a.elapsed_time(b))
+    copy_gbs = 2 * fields["x"].numel() * 8 / (min(copy_ms[2:]) * 1e-3) / 1e9
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -188,6 +199,7 @@ def run_single(args, torch):
                    "parallelism": "single GPU"},
         "pct_peak": round(100 * value / peak, 2),
         "gdof_per_s": round(3 * points / (ms_step * 1e-3) / 1e9, 2),
+        "copy_same_run_gbs": round(copy_gbs, 1),
         "ms_per_solve": {d: round(v, 5) for d, v in per_dir.items()},
         "direction_spread_pct": round(100 * (max(per_dir.values()) - min(per_dir.values()))
                                       / min(per_dir.values()), 2),
@@ -384,7 +396,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=0, help="grid extent (default 512 / 1024)")

@@ -44,6 +44,7 @@ struct FastArgs {
     const double2* Hp;     // C x K pairs: Hp[k*K+q] = (H[2k][q], H[2k+1][q])
     const double* g;       // 2 x K pass-A functionals
     long long lines;
+    long long items;       // work items of tiles_per_cta tiles (persistent kernels)
     int rows;              // rows per line in u/out
     int sz;
     int chunks;            // C
@@ -90,6 +91,9 @@ struct StagedArgs {
 // launchers (tds_kernels.cu)
 int launch_fast(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
                 cudaStream_t s);
+bool tma_eligible(int M, const FastArgs& a);
+int launch_tma(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
+               cudaStream_t s);
 int launch_staged_decouple(const StagedArgs& a, cudaStream_t s);
 int launch_staged_finish(const StagedArgs& a, cudaStream_t s);
 int launch_thomas(const StagedArgs& a, cudaStream_t s);

@@ -168,14 +168,14 @@ __global__ void __launch_bounds__(512) k_fast(const __grid_constant__ FastArgs p
 
     if (!valid) return;
     double* __restrict__ ob = p.out + lb;
-    ob[(long long)r0 * sz] = F;
+    __stcs(ob + (long long)r0 * sz, F);
 #pragma unroll
     for (int i = 1; i < M - 1; ++i) {
         const double sa = UNIFORM ? p.ut.sa[i] : TAB(i, 8);
         const double sc = UNIFORM ? p.ut.sc[i] : TAB(i, 9);
-        ob[(long long)(r0 + i) * sz] = fma(-sc, L, fma(-sa, F, d[i]));
+        __stcs(ob + (long long)(r0 + i) * sz, fma(-sc, L, fma(-sa, F, d[i])));
     }
-    ob[(long long)(r0 + M - 1) * sz] = L;
+    __stcs(ob + (long long)(r0 + M - 1) * sz, L);
 #undef TAB
 }
 
@@ -192,6 +192,7 @@ static int launch_fast_t(const FastArgs& a, long long tiles, cudaStream_t s) {
 
 int launch_fast(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
                 cudaStream_t s) {
+    if (tma_eligible(M, a)) return launch_tma(M, mode, uniform, a, tiles, s);
 #define DISPATCH_MODE(MM)                                                             \
     switch (mode) {                                                                   \
         case MODE_SOLVE:                                                              \

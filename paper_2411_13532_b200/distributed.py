@@ -328,6 +328,8 @@ def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
                               NotDominantWarning, stacklevel=2)
     plan = get_plan(sys, stencil, part, -1, arithmetic)
     fld = _Field(field_values)
+    if groups * sz == 0:
+        return fld.give(fld.empty_like(), out)
     res = out if (out is not None and not fld.host) else fld.empty_like()
     N.check(N.lib().tds_solve(plan.handle, fld.ptr, ctypes.c_void_p(res.data_ptr()),
                               groups, sz, _stream_handle(stream)), part.rank_count)
