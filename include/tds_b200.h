@@ -142,6 +142,26 @@ int tds_finish(const tds_plan* plan, const double* u, const double* halo_lo,
                const double* prev_last, const double* next_first, double* out,
                long long groups, int sz, void* stream);
 
+/* ---- fused per-rank solve over NVLink peer memory (k_dd) ----------------
+ * One kernel per rank does the whole distd2_solve (distributed.py:327-366):
+ * both neighbour rounds are peer stores into the neighbours' MAILBOXES plus
+ * per-tile acquire/release flags. A mailbox is tds_mailbox_words(groups, sz)
+ * 8-byte words of zeroed device memory; neighbours map it with CUDA IPC.
+ * `epoch` must increase by one per solve (same value on every rank). All
+ * ranks must have the same block size. Waits time out after 10 s and set
+ * the mailbox error word (tds_mailbox_error) instead of hanging. */
+long long tds_mailbox_words(long long groups, int sz);
+int tds_fused_eligible(const tds_plan* plan, long long groups, int sz);
+int tds_fused_solve(const tds_plan* plan, const double* u, double* out,
+                    long long groups, int sz, double* mail, double* mail_prev,
+                    double* mail_next, unsigned long long epoch, void* stream);
+int tds_mailbox_error(const double* mail, long long groups, int sz, int* err);
+/* CUDA IPC plumbing for mailboxes: handle is 64 bytes (cudaIpcMemHandle_t) */
+int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle);
+int tds_ipc_open(const unsigned char* handle, void** ptr);
+int tds_ipc_close(void* ptr);
+int tds_ipc_free(void* ptr);
+
 /* ---- phase-level kernels, reference arithmetic (bit-identical) ----------
  * Position-major (rows, lanes) device arrays, as the reference phase
  * functions take them. Coefficients are host arrays (copied per call). */

@@ -67,6 +67,14 @@ SIGNATURES = {
     "tds_substitute": (_I, [_P, _DP, _DP, _P, _P, _P, _I, _LL, _P]),
     "tds_boundary_pair": (_I, [_P, _P, _D, _D, _P, _P, _LL, _P]),
     "tds_thomas": (_I, [_DP, _DP, _DP, _I, _P, _P, _I, _LL, _I, _P]),
+    "tds_mailbox_words": (_LL, [_LL, _I]),
+    "tds_fused_eligible": (_I, [_P, _LL, _I]),
+    "tds_fused_solve": (_I, [_P, _P, _P, _LL, _I, _P, _P, _P, ctypes.c_ulonglong, _P]),
+    "tds_mailbox_error": (_I, [_P, _LL, _I, _IP]),
+    "tds_ipc_alloc": (_I, [_LL, ctypes.POINTER(_P), ctypes.c_char_p]),
+    "tds_ipc_open": (_I, [ctypes.c_char_p, ctypes.POINTER(_P)]),
+    "tds_ipc_close": (_I, [_P]),
+    "tds_ipc_free": (_I, [_P]),
     "tds_pack": (_I, [_P, _P, _I, _I, _I, _I, _I, _LL, _P]),
     "tds_unpack": (_I, [_P, _P, _I, _I, _I, _I, _I, _LL, _P]),
 }

@@ -1,6 +1,7 @@
 // C-ABI entry points (include/tds_b200.h): argument checking and dispatch of
 // the plan to the fast or staged kernels. No allocation on the solve path
 // except the phase-level calls that take host coefficient arrays.
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -275,3 +276,77 @@ extern "C" int tds_unpack(const double* field, double* cart, int nx, int ny, int
                           int direction, long long groups, void* stream) {
     return pack_common(field, cart, nx, ny, nz, sz, direction, groups, false, stream);
 }
+
+// ------------------------------------------------ fused multi-GPU (k_dd)
+
+namespace tds {
+long long dd_mail_words(long long lines);
+bool dd_eligible(int M, const FastArgs& a);
+int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
+              double* mail_next, unsigned long long epoch, long long tiles, cudaStream_t s);
+}  // namespace tds
+
+extern "C" long long tds_mailbox_words(long long groups, int sz) {
+    return tds::dd_mail_words(groups * sz);
+}
+
+extern "C" int tds_fused_eligible(const tds_plan* p, long long groups, int sz) {
+    if (!p || p->rank < 0 || p->P < 2 || p->path != TDS_PATH_FAST) return 0;
+    tds::FastArgs a = fast_args(p, groups * sz, sz);
+    a.u = reinterpret_cast<const double*>(uintptr_t(256));   // alignment probe only
+    return tds::dd_eligible(p->M, a) ? 1 : 0;
+}
+
+extern "C" int tds_fused_solve(const tds_plan* p, const double* u, double* out, long long groups,
+                               int sz, double* mail, double* mail_prev, double* mail_next,
+                               unsigned long long epoch, void* stream) {
+    int rc = check_field(p, groups, sz);
+    if (rc) return rc;
+    if (p->rank < 0 || p->P < 2 || p->path != TDS_PATH_FAST)
+        return set_err(TDS_ERR_UNSUPPORTED, "fused solve needs a per-rank fast-path plan");
+    if ((p->has_prev && !mail_prev) || (p->has_next && !mail_next) || !mail)
+        return set_err(TDS_ERR_INVALID, "missing mailbox");
+    const long long lines = groups * sz;
+    tds::FastArgs a = fast_args(p, lines, sz);
+    a.u = u;
+    a.out = out;
+    a.edge_mode = tds::EDGE_HALO;
+    if (!tds::dd_eligible(p->M, a))
+        return set_err(TDS_ERR_UNSUPPORTED, "field not eligible for the fused kernel");
+    return tds::launch_dd(p->M, p->uniform, a, mail, p->has_prev ? mail_prev : nullptr,
+                          p->has_next ? mail_next : nullptr, epoch, tiles_of(lines), S(stream));
+}
+
+extern "C" int tds_mailbox_error(const double* mail, long long groups, int sz, int* err) {
+    long long words = tds::dd_mail_words(groups * sz);
+    unsigned long long v = 0;
+    int rc = tds::cuda_check(cudaMemcpy(&v, mail + (words - 1), 8, cudaMemcpyDeviceToHost),
+                             "read mailbox error word");
+    *err = v ? 1 : 0;
+    return rc;
+}
+
+extern "C" int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle) {
+    int rc = tds::cuda_check(cudaMalloc(ptr, size_t(bytes)), "cudaMalloc(mailbox)");
+    if (rc) return rc;
+    rc = tds::cuda_check(cudaMemset(*ptr, 0, size_t(bytes)), "cudaMemset(mailbox)");
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    rc = tds::cuda_check(cudaIpcGetMemHandle(&h, *ptr), "cudaIpcGetMemHandle");
+    if (rc) return rc;
+    std::memcpy(handle, &h, sizeof(h));
+    return TDS_OK;
+}
+
+extern "C" int tds_ipc_open(const unsigned char* handle, void** ptr) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    return tds::cuda_check(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                           "cudaIpcOpenMemHandle");
+}
+
+extern "C" int tds_ipc_close(void* ptr) {
+    return tds::cuda_check(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+}
+
+extern "C" int tds_ipc_free(void* ptr) { return tds::cuda_check(cudaFree(ptr), "cudaFree"); }

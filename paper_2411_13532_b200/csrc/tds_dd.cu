@@ -1,0 +1,335 @@
+// Fused single-pass DistD2 for one rank per GPU (sm_100a): the whole
+// per-rank solve of distributed.py:327-366 -- both neighbour rounds included
+// -- in ONE kernel launch, 16 B/point of HBM traffic.
+//
+// Each rank owns a MAILBOX in its HBM that its neighbours map through CUDA
+// IPC (NVLink peer memory). Per tile of 16 lines:
+//   ROUND 1 (halo, transport.py:142-171): the rank stores its first two rows
+//     into prev's mailbox and its last two rows into next's, one item AHEAD
+//     of use, then raises a per-tile flag (st.relaxed.sys after
+//     fence.sc.sys); the consumer acquires the flag (ld.acquire.sys).
+//   decoupling: TMA tile -> registers, Alg. 6 sweeps (as k_tma).
+//   ROUND 2 (boundary rows, transport.py:174-191): g0.Y / g1.Y are the
+//     rank's d[0], d[m-1]; they go to prev / next the same way, and the
+//     2x2 pairs (distributed.py:279-293) give u_start / u_end in-kernel.
+//   substitution with the pinned reduced map, one streaming store.
+// Deadlock freedom: every rank runs the same persistent schedule (same grid,
+// same item order); in every iteration a CTA publishes before it waits, and
+// what it waits for is published by the same CTA index of the neighbour in
+// the same or an earlier iteration. Every wait has a device-side timeout
+// that records an error word instead of hanging the GPU.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "tds_device.cuh"
+#include "tds_tma.h"
+
+namespace tds {
+
+using namespace dev;
+
+struct DDArgs {
+    TmaArgs t;
+    double* mail;          // own mailbox
+    double* mail_prev;     // prev rank's mailbox (peer mapping), null on an open edge
+    double* mail_next;     // next rank's mailbox
+    unsigned long long epoch;
+    unsigned long long timeout_ns;
+};
+
+// mailbox layout (in 8-byte words), L = lines, T = tiles
+struct Mail {
+    long long L, T;
+    __host__ __device__ long long d_from_prev() const { return 0; }
+    __host__ __device__ long long d_from_next() const { return L; }
+    __host__ __device__ long long h_lo() const { return 2 * L; }
+    __host__ __device__ long long h_hi() const { return 4 * L; }
+    __host__ __device__ long long f_hlo() const { return 6 * L; }
+    __host__ __device__ long long f_hhi() const { return 6 * L + T; }
+    __host__ __device__ long long f_dprev() const { return 6 * L + 2 * T; }
+    __host__ __device__ long long f_dnext() const { return 6 * L + 3 * T; }
+    __host__ __device__ long long err() const { return 6 * L + 4 * T; }
+    __host__ __device__ long long words() const { return 6 * L + 4 * T + 1; }
+};
+
+namespace {
+
+__device__ __forceinline__ unsigned long long* flagp(double* base, long long off) {
+    return reinterpret_cast<unsigned long long*>(base + off);
+}
+
+// lane 0 of a half-warp waits for flag >= epoch (with timeout); the half-warp
+// then proceeds together. Returns false on timeout / earlier error.
+__device__ bool half_wait(const DDArgs& A, const Mail& mb, long long flag_off, unsigned mask,
+                          int lane) {
+    int ok = 1;
+    if (lane == 0) {
+        unsigned long long* f = flagp(A.mail, flag_off);
+        unsigned long long* err = flagp(A.mail, mb.err());
+        if (ld_acquire_sys(f) < A.epoch) {
+            const unsigned long long t0 = globaltimer();
+            unsigned ns = 32;
+            for (;;) {
+                if (ld_acquire_sys(f) >= A.epoch) break;
+                if (*reinterpret_cast<volatile unsigned long long*>(err) != 0ULL ||
+                    globaltimer() - t0 > A.timeout_ns) {
+                    atomicExch(err, 1ULL);
+                    ok = 0;
+                    break;
+                }
+                __nanosleep(ns);
+                if (ns < 1024) ns *= 2;
+            }
+        }
+    }
+    ok = __shfl_sync(mask, ok, (threadIdx.x & 31) & ~15);
+    __syncwarp(mask);
+    return ok != 0;
+}
+
+// every lane has stored its value into the peer mailbox; make the stores
+// visible system-wide, then lane 0 raises the tile's flag in the peer mailbox
+__device__ __forceinline__ void half_publish(double* peer, long long flag_off,
+                                             unsigned long long epoch, unsigned mask,
+                                             int lane) {
+    __threadfence_system();
+    __syncwarp(mask);
+    if (lane == 0) st_relaxed_sys(flagp(peer, flag_off), epoch);
+}
+
+}  // namespace
+
+template <int M, bool UNIFORM>
+__global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
+    const FastArgs& p = A.t.f;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int C = p.chunks;
+    const int K = 2 * C;
+    const int rows = p.rows;
+    const int tpc = p.tiles_per_cta;
+    const int t = threadIdx.x;
+    const int lane = t % TL;
+    const int chunk = (t / TL) % C;
+    const int tl = t / (TL * C);
+    const unsigned hmask = 0xFFFFu << (16 * ((t >> 4) & 1));
+    const long long sz = p.sz;
+    const int r0 = chunk * M;
+    const Mail mb{p.lines, (p.lines + TL - 1) / TL};
+    double* tiles = reinterpret_cast<double*>(smem);
+    const size_t tile_elems = (size_t)rows * TL;
+    double* sY = tiles + (size_t)tpc * tile_elems;
+    const size_t ybuf = (size_t)tpc * K * TL;
+    double* sP = sY + 2 * ybuf;                        // pins: [tpc][2][TL]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sP + (size_t)tpc * 2 * TL);
+    const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
+    const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
+
+    auto issue = [&](long long item) {
+        uint32_t bytes = 0;
+        for (int j = 0; j < tpc; ++j)
+            if ((item * tpc + j) * TL < p.lines) bytes += (uint32_t)(tile_elems * sizeof(double));
+        mbar_expect_tx(bar, bytes);
+        for (int j = 0; j < tpc; ++j) {
+            const long long first = (item * tpc + j) * TL;
+            if (first >= p.lines) break;
+            const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
+            for (int b = 0; b * A.t.boxr < rows; ++b)
+                tma_load_3d(tiles + j * tile_elems + (size_t)b * A.t.boxr * TL, &A.t.map, bar,
+                            l0, b * A.t.boxr, g);
+        }
+    };
+    // ROUND 1 for `item`: my first two rows -> prev's high halo, my last two
+    // rows -> next's low halo (read straight from my block in HBM)
+    auto publish_halo = [&](long long item) {
+        const long long tile = item * tpc + tl;
+        const long long ln = tile * TL + lane;
+        if (ln >= p.lines) return;                      // whole half-warp
+        const double* ub = p.u + line_base(ln, rows, p.sz);
+        const long long hb = halo_base(ln, p.sz);
+        if (first_chunk && A.mail_prev) {
+            A.mail_prev[mb.h_hi() + hb] = __ldg(ub);
+            A.mail_prev[mb.h_hi() + hb + sz] = __ldg(ub + sz);
+            half_publish(A.mail_prev, mb.f_hhi() + tile, A.epoch, hmask, lane);
+        }
+        if (last_chunk && A.mail_next) {
+            A.mail_next[mb.h_lo() + hb] = __ldg(ub + (long long)(rows - 2) * sz);
+            A.mail_next[mb.h_lo() + hb + sz] = __ldg(ub + (long long)(rows - 1) * sz);
+            half_publish(A.mail_next, mb.f_hlo() + tile, A.epoch, hmask, lane);
+        }
+    };
+
+    if (t == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    long long item = blockIdx.x;
+    if (item < p.items) {
+        if (t == 0) issue(item);
+        publish_halo(item);
+    }
+    uint32_t phase = 0;
+
+    for (int it = 0; item < p.items; item += gridDim.x, ++it) {
+        const long long tile = item * tpc + tl;
+        const long long line = tile * TL + lane;
+        const bool valid = line < p.lines;
+        const long long nxt = item + gridDim.x;
+        if (nxt < p.items) publish_halo(nxt);          // one item ahead
+
+        while (!mbar_try_wait(bar, phase)) {
+        }
+        phase ^= 1u;
+        const double* tl_tile = tiles + tl * tile_elems;
+        double v[M + 4];
+        // halos of the rank block come from the neighbours' ROUND-1 stores
+        double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+        const long long hb = valid ? halo_base(line, p.sz) : 0;
+        if (valid && first_chunk && A.mail_prev && half_wait(A, mb, mb.f_hlo() + tile, hmask, lane)) {
+            h0 = ld_relaxed_sys(A.mail + mb.h_lo() + hb);
+            h1 = ld_relaxed_sys(A.mail + mb.h_lo() + hb + sz);
+        }
+        if (valid && last_chunk && A.mail_next && half_wait(A, mb, mb.f_hhi() + tile, hmask, lane)) {
+            h2 = ld_relaxed_sys(A.mail + mb.h_hi() + hb);
+            h3 = ld_relaxed_sys(A.mail + mb.h_hi() + hb + sz);
+        }
+#pragma unroll
+        for (int i = 0; i < M + 4; ++i) {
+            const int row = r0 - 2 + i;
+            double x;
+            if (row < 0) x = (i == 0) ? h0 : h1;
+            else if (row >= rows) x = (row == rows) ? h2 : h3;
+            else x = tl_tile[row * TL + lane];
+            v[i] = x;
+        }
+        __syncthreads();   // tile buffer free
+        if (t == 0 && nxt < p.items) {
+            fence_proxy_async();
+            issue(nxt);
+        }
+
+        double d[M];
+        chunk_sweeps<M, UNIFORM>(p, tb, v, d);
+
+        double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TL;
+        Y[(2 * chunk) * TL + lane] = d[0];
+        Y[(2 * chunk + 1) * TL + lane] = d[M - 1];
+        __syncthreads();
+
+        // ROUND 2: the rank's decoupled boundary rows, 2x2 pairs, pins
+        double* P = sP + (size_t)tl * 2 * TL;
+        if (valid && (first_chunk || last_chunk)) {
+            double g0y = 0.0, g1y = 0.0;
+            for (int q = 0; q < K; ++q) {
+                const double y = Y[q * TL + lane];
+                if (first_chunk) g0y = fma(__ldg(p.g + q), y, g0y);
+                if (last_chunk) g1y = fma(__ldg(p.g + K + q), y, g1y);
+            }
+            if (first_chunk) {
+                if (A.mail_prev) {
+                    A.mail_prev[mb.d_from_next() + line] = g0y;
+                    half_publish(A.mail_prev, mb.f_dnext() + tile, A.epoch, hmask, lane);
+                }
+            }
+            if (last_chunk) {
+                if (A.mail_next) {
+                    A.mail_next[mb.d_from_prev() + line] = g1y;
+                    half_publish(A.mail_next, mb.f_dprev() + tile, A.epoch, hmask, lane);
+                }
+            }
+            if (first_chunk) {
+                double us = g0y;
+                if (p.has_prev && half_wait(A, mb, mb.f_dprev() + tile, hmask, lane)) {
+                    const double prev_last = ld_relaxed_sys(A.mail + mb.d_from_prev() + line);
+                    us = (g0y - p.sa_first * prev_last) / p.det_prev;
+                }
+                P[lane] = us;
+            }
+            if (last_chunk) {
+                double ue = g1y;
+                if (p.has_next && half_wait(A, mb, mb.f_dnext() + tile, hmask, lane)) {
+                    const double next_first = ld_relaxed_sys(A.mail + mb.d_from_next() + line);
+                    ue = (g1y - p.sc_last * next_first) / p.det_next;
+                }
+                P[TL + lane] = ue;
+            }
+        }
+        __syncthreads();
+
+        double F, L;
+        chunk_bounds(p.Hp + (size_t)chunk * K, Y, K, lane, P, P + TL, F, L);
+        if (valid)
+            chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F, L,
+                                    A.t.store_cs != 0);
+    }
+}
+
+namespace {
+
+size_t dd_smem(const FastArgs& a) { return tma_smem(a) + (size_t)a.tiles_per_cta * 2 * TL * 8; }
+
+template <int M, bool UNI>
+int launch_dd_t(const DDArgs& A0, long long tiles, cudaStream_t s) {
+    DDArgs A = A0;
+    FastArgs& a = A.t.f;
+    a.items = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+    if (a.items <= 0) return TDS_OK;
+    int rc = encode_field_map(a, M, &A.t.map, &A.t.boxr);
+    if (rc) return rc;
+    A.t.store_cs = store_policy();
+    const int threads = a.tiles_per_cta * a.chunks * TL;
+    const size_t smem = dd_smem(a);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        rc = cuda_check(cudaFuncSetAttribute(k_dd<M, UNI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem),
+                        "cudaFuncSetAttribute(k_dd)");
+        if (rc) return rc;
+        smem_set = smem;
+    }
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd<M, UNI>, threads, smem);
+    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
+    // exactly the resident capacity: every CTA is co-resident (no waits on
+    // unscheduled CTAs); identical on every rank
+    long long grid = (long long)nb * sms;
+    if (grid > a.items) grid = a.items;
+    k_dd<M, UNI><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_dd launch");
+}
+
+}  // namespace
+
+long long dd_mail_words(long long lines) {
+    Mail mb{lines, (lines + TL - 1) / TL};
+    return mb.words();
+}
+
+bool dd_eligible(int M, const FastArgs& a) {
+    if (const char* e = getenv("TDS_FUSED"))
+        if (e[0] == '0') return false;
+    if (!tma_eligible(M, a)) return false;
+    return dd_smem(a) <= 200 * 1024;
+}
+
+int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
+              double* mail_next, unsigned long long epoch, long long tiles, cudaStream_t s) {
+    DDArgs A;
+    A.t.f = a;
+    A.mail = mail;
+    A.mail_prev = mail_prev;
+    A.mail_next = mail_next;
+    A.epoch = epoch;
+    A.timeout_ns = 10ULL * 1000 * 1000 * 1000;   // 10 s: a stall records an error
+    if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
+        A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
+    if (M == 32) return uniform ? launch_dd_t<32, true>(A, tiles, s) : launch_dd_t<32, false>(A, tiles, s);
+    if (M == 16) return uniform ? launch_dd_t<16, true>(A, tiles, s) : launch_dd_t<16, false>(A, tiles, s);
+    return set_err(TDS_ERR_UNSUPPORTED, "unsupported chunk size");
+}
+
+}  // namespace tds

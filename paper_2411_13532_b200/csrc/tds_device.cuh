@@ -1,0 +1,184 @@
+// Device-side building blocks shared by the fast kernels (k_tma, k_dd):
+// PTX wrappers (mbarrier, TMA, sys-scope acquire/release) and the per-chunk
+// arithmetic of the fused DistD2 solve.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tds_internal.h"
+
+namespace tds {
+namespace dev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+// system-scope flag protocol for NVLink peer memory
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ long long line_base(long long line, int rows, int sz) {
+    return (line / sz) * (long long)rows * sz + (line % sz);
+}
+__device__ __forceinline__ long long halo_base(long long line, int sz) {
+    return (line / sz) * 2LL * sz + (line % sz);
+}
+
+// Fused width-5 stencil + Alg. 6 (reference distributed.py:257-276) on one
+// chunk of M rows held in registers: v = rows r0-2 .. r0+M+1, d = decoupled.
+template <int M, bool UNIFORM>
+__device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __restrict__ tb,
+                                             const double (&v)[M + 4], double (&d)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double s0, s1, s2, s3, s4, f, r;
+        if (UNIFORM) {
+            s0 = p.ut.st[0]; s1 = p.ut.st[1]; s2 = p.ut.st[2]; s3 = p.ut.st[3]; s4 = p.ut.st[4];
+            f = p.ut.f[i]; r = p.ut.r[i];
+        } else {
+            const double2 c01 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF));
+            const double2 c23 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 2));
+            const double2 c4f = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 4));
+            s0 = c01.x; s1 = c01.y; s2 = c23.x; s3 = c23.y; s4 = c4f.x; f = c4f.y;
+            r = __ldg(tb + i * NCOEF + 6);
+        }
+        double rhs = s0 * v[i];
+        rhs = fma(s1, v[i + 1], rhs);
+        rhs = fma(s2, v[i + 2], rhs);
+        rhs = fma(s3, v[i + 3], rhs);
+        rhs = fma(s4, v[i + 4], rhs);
+        if (i < 2) d[i] = rhs * r;
+        else d[i] = fma(-r, d[i - 1], rhs) * f;
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) {
+        const double w = UNIFORM ? p.ut.w[i] : __ldg(tb + i * NCOEF + 7);
+        d[i] = fma(-w, d[i + 1], d[i]);
+    }
+    const double w0 = UNIFORM ? p.ut.w[0] : __ldg(tb + 7);
+    const double f0 = UNIFORM ? p.ut.f[0] : __ldg(tb + 5);
+    d[0] = fma(-w0, d[1], d[0]) * f0;
+}
+
+// Chunk boundary values (F, L) = rows 2k, 2k+1 of H applied to the reduced
+// rhs Y (K entries, stride TL in shared memory). If pins are given, Y[0] and
+// Y[K-1] are replaced by pin0 / pin1 (the rank's u_start / u_end).
+__device__ __forceinline__ void chunk_bounds(const double2* __restrict__ hr, const double* Y,
+                                             int K, int lane, const double* pin0,
+                                             const double* pin1, double& F, double& L) {
+    double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
+    int q0 = 0, q1 = K;
+    if (pin0) {
+        const double2 h = __ldg(hr);
+        const double2 hl = __ldg(hr + K - 1);
+        const double a = pin0[lane], b = pin1[lane];
+        F0 = fma(h.x, a, 0.0);
+        L0 = fma(h.y, a, 0.0);
+        F1 = fma(hl.x, b, 0.0);
+        L1 = fma(hl.y, b, 0.0);
+        q0 = 1;
+        q1 = K - 1;
+    }
+    int q = q0;
+    for (; q + 1 < q1; q += 2) {
+        const double2 h0 = __ldg(hr + q);
+        const double2 h1 = __ldg(hr + q + 1);
+        const double ya = Y[q * TL + lane];
+        const double yb = Y[(q + 1) * TL + lane];
+        F0 = fma(h0.x, ya, F0);
+        L0 = fma(h0.y, ya, L0);
+        F1 = fma(h1.x, yb, F1);
+        L1 = fma(h1.y, yb, L1);
+    }
+    if (q < q1) {
+        const double2 h0 = __ldg(hr + q);
+        const double ya = Y[q * TL + lane];
+        F0 = fma(h0.x, ya, F0);
+        L0 = fma(h0.y, ya, L0);
+    }
+    F = F0 + F1;
+    L = L0 + L1;
+}
+
+// Alg. 7 at chunk level + one streaming store per row.
+template <int M, bool UNIFORM>
+__device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __restrict__ tb,
+                                            double* __restrict__ ob, long long sz, int r0,
+                                            const double (&d)[M], double F, double L,
+                                            bool stream) {
+    if (stream) {
+        __stcs(ob + (long long)r0 * sz, F);
+#pragma unroll
+        for (int i = 1; i < M - 1; ++i) {
+            const double sa = UNIFORM ? p.ut.sa[i] : __ldg(tb + i * NCOEF + 8);
+            const double sc = UNIFORM ? p.ut.sc[i] : __ldg(tb + i * NCOEF + 9);
+            __stcs(ob + (long long)(r0 + i) * sz, fma(-sc, L, fma(-sa, F, d[i])));
+        }
+        __stcs(ob + (long long)(r0 + M - 1) * sz, L);
+    } else {
+        ob[(long long)r0 * sz] = F;
+#pragma unroll
+        for (int i = 1; i < M - 1; ++i) {
+            const double sa = UNIFORM ? p.ut.sa[i] : __ldg(tb + i * NCOEF + 8);
+            const double sc = UNIFORM ? p.ut.sc[i] : __ldg(tb + i * NCOEF + 9);
+            ob[(long long)(r0 + i) * sz] = fma(-sc, L, fma(-sa, F, d[i]));
+        }
+        ob[(long long)(r0 + M - 1) * sz] = L;
+    }
+}
+
+}  // namespace dev
+}  // namespace tds

@@ -14,72 +14,16 @@
 //     without spending registers on the prefetch.
 // Eligible when sz % 16 == 0 (rows of whole 128-byte segments), the field is
 // 16-byte aligned and a tile fits in shared memory.
-#include <cuda.h>
 #include <cudaTypedefs.h>
-#include <cuda_runtime.h>
 
-#include <cstdint>
 #include <cstdlib>
 
-#include "tds_internal.h"
+#include "tds_device.cuh"
+#include "tds_tma.h"
 
 namespace tds {
 
-namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ long long line_base(long long line, int rows, int sz) {
-    return (line / sz) * (long long)rows * sz + (line % sz);
-}
-__device__ __forceinline__ long long halo_base(long long line, int sz) {
-    return (line / sz) * 2LL * sz + (line % sz);
-}
-
-}  // namespace
-
-struct TmaArgs {
-    FastArgs f;
-    CUtensorMap map;
-    int boxr;          // rows per TMA box (divides rows)
-    int store_cs;      // streaming stores (A/B knob TDS_STCS)
-};
+using namespace dev;
 
 template <int M, int MODE, bool UNIFORM>
 __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) {
@@ -101,7 +45,6 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     const size_t ybuf = (size_t)tpc * K * TL;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sY + 2 * ybuf);
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
-#define TAB(i, k) (UNIFORM ? 0.0 : __ldg(tb + (i) * NCOEF + (k)))
 
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
@@ -169,38 +112,7 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         }
 
         double d[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            double s0, s1, s2, s3, s4, f, r;
-            if (UNIFORM) {
-                s0 = p.ut.st[0]; s1 = p.ut.st[1]; s2 = p.ut.st[2]; s3 = p.ut.st[3];
-                s4 = p.ut.st[4];
-                f = p.ut.f[i]; r = p.ut.r[i];
-            } else {
-                const double2 c01 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF));
-                const double2 c23 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 2));
-                const double2 c4f = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 4));
-                s0 = c01.x; s1 = c01.y; s2 = c23.x; s3 = c23.y; s4 = c4f.x; f = c4f.y;
-                r = __ldg(tb + i * NCOEF + 6);
-            }
-            double rhs = s0 * v[i];
-            rhs = fma(s1, v[i + 1], rhs);
-            rhs = fma(s2, v[i + 2], rhs);
-            rhs = fma(s3, v[i + 3], rhs);
-            rhs = fma(s4, v[i + 4], rhs);
-            if (i < 2) d[i] = rhs * r;
-            else d[i] = fma(-r, d[i - 1], rhs) * f;
-        }
-#pragma unroll
-        for (int i = M - 3; i >= 1; --i) {
-            const double w = UNIFORM ? p.ut.w[i] : TAB(i, 7);
-            d[i] = fma(-w, d[i + 1], d[i]);
-        }
-        {
-            const double w0 = UNIFORM ? p.ut.w[0] : TAB(0, 7);
-            const double f0 = UNIFORM ? p.ut.f[0] : TAB(0, 5);
-            d[0] = fma(-w0, d[1], d[0]) * f0;
-        }
+        chunk_sweeps<M, UNIFORM>(p, tb, v, d);
 
         double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TL;
         double y0 = d[0], yL = d[M - 1];
@@ -232,47 +144,48 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
             continue;
         }
 
-        double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
-        const double2* __restrict__ hr = p.Hp + (size_t)chunk * K;
-        for (int q = 0; q + 1 < K; q += 2) {
-            const double2 h0 = __ldg(hr + q);
-            const double2 h1 = __ldg(hr + q + 1);
-            const double ya = Y[q * TL + lane];
-            const double yb = Y[(q + 1) * TL + lane];
-            F0 = fma(h0.x, ya, F0);
-            L0 = fma(h0.y, ya, L0);
-            F1 = fma(h1.x, yb, F1);
-            L1 = fma(h1.y, yb, L1);
-        }
-        const double F = F0 + F1, L = L0 + L1;
-
-        if (valid) {
-            double* __restrict__ ob = p.out + line_base(line, p.rows, p.sz);
-            if (A.store_cs) {   // streaming (evict-first) stores
-                __stcs(ob + (long long)r0 * sz, F);
-#pragma unroll
-                for (int i = 1; i < M - 1; ++i) {
-                    const double sa = UNIFORM ? p.ut.sa[i] : TAB(i, 8);
-                    const double sc = UNIFORM ? p.ut.sc[i] : TAB(i, 9);
-                    __stcs(ob + (long long)(r0 + i) * sz, fma(-sc, L, fma(-sa, F, d[i])));
-                }
-                __stcs(ob + (long long)(r0 + M - 1) * sz, L);
-            } else {
-                ob[(long long)r0 * sz] = F;
-#pragma unroll
-                for (int i = 1; i < M - 1; ++i) {
-                    const double sa = UNIFORM ? p.ut.sa[i] : TAB(i, 8);
-                    const double sc = UNIFORM ? p.ut.sc[i] : TAB(i, 9);
-                    ob[(long long)(r0 + i) * sz] = fma(-sc, L, fma(-sa, F, d[i]));
-                }
-                ob[(long long)(r0 + M - 1) * sz] = L;
-            }
-        }
+        double F, L;
+        chunk_bounds(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+        if (valid)
+            chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, p.rows, p.sz), sz, r0, d, F,
+                                    L, A.store_cs != 0);
     }
-#undef TAB
 }
 
 namespace {
+
+template <int M, int MODE, bool UNI>
+int launch_tma_t(const FastArgs& a, long long tiles, cudaStream_t s) {
+    TmaArgs A;
+    A.f = a;
+    A.f.items = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+    if (A.f.items <= 0) return TDS_OK;
+    int rc = encode_field_map(a, M, &A.map, &A.boxr);
+    if (rc) return rc;
+    A.store_cs = store_policy();
+    const int threads = a.tiles_per_cta * a.chunks * TL;
+    const size_t smem = tma_smem(a);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        rc = cuda_check(cudaFuncSetAttribute(k_tma<M, MODE, UNI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem),
+                        "cudaFuncSetAttribute(k_tma)");
+        if (rc) return rc;
+        smem_set = smem;
+    }
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tma<M, MODE, UNI>, threads, smem);
+    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_tma does not fit on an SM");
+    long long grid = (long long)nb * sms;
+    if (grid > A.f.items) grid = A.f.items;
+    k_tma<M, MODE, UNI><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_tma launch");
+}
+
+}  // namespace
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -299,15 +212,14 @@ int box_rows(int rows, int M) {
     return best;
 }
 
-template <int M, int MODE, bool UNI>
-int launch_tma_t(const FastArgs& a, long long tiles, cudaStream_t s) {
-    TmaArgs A;
-    A.f = a;
-    A.f.items = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
-    if (A.f.items <= 0) return TDS_OK;
-    A.boxr = box_rows(a.rows, M);
-    A.store_cs = 1;   // measured: +2% over write-back stores on B200
-    if (const char* e = getenv("TDS_STCS")) A.store_cs = e[0] != '0';
+int store_policy() {
+    int cs = 1;   // measured: +2% over write-back stores on B200
+    if (const char* e = getenv("TDS_STCS")) cs = e[0] != '0';
+    return cs;
+}
+
+int encode_field_map(const FastArgs& a, int M, CUtensorMap* map, int* boxr) {
+    *boxr = box_rows(a.rows, M);
     CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (const char* e = getenv("TDS_L2PROMO")) {
         if (e[0] == '0') prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
@@ -316,36 +228,15 @@ int launch_tma_t(const FastArgs& a, long long tiles, cudaStream_t s) {
     const long long groups = a.lines / a.sz;
     cuuint64_t dims[3] = {(cuuint64_t)a.sz, (cuuint64_t)a.rows, (cuuint64_t)groups};
     cuuint64_t strides[2] = {(cuuint64_t)a.sz * 8, (cuuint64_t)a.rows * a.sz * 8};
-    cuuint32_t box[3] = {(cuuint32_t)TL, (cuuint32_t)A.boxr, 1};
+    cuuint32_t box[3] = {(cuuint32_t)TL, (cuuint32_t)*boxr, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult cr = encode_fn()(&A.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
-                              const_cast<double*>(a.u), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
+    CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.u),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, prom,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return set_err(TDS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    const int threads = a.tiles_per_cta * a.chunks * TL;
-    const size_t smem = tma_smem(a);
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        int rc = cuda_check(cudaFuncSetAttribute(k_tma<M, MODE, UNI>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem),
-                            "cudaFuncSetAttribute(k_tma)");
-        if (rc) return rc;
-        smem_set = smem;
-    }
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tma<M, MODE, UNI>, threads, smem);
-    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_tma does not fit on an SM");
-    long long grid = (long long)nb * sms;
-    if (grid > A.f.items) grid = A.f.items;
-    k_tma<M, MODE, UNI><<<(unsigned)grid, threads, smem, s>>>(A);
-    return cuda_check(cudaGetLastError(), "k_tma launch");
+    return TDS_OK;
 }
-
-}  // namespace
 
 bool tma_eligible(int M, const FastArgs& a) {
     if (const char* e = getenv("TDS_TMA"))

@@ -10,9 +10,17 @@ DistD2Rank.solve(u_local) for a rank holding rows [off, off+m) of every line:
     ROUND 2            -> prev's d[m-1], next's d[0]      (NCCL P2P)
     tds_finish         -> 2x2 pairs + substitution, out   (pass B: reads u,
                                                            writes out)
-The fast path recomputes the decoupling in pass B instead of materialising d:
-24 B/point of HBM traffic instead of the staged path's 32+.
+The two-pass path recomputes the decoupling in pass B instead of
+materialising d: 24 B/point of HBM traffic.
+
+FUSED path (default when every rank holds the same number of rows and the
+field is TMA-eligible): ONE kernel per rank per solve, `tds_fused_solve`
+(k_dd). Both neighbour rounds are NVLink peer stores into the neighbours'
+IPC-mapped mailboxes with per-tile acquire/release flags -- 16 B/point, no
+NCCL call and no host synchronisation on the solve path.
 """
+
+import os
 
 import ctypes
 
@@ -44,6 +52,10 @@ class DistD2Rank:
         st = None if stencil is None else stencil.c
         self.plan = Plan.create(sys, st, part.local_sizes, ctx.rank_id, _flags(arithmetic))
         self._bufs = {}
+        self._mail = {}
+        self._epoch = 0
+        self.fused = (self.plan.path == "fast" and len(set(part.local_sizes)) == 1
+                      and os.environ.get("TDS_FUSED", "1") != "0")
 
     @property
     def path(self):
@@ -65,6 +77,55 @@ class DistD2Rank:
             self._bufs[key] = b
         return b
 
+    def _mailbox(self, groups, sz):
+        """Own mailbox + the neighbours' mailboxes mapped through CUDA IPC
+        (one collective handle exchange per field shape)."""
+        import torch.distributed as dist
+        key = (groups, sz)
+        mb = self._mail.get(key)
+        if mb is not None:
+            return mb
+        lib, ctx = N.lib(), self.ctx
+        words = lib.tds_mailbox_words(groups, sz)
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        N.check(lib.tds_ipc_alloc(words * 8, ctypes.byref(own), handle))
+        handles = [None] * ctx.rank_count
+        dist.all_gather_object(handles, handle.raw, group=ctx.group)
+        opened = {}
+
+        def open_rank(pos):
+            pos %= ctx.rank_count
+            if pos not in opened:
+                ptr = ctypes.c_void_p()
+                N.check(lib.tds_ipc_open(handles[pos], ctypes.byref(ptr)))
+                opened[pos] = ptr
+            return opened[pos]
+
+        prev = open_rank(ctx.rank_id - 1) if ctx.has_prev else ctypes.c_void_p(0)
+        nxt = open_rank(ctx.rank_id + 1) if ctx.has_next else ctypes.c_void_p(0)
+        mb = (own, prev, nxt, list(opened.values()))
+        self._mail[key] = mb
+        return mb
+
+    def check(self):
+        """Raise if a fused solve timed out waiting for a neighbour (reads the
+        mailbox error words; synchronous)."""
+        for (groups, sz), (own, _, _, _) in self._mail.items():
+            err = ctypes.c_int(0)
+            N.check(N.lib().tds_mailbox_error(own, groups, sz, ctypes.byref(err)))
+            if err.value:
+                raise TimeoutError(f"rank {self.ctx.rank_id}: fused DistD2 solve timed out "
+                                   "waiting for a neighbour")
+
+    def close(self):
+        lib = N.lib()
+        for own, _, _, opened in self._mail.values():
+            for ptr in opened:
+                lib.tds_ipc_close(ptr)
+            lib.tds_ipc_free(own)
+        self._mail = {}
+
     def solve(self, u, out=None):
         """u: this rank's (n_groups, m, sz) fp64 CUDA tensor -> out (same shape)."""
         import torch
@@ -72,8 +133,18 @@ class DistD2Rank:
         if m != self.m:
             raise ValueError(f"rank {self.ctx.rank_id} holds {self.m} rows, got {m}")
         u = u.contiguous()
+        if u.data_ptr() % 16:
+            u = u.clone()
         if out is None:
             out = torch.empty_like(u)
+        if self.fused and N.lib().tds_fused_eligible(self.plan.handle, groups, sz):
+            own, prev, nxt, _ = self._mailbox(groups, sz)
+            self._epoch += 1
+            self.ctx.begin_solve()
+            self.ctx.exchange_rounds += 2          # both rounds run inside the kernel
+            N.check(N.lib().tds_fused_solve(self.plan.handle, _vp(u), _vp(out), groups, sz, own,
+                                            prev, nxt, self._epoch, _stream_handle()))
+            return out
         b = self._buffers(groups, sz, u.device)
         lib, h, s, ctx = N.lib(), self.plan.handle, _stream_handle(), self.ctx
         ctx.begin_solve()

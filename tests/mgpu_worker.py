@@ -43,7 +43,9 @@ def main():
         u = torch.from_numpy(np.ascontiguousarray(field[:, off:off + m, :])).to(dev)
         solver = T.DistD2Rank(s, stc, part, ctx, arithmetic=arith)
         out = solver.solve(u)
-        out2 = solver.solve(u)            # buffers reused, same bits
+        out2 = solver.solve(u)            # buffers / mailboxes reused, same bits
+        torch.cuda.synchronize()
+        solver.check()
         same = bool(torch.equal(out, out2))
         full = gather_to_root(ctx, out)
         # reference-shaped per-rank path: preprocess + one-time share + 2 rounds
@@ -60,7 +62,8 @@ def main():
             exact = np.array_equal(got, want)
             rs_exact = np.array_equal(full_rs.cpu().numpy(), want)
             ok = same and rs_exact and ((exact) if arith == "strict" else (err <= 1e-12))
-            print(f"[{name}] P={world} path={solver.path} rel={err:.3e} bitwise={exact} "
+            print(f"[{name}] P={world} path={solver.path} fused={solver.fused} "
+                  f"rel={err:.3e} bitwise={exact} "
                   f"reference_shaped_bitwise={rs_exact} repeat_same={same} "
                   f"{'OK' if ok else 'FAIL'}", flush=True)
             if not ok:

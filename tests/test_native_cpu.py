@@ -18,7 +18,8 @@ HEADER = os.path.join(ROOT, "include", "tds_b200.h")
 
 def header_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const\s+char\*|int)\s+(tds_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\*|int|long\s+long)\s+(tds_\w+)\s*\(",
+                                 text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
