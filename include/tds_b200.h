@@ -144,9 +144,10 @@ int tds_finish(const tds_plan* plan, const double* u, const double* halo_lo,
 
 /* ---- fused per-rank solve over NVLink peer memory (k_dd) ----------------
  * One kernel per rank does the whole distd2_solve (distributed.py:327-366):
- * both neighbour rounds are peer stores into the neighbours' MAILBOXES plus
- * per-tile acquire/release flags. A mailbox is tds_mailbox_words(groups, sz)
- * 8-byte words of zeroed device memory; neighbours map it with CUDA IPC.
+ * both neighbour rounds are peer stores into the neighbours' MAILBOXES,
+ * fence-free (sentinel-armed slots). A mailbox is tds_mailbox_words(groups,
+ * sz) 8-byte words filled with 0xFF bytes (tds_ipc_alloc does this);
+ * neighbours map it with CUDA IPC.
  * `epoch` must increase by one per solve (same value on every rank). All
  * ranks must have the same block size. Waits time out after 10 s and set
  * the mailbox error word (tds_mailbox_error) instead of hanging. */

@@ -322,14 +322,14 @@ extern "C" int tds_mailbox_error(const double* mail, long long groups, int sz, i
     unsigned long long v = 0;
     int rc = tds::cuda_check(cudaMemcpy(&v, mail + (words - 1), 8, cudaMemcpyDeviceToHost),
                              "read mailbox error word");
-    *err = v ? 1 : 0;
+    *err = (v == 1ULL) ? 1 : 0;   // ERR_TIMEOUT (sentinel fill = no error)
     return rc;
 }
 
 extern "C" int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle) {
     int rc = tds::cuda_check(cudaMalloc(ptr, size_t(bytes)), "cudaMalloc(mailbox)");
     if (rc) return rc;
-    rc = tds::cuda_check(cudaMemset(*ptr, 0, size_t(bytes)), "cudaMemset(mailbox)");
+    rc = tds::cuda_check(cudaMemset(*ptr, 0xFF, size_t(bytes)), "cudaMemset(mailbox)");   // sentinel fill
     if (rc) return rc;
     cudaIpcMemHandle_t h;
     rc = tds::cuda_check(cudaIpcGetMemHandle(&h, *ptr), "cudaIpcGetMemHandle");
