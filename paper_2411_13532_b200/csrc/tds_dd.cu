@@ -6,18 +6,18 @@
 // IPC (NVLink peer memory). Per tile of 16 lines:
 //   ROUND 1 (halo, transport.py:142-171): the rank stores its first two rows
 //     into prev's mailbox and its last two rows into next's, one item AHEAD
-//     of use, then raises a per-tile flag (st.relaxed.sys after
-//     fence.sc.sys); the consumer acquires the flag (ld.acquire.sys).
-//   decoupling: TMA tile -> registers, Alg. 6 sweeps (as k_tma).
+//     of use;
+//   decoupling: TMA tile -> registers, Alg. 6 sweeps (as k_tma);
 //   ROUND 2 (boundary rows, transport.py:174-191): g0.Y / g1.Y are the
-//     rank's d[0], d[m-1]; they go to prev / next the same way, and the
-//     2x2 pairs (distributed.py:279-293) give u_start / u_end in-kernel.
+//     rank's d[0], d[m-1]; they go to prev / next the same way, and the 2x2
+//     pairs (distributed.py:279-293) give u_start / u_end in-kernel;
 //   substitution with the pinned reduced map, one streaming store.
-// Deadlock freedom: every rank runs the same persistent schedule (same grid,
-// same item order); in every iteration a CTA publishes before it waits, and
-// what it waits for is published by the same CTA index of the neighbour in
-// the same or an earlier iteration. Every wait has a device-side timeout
-// that records an error word instead of hanging the GPU.
+// Messages are fence-free (sentinel-armed slots, see Mail). Deadlock
+// freedom: every rank runs the same persistent schedule (same grid, same
+// item order); in every iteration a CTA posts before it waits, and what it
+// waits for is posted by the same CTA index of the neighbour in the same or
+// an earlier iteration. Every wait has a device-side timeout that records an
+// error word instead of hanging the GPU.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -38,64 +38,65 @@ struct DDArgs {
     unsigned long long timeout_ns;
 };
 
-// mailbox layout (in 8-byte words), L = lines, T = tiles
+// Mailbox layout (8-byte words), L = lines. Two parity halves (epoch & 1)
+// of 6L value slots each, then one error word:
+//   D_FROM_PREV [L]  prev's d[m-1] per line      D_FROM_NEXT [L]  next's d[0]
+//   H_LO [2L]  prev's last two rows (G,2,sz)     H_HI [2L]  next's first two rows
+// A slot holds either the SENTINEL bit pattern (all ones: the byte-uniform
+// fill of cudaMemset(0xFF)) or a value. Writers canonicalise NaNs, so no
+// value equals the sentinel; readers poll their own slot and re-arm it. The
+// next write to the same slot is two epochs later, i.e. in a kernel that
+// starts after this one has finished -- no fences and no flags are needed.
 struct Mail {
-    long long L, T;
+    long long L;
+    __host__ __device__ long long half(unsigned long long epoch) const {
+        return (long long)(epoch & 1ULL) * 6 * L;
+    }
     __host__ __device__ long long d_from_prev() const { return 0; }
     __host__ __device__ long long d_from_next() const { return L; }
     __host__ __device__ long long h_lo() const { return 2 * L; }
     __host__ __device__ long long h_hi() const { return 4 * L; }
-    __host__ __device__ long long f_hlo() const { return 6 * L; }
-    __host__ __device__ long long f_hhi() const { return 6 * L + T; }
-    __host__ __device__ long long f_dprev() const { return 6 * L + 2 * T; }
-    __host__ __device__ long long f_dnext() const { return 6 * L + 3 * T; }
-    __host__ __device__ long long err() const { return 6 * L + 4 * T; }
-    __host__ __device__ long long words() const { return 6 * L + 4 * T + 1; }
+    __host__ __device__ long long err() const { return 12 * L; }
+    __host__ __device__ long long words() const { return 12 * L + 1; }
 };
+
+constexpr unsigned long long SENTINEL = ~0ULL;
+constexpr unsigned long long ERR_TIMEOUT = 1ULL;
 
 namespace {
 
-__device__ __forceinline__ unsigned long long* flagp(double* base, long long off) {
-    return reinterpret_cast<unsigned long long*>(base + off);
+__device__ __forceinline__ double canon(double x) {
+    return isnan(x) ? __longlong_as_double(0x7FF8000000000000LL) : x;
 }
-
-// lane 0 of a half-warp waits for flag >= epoch (with timeout); the half-warp
-// then proceeds together. Returns false on timeout / earlier error.
-__device__ bool half_wait(const DDArgs& A, const Mail& mb, long long flag_off, unsigned mask,
-                          int lane) {
-    int ok = 1;
-    if (lane == 0) {
-        unsigned long long* f = flagp(A.mail, flag_off);
-        unsigned long long* err = flagp(A.mail, mb.err());
-        if (ld_acquire_sys(f) < A.epoch) {
-            const unsigned long long t0 = globaltimer();
-            unsigned ns = 32;
-            for (;;) {
-                if (ld_acquire_sys(f) >= A.epoch) break;
-                if (*reinterpret_cast<volatile unsigned long long*>(err) != 0ULL ||
-                    globaltimer() - t0 > A.timeout_ns) {
-                    atomicExch(err, 1ULL);
-                    ok = 0;
-                    break;
-                }
-                __nanosleep(ns);
-                if (ns < 1024) ns *= 2;
+// post a value into a neighbour's mailbox slot (NVLink peer store)
+__device__ __forceinline__ void post(double* slot, double x) {
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(slot), "d"(canon(x)) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_sys_u64(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// wait for a neighbour's value in my mailbox slot, consume it, re-arm the slot
+__device__ double take(double* slot, const DDArgs& A, unsigned long long* err) {
+    unsigned long long v = ld_sys_u64(slot);
+    if (v == SENTINEL) {
+        const unsigned long long t0 = globaltimer();
+        unsigned ns = 32;
+        for (;;) {
+            __nanosleep(ns);
+            if (ns < 256) ns *= 2;
+            v = ld_sys_u64(slot);
+            if (v != SENTINEL) break;
+            if (*reinterpret_cast<volatile unsigned long long*>(err) == ERR_TIMEOUT ||
+                globaltimer() - t0 > A.timeout_ns) {
+                atomicExch(err, ERR_TIMEOUT);
+                return 0.0;
             }
         }
     }
-    ok = __shfl_sync(mask, ok, (threadIdx.x & 31) & ~15);
-    __syncwarp(mask);
-    return ok != 0;
-}
-
-// every lane has stored its value into the peer mailbox; make the stores
-// visible system-wide, then lane 0 raises the tile's flag in the peer mailbox
-__device__ __forceinline__ void half_publish(double* peer, long long flag_off,
-                                             unsigned long long epoch, unsigned mask,
-                                             int lane) {
-    __threadfence_system();
-    __syncwarp(mask);
-    if (lane == 0) st_relaxed_sys(flagp(peer, flag_off), epoch);
+    *reinterpret_cast<unsigned long long*>(slot) = SENTINEL;
+    return __longlong_as_double((long long)v);
 }
 
 }  // namespace
@@ -112,10 +113,11 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     const int lane = t % TL;
     const int chunk = (t / TL) % C;
     const int tl = t / (TL * C);
-    const unsigned hmask = 0xFFFFu << (16 * ((t >> 4) & 1));
     const long long sz = p.sz;
     const int r0 = chunk * M;
-    const Mail mb{p.lines, (p.lines + TL - 1) / TL};
+    const Mail mb{p.lines};
+    const long long par = mb.half(A.epoch);
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(A.mail + mb.err());
     double* tiles = reinterpret_cast<double*>(smem);
     const size_t tile_elems = (size_t)rows * TL;
     double* sY = tiles + (size_t)tpc * tile_elems;
@@ -142,20 +144,17 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     // ROUND 1 for `item`: my first two rows -> prev's high halo, my last two
     // rows -> next's low halo (read straight from my block in HBM)
     auto publish_halo = [&](long long item) {
-        const long long tile = item * tpc + tl;
-        const long long ln = tile * TL + lane;
-        if (ln >= p.lines) return;                      // whole half-warp
+        const long long ln = (item * tpc + tl) * TL + lane;
+        if (ln >= p.lines) return;
         const double* ub = p.u + line_base(ln, rows, p.sz);
         const long long hb = halo_base(ln, p.sz);
         if (first_chunk && A.mail_prev) {
-            A.mail_prev[mb.h_hi() + hb] = __ldg(ub);
-            A.mail_prev[mb.h_hi() + hb + sz] = __ldg(ub + sz);
-            half_publish(A.mail_prev, mb.f_hhi() + tile, A.epoch, hmask, lane);
+            post(A.mail_prev + par + mb.h_hi() + hb, __ldg(ub));
+            post(A.mail_prev + par + mb.h_hi() + hb + sz, __ldg(ub + sz));
         }
         if (last_chunk && A.mail_next) {
-            A.mail_next[mb.h_lo() + hb] = __ldg(ub + (long long)(rows - 2) * sz);
-            A.mail_next[mb.h_lo() + hb + sz] = __ldg(ub + (long long)(rows - 1) * sz);
-            half_publish(A.mail_next, mb.f_hlo() + tile, A.epoch, hmask, lane);
+            post(A.mail_next + par + mb.h_lo() + hb, __ldg(ub + (long long)(rows - 2) * sz));
+            post(A.mail_next + par + mb.h_lo() + hb + sz, __ldg(ub + (long long)(rows - 1) * sz));
         }
     };
 
@@ -172,8 +171,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     uint32_t phase = 0;
 
     for (int it = 0; item < p.items; item += gridDim.x, ++it) {
-        const long long tile = item * tpc + tl;
-        const long long line = tile * TL + lane;
+        const long long line = (item * tpc + tl) * TL + lane;
         const bool valid = line < p.lines;
         const long long nxt = item + gridDim.x;
         if (nxt < p.items) publish_halo(nxt);          // one item ahead
@@ -183,16 +181,16 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         phase ^= 1u;
         const double* tl_tile = tiles + tl * tile_elems;
         double v[M + 4];
-        // halos of the rank block come from the neighbours' ROUND-1 stores
+        // halos of the rank block come from the neighbours' ROUND-1 posts
         double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
         const long long hb = valid ? halo_base(line, p.sz) : 0;
-        if (valid && first_chunk && A.mail_prev && half_wait(A, mb, mb.f_hlo() + tile, hmask, lane)) {
-            h0 = ld_relaxed_sys(A.mail + mb.h_lo() + hb);
-            h1 = ld_relaxed_sys(A.mail + mb.h_lo() + hb + sz);
+        if (valid && first_chunk && A.mail_prev) {
+            h0 = take(A.mail + par + mb.h_lo() + hb, A, err);
+            h1 = take(A.mail + par + mb.h_lo() + hb + sz, A, err);
         }
-        if (valid && last_chunk && A.mail_next && half_wait(A, mb, mb.f_hhi() + tile, hmask, lane)) {
-            h2 = ld_relaxed_sys(A.mail + mb.h_hi() + hb);
-            h3 = ld_relaxed_sys(A.mail + mb.h_hi() + hb + sz);
+        if (valid && last_chunk && A.mail_next) {
+            h2 = take(A.mail + par + mb.h_hi() + hb, A, err);
+            h3 = take(A.mail + par + mb.h_hi() + hb + sz, A, err);
         }
 #pragma unroll
         for (int i = 0; i < M + 4; ++i) {
@@ -226,30 +224,20 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
                 if (first_chunk) g0y = fma(__ldg(p.g + q), y, g0y);
                 if (last_chunk) g1y = fma(__ldg(p.g + K + q), y, g1y);
             }
-            if (first_chunk) {
-                if (A.mail_prev) {
-                    A.mail_prev[mb.d_from_next() + line] = g0y;
-                    half_publish(A.mail_prev, mb.f_dnext() + tile, A.epoch, hmask, lane);
-                }
-            }
-            if (last_chunk) {
-                if (A.mail_next) {
-                    A.mail_next[mb.d_from_prev() + line] = g1y;
-                    half_publish(A.mail_next, mb.f_dprev() + tile, A.epoch, hmask, lane);
-                }
-            }
+            if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, g0y);
+            if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, g1y);
             if (first_chunk) {
                 double us = g0y;
-                if (p.has_prev && half_wait(A, mb, mb.f_dprev() + tile, hmask, lane)) {
-                    const double prev_last = ld_relaxed_sys(A.mail + mb.d_from_prev() + line);
+                if (p.has_prev) {
+                    const double prev_last = take(A.mail + par + mb.d_from_prev() + line, A, err);
                     us = (g0y - p.sa_first * prev_last) / p.det_prev;
                 }
                 P[lane] = us;
             }
             if (last_chunk) {
                 double ue = g1y;
-                if (p.has_next && half_wait(A, mb, mb.f_dnext() + tile, hmask, lane)) {
-                    const double next_first = ld_relaxed_sys(A.mail + mb.d_from_next() + line);
+                if (p.has_next) {
+                    const double next_first = take(A.mail + par + mb.d_from_next() + line, A, err);
                     ue = (g1y - p.sc_last * next_first) / p.det_next;
                 }
                 P[TL + lane] = ue;
@@ -304,10 +292,7 @@ int launch_dd_t(const DDArgs& A0, long long tiles, cudaStream_t s) {
 
 }  // namespace
 
-long long dd_mail_words(long long lines) {
-    Mail mb{lines, (lines + TL - 1) / TL};
-    return mb.words();
-}
+long long dd_mail_words(long long lines) { return Mail{lines}.words(); }
 
 bool dd_eligible(int M, const FastArgs& a) {
     if (const char* e = getenv("TDS_FUSED"))
@@ -327,8 +312,10 @@ int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail
     A.timeout_ns = 10ULL * 1000 * 1000 * 1000;   // 10 s: a stall records an error
     if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
         A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
-    if (M == 32) return uniform ? launch_dd_t<32, true>(A, tiles, s) : launch_dd_t<32, false>(A, tiles, s);
-    if (M == 16) return uniform ? launch_dd_t<16, true>(A, tiles, s) : launch_dd_t<16, false>(A, tiles, s);
+    if (M == 32)
+        return uniform ? launch_dd_t<32, true>(A, tiles, s) : launch_dd_t<32, false>(A, tiles, s);
+    if (M == 16)
+        return uniform ? launch_dd_t<16, true>(A, tiles, s) : launch_dd_t<16, false>(A, tiles, s);
     return set_err(TDS_ERR_UNSUPPORTED, "unsupported chunk size");
 }
 
