@@ -3,7 +3,7 @@
 // -- in ONE kernel launch, 16 B/point of HBM traffic.
 //
 // Each rank owns a MAILBOX in its HBM that its neighbours map through CUDA
-// IPC (NVLink peer memory). Per tile of 16 lines:
+// IPC (NVLink peer memory). Per tile of TLT lines:
 //   ROUND 1 (halo, transport.py:142-171): the rank stores its first two rows
 //     into prev's mailbox and its last two rows into next's, one item AHEAD
 //     of use;
@@ -78,8 +78,10 @@ __device__ __forceinline__ unsigned long long ld_sys_u64(const double* p) {
     return v;
 }
 // wait for a neighbour's value in my mailbox slot, consume it, re-arm the slot
-__device__ double take(double* slot, const DDArgs& A, unsigned long long* err) {
-    unsigned long long v = ld_sys_u64(slot);
+// (v: the slot's value if already loaded, else SENTINEL)
+__device__ double take_v(double* slot, unsigned long long v, const DDArgs& A,
+                         unsigned long long* err) {
+    if (v == SENTINEL) v = ld_sys_u64(slot);
     if (v == SENTINEL) {
         const unsigned long long t0 = globaltimer();
         unsigned ns = 32;
@@ -98,10 +100,13 @@ __device__ double take(double* slot, const DDArgs& A, unsigned long long* err) {
     *reinterpret_cast<unsigned long long*>(slot) = SENTINEL;
     return __longlong_as_double((long long)v);
 }
+__device__ __forceinline__ double take(double* slot, const DDArgs& A, unsigned long long* err) {
+    return take_v(slot, SENTINEL, A, err);
+}
 
 }  // namespace
 
-template <int M, bool UNIFORM>
+template <int M, bool UNIFORM, int TLT>
 __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     const FastArgs& p = A.t.f;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -110,51 +115,54 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     const int rows = p.rows;
     const int tpc = p.tiles_per_cta;
     const int t = threadIdx.x;
-    const int lane = t % TL;
-    const int chunk = (t / TL) % C;
-    const int tl = t / (TL * C);
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
     const long long sz = p.sz;
     const int r0 = chunk * M;
     const Mail mb{p.lines};
     const long long par = mb.half(A.epoch);
     unsigned long long* err = reinterpret_cast<unsigned long long*>(A.mail + mb.err());
     double* tiles = reinterpret_cast<double*>(smem);
-    const size_t tile_elems = (size_t)rows * TL;
+    const size_t tile_elems = (size_t)rows * TLT;
     double* sY = tiles + (size_t)tpc * tile_elems;
-    const size_t ybuf = (size_t)tpc * K * TL;
-    double* sP = sY + 2 * ybuf;                        // pins: [tpc][2][TL]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sP + (size_t)tpc * 2 * TL);
+    const size_t ybuf = (size_t)tpc * K * TLT;
+    double* sP = sY + 2 * ybuf;                        // pins: [tpc][2][TLT]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sP + (size_t)tpc * 2 * TLT);
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
     const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
 
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
         for (int j = 0; j < tpc; ++j)
-            if ((item * tpc + j) * TL < p.lines) bytes += (uint32_t)(tile_elems * sizeof(double));
+            if ((item * tpc + j) * TLT < p.lines) bytes += (uint32_t)(tile_elems * sizeof(double));
         mbar_expect_tx(bar, bytes);
         for (int j = 0; j < tpc; ++j) {
-            const long long first = (item * tpc + j) * TL;
+            const long long first = (item * tpc + j) * TLT;
             if (first >= p.lines) break;
             const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
             for (int b = 0; b * A.t.boxr < rows; ++b)
-                tma_load_3d(tiles + j * tile_elems + (size_t)b * A.t.boxr * TL, &A.t.map, bar,
+                tma_load_3d(tiles + j * tile_elems + (size_t)b * A.t.boxr * TLT, &A.t.map, bar,
                             l0, b * A.t.boxr, g);
         }
     };
     // ROUND 1 for `item`: my first two rows -> prev's high halo, my last two
     // rows -> next's low halo (read straight from my block in HBM)
     auto publish_halo = [&](long long item) {
-        const long long ln = (item * tpc + tl) * TL + lane;
+        const long long ln = (item * tpc + tl) * TLT + lane;
         if (ln >= p.lines) return;
         const double* ub = p.u + line_base(ln, rows, p.sz);
         const long long hb = halo_base(ln, p.sz);
         if (first_chunk && A.mail_prev) {
-            post(A.mail_prev + par + mb.h_hi() + hb, __ldg(ub));
-            post(A.mail_prev + par + mb.h_hi() + hb + sz, __ldg(ub + sz));
+            const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
+            post(A.mail_prev + par + mb.h_hi() + hb, a0);
+            post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
         }
         if (last_chunk && A.mail_next) {
-            post(A.mail_next + par + mb.h_lo() + hb, __ldg(ub + (long long)(rows - 2) * sz));
-            post(A.mail_next + par + mb.h_lo() + hb + sz, __ldg(ub + (long long)(rows - 1) * sz));
+            const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
+            const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
+            post(A.mail_next + par + mb.h_lo() + hb, a0);
+            post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
         }
     };
 
@@ -171,10 +179,23 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     uint32_t phase = 0;
 
     for (int it = 0; item < p.items; item += gridDim.x, ++it) {
-        const long long line = (item * tpc + tl) * TL + lane;
+        const long long line = (item * tpc + tl) * TLT + lane;
         const bool valid = line < p.lines;
         const long long nxt = item + gridDim.x;
         if (nxt < p.items) publish_halo(nxt);          // one item ahead
+        // halo slots of this item: loads in flight across the TMA wait
+        const long long hb = valid ? halo_base(line, p.sz) : 0;
+        double* hlo = (valid && first_chunk && A.mail_prev) ? A.mail + par + mb.h_lo() + hb : nullptr;
+        double* hhi = (valid && last_chunk && A.mail_next) ? A.mail + par + mb.h_hi() + hb : nullptr;
+        unsigned long long a0 = SENTINEL, a1 = SENTINEL, b0 = SENTINEL, b1 = SENTINEL;
+        if (hlo) {
+            a0 = ld_sys_u64(hlo);
+            a1 = ld_sys_u64(hlo + sz);
+        }
+        if (hhi) {
+            b0 = ld_sys_u64(hhi);
+            b1 = ld_sys_u64(hhi + sz);
+        }
 
         while (!mbar_try_wait(bar, phase)) {
         }
@@ -183,14 +204,13 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         double v[M + 4];
         // halos of the rank block come from the neighbours' ROUND-1 posts
         double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
-        const long long hb = valid ? halo_base(line, p.sz) : 0;
-        if (valid && first_chunk && A.mail_prev) {
-            h0 = take(A.mail + par + mb.h_lo() + hb, A, err);
-            h1 = take(A.mail + par + mb.h_lo() + hb + sz, A, err);
+        if (hlo) {
+            h0 = take_v(hlo, a0, A, err);
+            h1 = take_v(hlo + sz, a1, A, err);
         }
-        if (valid && last_chunk && A.mail_next) {
-            h2 = take(A.mail + par + mb.h_hi() + hb, A, err);
-            h3 = take(A.mail + par + mb.h_hi() + hb + sz, A, err);
+        if (hhi) {
+            h2 = take_v(hhi, b0, A, err);
+            h3 = take_v(hhi + sz, b1, A, err);
         }
 #pragma unroll
         for (int i = 0; i < M + 4; ++i) {
@@ -198,7 +218,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             double x;
             if (row < 0) x = (i == 0) ? h0 : h1;
             else if (row >= rows) x = (row == rows) ? h2 : h3;
-            else x = tl_tile[row * TL + lane];
+            else x = tl_tile[row * TLT + lane];
             v[i] = x;
         }
         __syncthreads();   // tile buffer free
@@ -210,17 +230,22 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         double d[M];
         chunk_sweeps<M, UNIFORM>(p, tb, v, d);
 
-        double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TL;
-        Y[(2 * chunk) * TL + lane] = d[0];
-        Y[(2 * chunk + 1) * TL + lane] = d[M - 1];
+        double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TLT;
+        Y[(2 * chunk) * TLT + lane] = d[0];
+        Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
         __syncthreads();
 
+        // pin-independent part of the reduced map first (overlaps the
+        // edge warps' ROUND 2 below)
+        double F, L;
+        chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr, nullptr,
+                          F, L);
         // ROUND 2: the rank's decoupled boundary rows, 2x2 pairs, pins
-        double* P = sP + (size_t)tl * 2 * TL;
+        double* P = sP + (size_t)tl * 2 * TLT;
         if (valid && (first_chunk || last_chunk)) {
             double g0y = 0.0, g1y = 0.0;
             for (int q = 0; q < K; ++q) {
-                const double y = Y[q * TL + lane];
+                const double y = Y[q * TLT + lane];
                 if (first_chunk) g0y = fma(__ldg(p.g + q), y, g0y);
                 if (last_chunk) g1y = fma(__ldg(p.g + K + q), y, g1y);
             }
@@ -240,13 +265,18 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
                     const double next_first = take(A.mail + par + mb.d_from_next() + line, A, err);
                     ue = (g1y - p.sc_last * next_first) / p.det_next;
                 }
-                P[TL + lane] = ue;
+                P[TLT + lane] = ue;
             }
         }
         __syncthreads();
 
-        double F, L;
-        chunk_bounds(p.Hp + (size_t)chunk * K, Y, K, lane, P, P + TL, F, L);
+        {
+            const double2 h0 = __ldg(p.Hp + (size_t)chunk * K);
+            const double2 hl = __ldg(p.Hp + (size_t)chunk * K + K - 1);
+            const double us = P[lane], ue = P[TLT + lane];
+            F = fma(h0.x, us, fma(hl.x, ue, F));
+            L = fma(h0.y, us, fma(hl.y, ue, L));
+        }
         if (valid)
             chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F, L,
                                     A.t.store_cs != 0);
@@ -255,22 +285,26 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
 
 namespace {
 
-size_t dd_smem(const FastArgs& a) { return tma_smem(a) + (size_t)a.tiles_per_cta * 2 * TL * 8; }
+size_t dd_smem(const FastArgs& a, TileCfg c) {
+    return tma_smem(a, c) + (size_t)c.tpc * 2 * c.tl * 8;
+}
 
-template <int M, bool UNI>
-int launch_dd_t(const DDArgs& A0, long long tiles, cudaStream_t s) {
+template <int M, bool UNI, int TLT>
+int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     DDArgs A = A0;
     FastArgs& a = A.t.f;
-    a.items = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+    a.tiles_per_cta = cfg.tpc;
+    const long long tiles = (a.lines + TLT - 1) / TLT;
+    a.items = (tiles + cfg.tpc - 1) / cfg.tpc;
     if (a.items <= 0) return TDS_OK;
-    int rc = encode_field_map(a, M, &A.t.map, &A.t.boxr);
+    int rc = encode_field_map(a, M, TLT, &A.t.map, &A.t.boxr);
     if (rc) return rc;
     A.t.store_cs = store_policy();
-    const int threads = a.tiles_per_cta * a.chunks * TL;
-    const size_t smem = dd_smem(a);
+    const int threads = cfg.tpc * a.chunks * TLT;
+    const size_t smem = dd_smem(a, cfg);
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_dd<M, UNI>,
+        rc = cuda_check(cudaFuncSetAttribute(k_dd<M, UNI, TLT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem),
                         "cudaFuncSetAttribute(k_dd)");
@@ -280,14 +314,21 @@ int launch_dd_t(const DDArgs& A0, long long tiles, cudaStream_t s) {
     int dev = 0, sms = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd<M, UNI>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd<M, UNI, TLT>, threads, smem);
     if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
     // exactly the resident capacity: every CTA is co-resident (no waits on
     // unscheduled CTAs); identical on every rank
     long long grid = (long long)nb * sms;
     if (grid > a.items) grid = a.items;
-    k_dd<M, UNI><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_dd<M, UNI, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd launch");
+}
+
+template <int M, bool UNI>
+int launch_dd_m(const DDArgs& A, cudaStream_t s) {
+    const TileCfg cfg = tile_cfg(A.t.f);
+    if (cfg.tl == 8) return launch_dd_t<M, UNI, 8>(A, cfg, s);
+    return launch_dd_t<M, UNI, 16>(A, cfg, s);
 }
 
 }  // namespace
@@ -298,11 +339,11 @@ bool dd_eligible(int M, const FastArgs& a) {
     if (const char* e = getenv("TDS_FUSED"))
         if (e[0] == '0') return false;
     if (!tma_eligible(M, a)) return false;
-    return dd_smem(a) <= 200 * 1024;
+    return dd_smem(a, tile_cfg(a)) <= 200 * 1024;
 }
 
 int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
-              double* mail_next, unsigned long long epoch, long long tiles, cudaStream_t s) {
+              double* mail_next, unsigned long long epoch, long long /*tiles*/, cudaStream_t s) {
     DDArgs A;
     A.t.f = a;
     A.mail = mail;
@@ -312,10 +353,8 @@ int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail
     A.timeout_ns = 10ULL * 1000 * 1000 * 1000;   // 10 s: a stall records an error
     if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
         A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
-    if (M == 32)
-        return uniform ? launch_dd_t<32, true>(A, tiles, s) : launch_dd_t<32, false>(A, tiles, s);
-    if (M == 16)
-        return uniform ? launch_dd_t<16, true>(A, tiles, s) : launch_dd_t<16, false>(A, tiles, s);
+    if (M == 32) return uniform ? launch_dd_m<32, true>(A, s) : launch_dd_m<32, false>(A, s);
+    if (M == 16) return uniform ? launch_dd_m<16, true>(A, s) : launch_dd_m<16, false>(A, s);
     return set_err(TDS_ERR_UNSUPPORTED, "unsupported chunk size");
 }
 

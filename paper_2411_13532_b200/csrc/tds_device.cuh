@@ -114,8 +114,9 @@ __device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __
 }
 
 // Chunk boundary values (F, L) = rows 2k, 2k+1 of H applied to the reduced
-// rhs Y (K entries, stride TL in shared memory). If pins are given, Y[0] and
+// rhs Y (K entries, stride TLT in shared memory). If pins are given, Y[0] and
 // Y[K-1] are replaced by pin0 / pin1 (the rank's u_start / u_end).
+template <int TLT>
 __device__ __forceinline__ void chunk_bounds(const double2* __restrict__ hr, const double* Y,
                                              int K, int lane, const double* pin0,
                                              const double* pin1, double& F, double& L) {
@@ -136,8 +137,8 @@ __device__ __forceinline__ void chunk_bounds(const double2* __restrict__ hr, con
     for (; q + 1 < q1; q += 2) {
         const double2 h0 = __ldg(hr + q);
         const double2 h1 = __ldg(hr + q + 1);
-        const double ya = Y[q * TL + lane];
-        const double yb = Y[(q + 1) * TL + lane];
+        const double ya = Y[q * TLT + lane];
+        const double yb = Y[(q + 1) * TLT + lane];
         F0 = fma(h0.x, ya, F0);
         L0 = fma(h0.y, ya, L0);
         F1 = fma(h1.x, yb, F1);
@@ -145,7 +146,7 @@ __device__ __forceinline__ void chunk_bounds(const double2* __restrict__ hr, con
     }
     if (q < q1) {
         const double2 h0 = __ldg(hr + q);
-        const double ya = Y[q * TL + lane];
+        const double ya = Y[q * TLT + lane];
         F0 = fma(h0.x, ya, F0);
         L0 = fma(h0.y, ya, L0);
     }

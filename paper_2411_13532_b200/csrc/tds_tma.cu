@@ -5,15 +5,17 @@
 // values, Alg. 7 substitution, one store -- but the input tile reaches the
 // CTA through the Tensor Memory Accelerator:
 //   * a 3-D tensor map views the field as (groups, rows, sz) fp64; one box
-//     is 16 lanes (128 B) x up to 256 rows, so a tile of 16 lines is one to
-//     a few cp.async.bulk.tensor loads completing on an mbarrier;
+//     is TLT lanes (TLT x 8 bytes) x up to 256 rows, so a tile of TLT lines
+//     is one to a few cp.async.bulk.tensor loads completing on an mbarrier;
 //   * the CTA is persistent (resident CTAs x SMs) and issues the NEXT item's
 //     TMA as soon as every thread has copied the current tile from shared
 //     memory into registers, so HBM reads stay in flight through the sweeps,
 //     the reduced solve, the substitution and the stores of this item --
 //     without spending registers on the prefetch.
-// Eligible when sz % 16 == 0 (rows of whole 128-byte segments), the field is
-// 16-byte aligned and a tile fits in shared memory.
+// TLT (lines per tile) is 16 (128-byte row segments, 256-thread CTAs) or 8
+// (64-byte segments, 128-thread CTAs: twice the independent items per SM).
+// Eligible when sz % TLT == 0, the field is 16-byte aligned and a tile fits
+// in shared memory.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -25,7 +27,7 @@ namespace tds {
 
 using namespace dev;
 
-template <int M, int MODE, bool UNIFORM>
+template <int M, int MODE, bool UNIFORM, int TLT>
 __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) {
     const FastArgs& p = A.f;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -34,29 +36,29 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     const int rows = p.rows;
     const int tpc = p.tiles_per_cta;
     const int t = threadIdx.x;
-    const int lane = t % TL;
-    const int chunk = (t / TL) % C;
-    const int tl = t / (TL * C);
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
     const long long sz = p.sz;
     const int r0 = chunk * M;
     double* tiles = reinterpret_cast<double*>(smem);
-    const size_t tile_elems = (size_t)rows * TL;
+    const size_t tile_elems = (size_t)rows * TLT;
     double* sY = tiles + (size_t)tpc * tile_elems;
-    const size_t ybuf = (size_t)tpc * K * TL;
+    const size_t ybuf = (size_t)tpc * K * TLT;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sY + 2 * ybuf);
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
 
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
         for (int j = 0; j < tpc; ++j)
-            if ((item * tpc + j) * TL < p.lines) bytes += (uint32_t)(tile_elems * sizeof(double));
+            if ((item * tpc + j) * TLT < p.lines) bytes += (uint32_t)(tile_elems * sizeof(double));
         mbar_expect_tx(bar, bytes);
         for (int j = 0; j < tpc; ++j) {
-            const long long first = (item * tpc + j) * TL;
+            const long long first = (item * tpc + j) * TLT;
             if (first >= p.lines) break;
             const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
             for (int b = 0; b * A.boxr < rows; ++b)
-                tma_load_3d(tiles + j * tile_elems + (size_t)b * A.boxr * TL, &A.map, bar, l0,
+                tma_load_3d(tiles + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map, bar, l0,
                             b * A.boxr, g);
         }
     };
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     uint32_t phase = 0;
 
     for (int it = 0; item < p.items; item += gridDim.x, ++it) {
-        const long long line = (item * tpc + tl) * TL + lane;
+        const long long line = (item * tpc + tl) * TLT + lane;
         const bool valid = line < p.lines;
 
         while (!mbar_try_wait(bar, phase)) {
@@ -87,18 +89,18 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
             double x = 0.0;
             if (i < 2 || i >= M + 2) {
                 if (row < 0) {
-                    if (p.edge_mode == EDGE_WRAP) x = tile[(row + rows) * TL + lane];
+                    if (p.edge_mode == EDGE_WRAP) x = tile[(row + rows) * TLT + lane];
                     else if (p.edge_mode == EDGE_HALO && p.halo_lo && valid)
                         x = __ldg(p.halo_lo + hb + (row + 2) * sz);
                 } else if (row >= rows) {
-                    if (p.edge_mode == EDGE_WRAP) x = tile[(row - rows) * TL + lane];
+                    if (p.edge_mode == EDGE_WRAP) x = tile[(row - rows) * TLT + lane];
                     else if (p.edge_mode == EDGE_HALO && p.halo_hi && valid)
                         x = __ldg(p.halo_hi + hb + (row - rows) * sz);
                 } else {
-                    x = tile[row * TL + lane];
+                    x = tile[row * TLT + lane];
                 }
             } else {
-                x = tile[row * TL + lane];
+                x = tile[row * TLT + lane];
             }
             v[i] = x;
         }
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         double d[M];
         chunk_sweeps<M, UNIFORM>(p, tb, v, d);
 
-        double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TL;
+        double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TLT;
         double y0 = d[0], yL = d[M - 1];
         if (MODE == MODE_PASS_B) {
             if (chunk == 0 && valid) {
@@ -126,26 +128,26 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
                 yL = p.has_next ? (dl - p.sc_last * p.next_first[line]) / p.det_next : dl;
             }
         }
-        Y[(2 * chunk) * TL + lane] = y0;
-        Y[(2 * chunk + 1) * TL + lane] = yL;
+        Y[(2 * chunk) * TLT + lane] = y0;
+        Y[(2 * chunk + 1) * TLT + lane] = yL;
         __syncthreads();
 
         if (MODE == MODE_PASS_A) {
             if (valid && chunk == 0) {
                 double s = 0.0;
-                for (int q = 0; q < K; ++q) s = fma(__ldg(p.g + q), Y[q * TL + lane], s);
+                for (int q = 0; q < K; ++q) s = fma(__ldg(p.g + q), Y[q * TLT + lane], s);
                 p.d_first_out[line] = s;
             }
             if (valid && chunk == C - 1) {
                 double s = 0.0;
-                for (int q = 0; q < K; ++q) s = fma(__ldg(p.g + K + q), Y[q * TL + lane], s);
+                for (int q = 0; q < K; ++q) s = fma(__ldg(p.g + K + q), Y[q * TLT + lane], s);
                 p.d_last_out[line] = s;
             }
             continue;
         }
 
         double F, L;
-        chunk_bounds(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+        chunk_bounds<TLT>(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
         if (valid)
             chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, p.rows, p.sz), sz, r0, d, F,
                                     L, A.store_cs != 0);
@@ -154,20 +156,22 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
 
 namespace {
 
-template <int M, int MODE, bool UNI>
-int launch_tma_t(const FastArgs& a, long long tiles, cudaStream_t s) {
+template <int M, int MODE, bool UNI, int TLT>
+int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     TmaArgs A;
     A.f = a;
-    A.f.items = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+    A.f.tiles_per_cta = cfg.tpc;
+    const long long tiles = (a.lines + TLT - 1) / TLT;
+    A.f.items = (tiles + cfg.tpc - 1) / cfg.tpc;
     if (A.f.items <= 0) return TDS_OK;
-    int rc = encode_field_map(a, M, &A.map, &A.boxr);
+    int rc = encode_field_map(a, M, TLT, &A.map, &A.boxr);
     if (rc) return rc;
     A.store_cs = store_policy();
-    const int threads = a.tiles_per_cta * a.chunks * TL;
-    const size_t smem = tma_smem(a);
+    const int threads = cfg.tpc * a.chunks * TLT;
+    const size_t smem = tma_smem(a, cfg);
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_tma<M, MODE, UNI>,
+        rc = cuda_check(cudaFuncSetAttribute(k_tma<M, MODE, UNI, TLT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem),
                         "cudaFuncSetAttribute(k_tma)");
@@ -177,12 +181,19 @@ int launch_tma_t(const FastArgs& a, long long tiles, cudaStream_t s) {
     int dev = 0, sms = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tma<M, MODE, UNI>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tma<M, MODE, UNI, TLT>, threads, smem);
     if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_tma does not fit on an SM");
     long long grid = (long long)nb * sms;
     if (grid > A.f.items) grid = A.f.items;
-    k_tma<M, MODE, UNI><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_tma<M, MODE, UNI, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_tma launch");
+}
+
+template <int M, int MODE, bool UNI>
+int launch_tma_m(const FastArgs& a, cudaStream_t s) {
+    const TileCfg cfg = tile_cfg(a);
+    if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
+    return launch_tma_t<M, MODE, UNI, 16>(a, cfg, s);
 }
 
 }  // namespace
@@ -200,9 +211,22 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-size_t tma_smem(const FastArgs& a) {
-    return (size_t)a.tiles_per_cta * a.rows * TL * sizeof(double) +
-           (size_t)2 * a.tiles_per_cta * 2 * a.chunks * TL * sizeof(double) + 16;
+TileCfg tile_cfg(const FastArgs& a) {
+    int tl = 16;
+    if (const char* e = getenv("TDS_TL")) tl = atoi(e) == 8 ? 8 : 16;
+    if (a.sz % tl != 0) tl = (a.sz % 8 == 0) ? 8 : 0;
+    TileCfg c{tl, 1};
+    if (tl) {
+        const int per_tile = a.chunks * tl;
+        const int target = tl == 8 ? 128 : 256;
+        c.tpc = per_tile >= target ? 1 : target / per_tile;
+    }
+    return c;
+}
+
+size_t tma_smem(const FastArgs& a, TileCfg c) {
+    return (size_t)c.tpc * a.rows * c.tl * sizeof(double) +
+           (size_t)2 * c.tpc * 2 * a.chunks * c.tl * sizeof(double) + 16;
 }
 
 int box_rows(int rows, int M) {
@@ -218,17 +242,19 @@ int store_policy() {
     return cs;
 }
 
-int encode_field_map(const FastArgs& a, int M, CUtensorMap* map, int* boxr) {
+int encode_field_map(const FastArgs& a, int M, int tl, CUtensorMap* map, int* boxr) {
     *boxr = box_rows(a.rows, M);
-    CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    CUtensorMapL2promotion prom =
+        tl == 16 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     if (const char* e = getenv("TDS_L2PROMO")) {
         if (e[0] == '0') prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
         else if (e[0] == '1') prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        else if (e[0] == '2') prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     }
     const long long groups = a.lines / a.sz;
     cuuint64_t dims[3] = {(cuuint64_t)a.sz, (cuuint64_t)a.rows, (cuuint64_t)groups};
     cuuint64_t strides[2] = {(cuuint64_t)a.sz * 8, (cuuint64_t)a.rows * a.sz * 8};
-    cuuint32_t box[3] = {(cuuint32_t)TL, (cuuint32_t)*boxr, 1};
+    cuuint32_t box[3] = {(cuuint32_t)tl, (cuuint32_t)*boxr, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.u),
                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -241,26 +267,27 @@ int encode_field_map(const FastArgs& a, int M, CUtensorMap* map, int* boxr) {
 bool tma_eligible(int M, const FastArgs& a) {
     if (const char* e = getenv("TDS_TMA"))
         if (e[0] == '0') return false;
-    if (a.sz % TL != 0) return false;
+    const TileCfg c = tile_cfg(a);
+    if (c.tl == 0) return false;
     if (reinterpret_cast<uintptr_t>(a.u) % 16 != 0) return false;
     if (box_rows(a.rows, M) == 0) return false;
-    if (tma_smem(a) > 200 * 1024) return false;
+    if (tma_smem(a, c) > 200 * 1024) return false;
     return encode_fn() != nullptr;
 }
 
-int launch_tma(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
+int launch_tma(int M, int mode, bool uniform, const FastArgs& a, long long /*tiles*/,
                cudaStream_t s) {
-#define DISPATCH_MODE(MM)                                                           \
-    switch (mode) {                                                                 \
-        case MODE_SOLVE:                                                            \
-            return uniform ? launch_tma_t<MM, MODE_SOLVE, true>(a, tiles, s)        \
-                           : launch_tma_t<MM, MODE_SOLVE, false>(a, tiles, s);      \
-        case MODE_PASS_A:                                                           \
-            return uniform ? launch_tma_t<MM, MODE_PASS_A, true>(a, tiles, s)       \
-                           : launch_tma_t<MM, MODE_PASS_A, false>(a, tiles, s);     \
-        default:                                                                    \
-            return uniform ? launch_tma_t<MM, MODE_PASS_B, true>(a, tiles, s)       \
-                           : launch_tma_t<MM, MODE_PASS_B, false>(a, tiles, s);     \
+#define DISPATCH_MODE(MM)                                                               \
+    switch (mode) {                                                                     \
+        case MODE_SOLVE:                                                                \
+            return uniform ? launch_tma_m<MM, MODE_SOLVE, true>(a, s)                   \
+                           : launch_tma_m<MM, MODE_SOLVE, false>(a, s);                 \
+        case MODE_PASS_A:                                                               \
+            return uniform ? launch_tma_m<MM, MODE_PASS_A, true>(a, s)                  \
+                           : launch_tma_m<MM, MODE_PASS_A, false>(a, s);                \
+        default:                                                                        \
+            return uniform ? launch_tma_m<MM, MODE_PASS_B, true>(a, s)                  \
+                           : launch_tma_m<MM, MODE_PASS_B, false>(a, s);                \
     }
     if (M == 32) { DISPATCH_MODE(32) }
     if (M == 16) { DISPATCH_MODE(16) }

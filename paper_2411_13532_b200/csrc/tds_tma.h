@@ -15,11 +15,18 @@ struct TmaArgs {
     int store_cs;      // streaming stores (A/B knob TDS_STCS)
 };
 
+// lines per tile (8 or 16; 0 = not TMA-eligible) and tiles per CTA
+struct TileCfg {
+    int tl;
+    int tpc;
+};
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
-size_t tma_smem(const FastArgs& a);
+TileCfg tile_cfg(const FastArgs& a);   // A/B knob TDS_TL=8|16
+size_t tma_smem(const FastArgs& a, TileCfg c);
 int box_rows(int rows, int M);
 int store_policy();
-// 3-D tensor map (lanes, rows, groups) over the field a.u; box 16 x boxr x 1
-int encode_field_map(const FastArgs& a, int M, CUtensorMap* map, int* boxr);
+// 3-D tensor map (lanes, rows, groups) over the field a.u; box tl x boxr x 1
+int encode_field_map(const FastArgs& a, int M, int tl, CUtensorMap* map, int* boxr);
 
 }  // namespace tds
