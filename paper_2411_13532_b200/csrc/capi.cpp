@@ -41,6 +41,8 @@ tds::FastArgs fast_args(const tds_plan* p, long long lines, int sz) {
     a.det_prev = p->det_prev;
     a.det_next = p->det_next;
     a.ut = p->ut;
+    a.dd_defer16 = p->dd_defer[0];
+    a.dd_defer8 = p->dd_defer[1];
     return a;
 }
 

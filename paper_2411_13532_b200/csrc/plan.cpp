@@ -438,6 +438,31 @@ int build_local(tds_plan* p, const Global& loc, int has_prev, int has_next, doub
         vector<double> gv(size_t(2) * rm.K);
         std::copy(rm.g0.begin(), rm.g0.end(), gv.begin());
         std::copy(rm.g1.begin(), rm.g1.end(), gv.begin() + rm.K);
+        // Fused kernel with deferred edges (k_dd2): a chunk outside the first
+        // / last warp of its tile is finished without the rank's u_start /
+        // u_end. Allowed only if every coefficient through which they reach
+        // that chunk's rows is <= 2^-70; since u_start, u_end are themselves
+        // entries of the solution, the omitted terms are < 2^-70 max|out|.
+        const int C = cs.C, K = rm.K;
+        const double eps = std::ldexp(1.0, -70);
+        auto pin_free = [&](int k, int col) {
+            const double hF = rm.Hpin[size_t(2 * k) * K + col];
+            const double hL = rm.Hpin[size_t(2 * k + 1) * K + col];
+            double worst = std::fmax(std::fabs(hF), std::fabs(hL));
+            for (int i = 1; i < M - 1; ++i)
+                worst = std::fmax(worst, std::fabs(cs.co[k].sa[i] * hF + cs.co[k].sc[i] * hL));
+            return worst <= eps;
+        };
+        for (int v = 0; v < 2; ++v) {
+            const int cw = v == 0 ? 2 : 4;   // chunks per warp for 16 / 8 lines per tile
+            bool ok = C >= cw && C % cw == 0;
+            for (int k = 0; k < C && ok; ++k) {
+                const int wg = k / cw;
+                if (wg != 0 && !pin_free(k, 0)) ok = false;
+                if (wg != (C - 1) / cw && !pin_free(k, K - 1)) ok = false;
+            }
+            p->dd_defer[v] = ok ? 1 : 0;
+        }
         return upload_H(p, rm.Hpin, gv);
     }
     p->path = TDS_PATH_STAGED;

@@ -283,6 +283,222 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_dd2: the fused per-rank kernel with DEFERRED EDGES. The plan guarantees
+// (plan.cpp, dd_defer) that chunks outside the first / last warp of a tile
+// depend on the rank pins u_start / u_end by less than 2^-70: those chunks
+// store their final rows in the same iteration, without waiting for the
+// neighbour. The two edge warps of a tile post ROUND 2 for item t, stash
+// their chunks (F', L', d rows, g.Y) in shared memory, and finish item t-1
+// -- whose neighbour values arrived an iteration ago -- so the NVLink round
+// trip is off the critical path.
+template <int M, bool UNIFORM, int TLT>
+__global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
+    const FastArgs& p = A.t.f;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int CW = 32 / TLT;                       // chunks per warp
+    const int C = p.chunks;
+    const int K = 2 * C;
+    const int rows = p.rows;
+    const int tpc = p.tiles_per_cta;
+    const int t = threadIdx.x;
+    const int wl = t & 31;
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
+    const int wc0 = chunk - (wl / TLT);                // first chunk of my warp
+    const bool has_first = wc0 == 0, has_last = wc0 + CW - 1 >= C - 1;
+    const bool edge_warp = has_first || has_last;
+    const long long sz = p.sz;
+    const int r0 = chunk * M;
+    const Mail mb{p.lines};
+    const long long par = mb.half(A.epoch);
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(A.mail + mb.err());
+    double* tiles = reinterpret_cast<double*>(smem);
+    const size_t tile_elems = (size_t)rows * TLT;
+    double* sY = tiles + (size_t)tpc * tile_elems;
+    const size_t ybuf = (size_t)tpc * K * TLT;
+    double* sS = sY + 2 * ybuf;                        // stash: [tpc][2][M+1][32]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sS + (size_t)tpc * 2 * (M + 1) * 32);
+    double* stash = sS + ((size_t)(2 * tl + (has_first ? 0 : 1)) * (M + 1)) * 32 + wl;
+    const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
+    const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
+
+    auto issue = [&](long long item) {
+        uint32_t bytes = 0;
+        for (int j = 0; j < tpc; ++j)
+            if ((item * tpc + j) * TLT < p.lines) bytes += (uint32_t)(tile_elems * sizeof(double));
+        mbar_expect_tx(bar, bytes);
+        for (int j = 0; j < tpc; ++j) {
+            const long long first = (item * tpc + j) * TLT;
+            if (first >= p.lines) break;
+            const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
+            for (int b = 0; b * A.t.boxr < rows; ++b)
+                tma_load_3d(tiles + j * tile_elems + (size_t)b * A.t.boxr * TLT, &A.t.map, bar,
+                            l0, b * A.t.boxr, g);
+        }
+    };
+    auto publish_halo = [&](long long item) {
+        const long long ln = (item * tpc + tl) * TLT + lane;
+        if (ln >= p.lines) return;
+        const double* ub = p.u + line_base(ln, rows, p.sz);
+        const long long hb = halo_base(ln, p.sz);
+        if (first_chunk && A.mail_prev) {
+            const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
+            post(A.mail_prev + par + mb.h_hi() + hb, a0);
+            post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
+        }
+        if (last_chunk && A.mail_next) {
+            const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
+            const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
+            post(A.mail_next + par + mb.h_lo() + hb, a0);
+            post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
+        }
+    };
+    // finish the stashed item `fi` (edge warps only; warp-synchronous)
+    auto finish = [&](long long fi) {
+        const long long fl = (fi * tpc + tl) * TLT + lane;
+        const bool fv = fl < p.lines;
+        double us = 0.0, ue = 0.0;
+        if (first_chunk) {
+            us = stash[M * 32];
+            if (fv && p.has_prev) {
+                const double prev_last = take(A.mail + par + mb.d_from_prev() + fl, A, err);
+                us = (us - p.sa_first * prev_last) / p.det_prev;
+            }
+        }
+        if (last_chunk) {
+            ue = stash[M * 32];
+            if (fv && p.has_next) {
+                const double next_first = take(A.mail + par + mb.d_from_next() + fl, A, err);
+                ue = (ue - p.sc_last * next_first) / p.det_next;
+            }
+        }
+        // broadcast the pins of each line to every chunk of this warp
+        us = __shfl_sync(0xffffffffu, us, lane);
+        ue = __shfl_sync(0xffffffffu, ue, (C - 1 - wc0) * TLT + lane);
+        const double2 h0 = __ldg(p.Hp + (size_t)chunk * K);
+        const double2 hl = __ldg(p.Hp + (size_t)chunk * K + K - 1);
+        double F = stash[0], L = stash[(M - 1) * 32];
+        if (has_first) {
+            F = fma(h0.x, us, F);
+            L = fma(h0.y, us, L);
+        }
+        if (has_last) {
+            F = fma(hl.x, ue, F);
+            L = fma(hl.y, ue, L);
+        }
+        if (!fv) return;
+        double* ob = p.out + line_base(fl, rows, p.sz);
+        __stcs(ob + (long long)r0 * sz, F);
+#pragma unroll
+        for (int i = 1; i < M - 1; ++i) {
+            const double sa = UNIFORM ? p.ut.sa[i] : __ldg(tb + i * NCOEF + 8);
+            const double sc = UNIFORM ? p.ut.sc[i] : __ldg(tb + i * NCOEF + 9);
+            __stcs(ob + (long long)(r0 + i) * sz, fma(-sc, L, fma(-sa, F, stash[i * 32])));
+        }
+        __stcs(ob + (long long)(r0 + M - 1) * sz, L);
+    };
+
+    if (t == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    long long item = blockIdx.x;
+    if (item < p.items) {
+        if (t == 0) issue(item);
+        publish_halo(item);
+    }
+    uint32_t phase = 0;
+    long long prev_item = -1;
+
+    for (int it = 0; item < p.items; item += gridDim.x, ++it) {
+        const long long line = (item * tpc + tl) * TLT + lane;
+        const bool valid = line < p.lines;
+        const long long nxt = item + gridDim.x;
+        if (nxt < p.items) publish_halo(nxt);          // one item ahead
+        const long long hb = valid ? halo_base(line, p.sz) : 0;
+        double* hlo = (valid && first_chunk && A.mail_prev) ? A.mail + par + mb.h_lo() + hb : nullptr;
+        double* hhi = (valid && last_chunk && A.mail_next) ? A.mail + par + mb.h_hi() + hb : nullptr;
+        unsigned long long a0 = SENTINEL, a1 = SENTINEL, b0 = SENTINEL, b1 = SENTINEL;
+        if (hlo) {
+            a0 = ld_sys_u64(hlo);
+            a1 = ld_sys_u64(hlo + sz);
+        }
+        if (hhi) {
+            b0 = ld_sys_u64(hhi);
+            b1 = ld_sys_u64(hhi + sz);
+        }
+
+        while (!mbar_try_wait(bar, phase)) {
+        }
+        phase ^= 1u;
+        const double* tl_tile = tiles + tl * tile_elems;
+        double v[M + 4];
+        double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+        if (hlo) {
+            h0 = take_v(hlo, a0, A, err);
+            h1 = take_v(hlo + sz, a1, A, err);
+        }
+        if (hhi) {
+            h2 = take_v(hhi, b0, A, err);
+            h3 = take_v(hhi + sz, b1, A, err);
+        }
+#pragma unroll
+        for (int i = 0; i < M + 4; ++i) {
+            const int row = r0 - 2 + i;
+            double x;
+            if (row < 0) x = (i == 0) ? h0 : h1;
+            else if (row >= rows) x = (row == rows) ? h2 : h3;
+            else x = tl_tile[row * TLT + lane];
+            v[i] = x;
+        }
+        __syncthreads();   // tile buffer free
+        if (t == 0 && nxt < p.items) {
+            fence_proxy_async();
+            issue(nxt);
+        }
+
+        double d[M];
+        chunk_sweeps<M, UNIFORM>(p, tb, v, d);
+
+        double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TLT;
+        Y[(2 * chunk) * TLT + lane] = d[0];
+        Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+        __syncthreads();
+
+        // chunk boundary values without the rank pins
+        double F, L;
+        chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr, nullptr,
+                          F, L);
+        if (!edge_warp) {
+            if (valid)
+                chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F,
+                                        L, true);
+        } else {
+            // ROUND 2 posts of this item: the rank's d[0] / d[m-1]
+            double gy = 0.0;
+            if (valid && (first_chunk || last_chunk)) {
+                const double* g = p.g + (first_chunk ? 0 : K);
+                for (int q = 0; q < K; ++q) gy = fma(__ldg(g + q), Y[q * TLT + lane], gy);
+                if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
+                if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
+            }
+            if (prev_item >= 0) finish(prev_item);
+            __syncwarp();
+            stash[0] = F;
+#pragma unroll
+            for (int i = 1; i < M - 1; ++i) stash[i * 32] = d[i];
+            stash[(M - 1) * 32] = L;
+            stash[M * 32] = gy;
+            __syncwarp();
+        }
+        prev_item = item;
+    }
+    if (edge_warp && prev_item >= 0) finish(prev_item);
+}
+
 namespace {
 
 size_t dd_smem(const FastArgs& a, TileCfg c) {
@@ -324,11 +540,56 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     return cuda_check(cudaGetLastError(), "k_dd launch");
 }
 
+size_t dd2_smem(const FastArgs& a, TileCfg c, int M) {
+    return tma_smem(a, c) + (size_t)c.tpc * 2 * (M + 1) * 32 * 8;
+}
+
+template <int M, bool UNI, int TLT>
+int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
+    DDArgs A = A0;
+    FastArgs& a = A.t.f;
+    // keep >= 2 CTAs per SM: fewer tiles per CTA if the stash does not fit
+    while (cfg.tpc > 1 && dd2_smem(a, cfg, M) > 110 * 1024) cfg.tpc /= 2;
+    a.tiles_per_cta = cfg.tpc;
+    const long long tiles = (a.lines + TLT - 1) / TLT;
+    a.items = (tiles + cfg.tpc - 1) / cfg.tpc;
+    if (a.items <= 0) return TDS_OK;
+    int rc = encode_field_map(a, M, TLT, &A.t.map, &A.t.boxr);
+    if (rc) return rc;
+    const int threads = cfg.tpc * a.chunks * TLT;
+    const size_t smem = dd2_smem(a, cfg, M);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        rc = cuda_check(cudaFuncSetAttribute(k_dd2<M, UNI, TLT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem),
+                        "cudaFuncSetAttribute(k_dd2)");
+        if (rc) return rc;
+        smem_set = smem;
+    }
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd2<M, UNI, TLT>, threads, smem);
+    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
+    long long grid = (long long)nb * sms;
+    if (grid > a.items) grid = a.items;
+    k_dd2<M, UNI, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_dd2 launch");
+}
+
+bool defer_policy() {
+    if (const char* e = getenv("TDS_DEFER")) return e[0] != '0';
+    return true;
+}
+
 template <int M, bool UNI>
 int launch_dd_m(const DDArgs& A, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(A.t.f);
-    if (cfg.tl == 8) return launch_dd_t<M, UNI, 8>(A, cfg, s);
-    return launch_dd_t<M, UNI, 16>(A, cfg, s);
+    const bool defer = defer_policy() && (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
+    if (cfg.tl == 8)
+        return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);
+    return defer ? launch_dd2_t<M, UNI, 16>(A, cfg, s) : launch_dd_t<M, UNI, 16>(A, cfg, s);
 }
 
 }  // namespace

@@ -51,6 +51,7 @@ struct FastArgs {
     int tiles_per_cta;
     int edge_mode;
     int has_prev, has_next;
+    int dd_defer16, dd_defer8;   // deferred-edge fused kernel allowed (see plan.cpp)
     double sa_first, sc_last, prev_sc_last, next_sa_first, det_prev, det_next;
     UniformTable ut;
 };
@@ -141,6 +142,7 @@ struct tds_plan {
     double sa_first = 0, sc_last = 0, prev_sc_last = 0, next_sa_first = 0;
     double det_prev = 1, det_next = 1;
     int has_prev = 0, has_next = 0;
+    int dd_defer[2] = {0, 0};             // k_dd2 allowed for 16 / 8 lines per tile
 
     // staged path (device tables indexed by block row)
     double* d_st = nullptr;
