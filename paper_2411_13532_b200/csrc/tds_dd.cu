@@ -586,7 +586,10 @@ bool defer_policy() {
 template <int M, bool UNI>
 int launch_dd_m(const DDArgs& A, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(A.t.f);
-    const bool defer = defer_policy() && (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
+    // deferral pays only if some warps are interior (chunks > 2 warps' worth)
+    const int cw = 32 / (cfg.tl ? cfg.tl : 16);
+    const bool defer = defer_policy() && A.t.f.chunks > 2 * cw &&
+                       (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
     if (cfg.tl == 8)
         return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);
     return defer ? launch_dd2_t<M, UNI, 16>(A, cfg, s) : launch_dd_t<M, UNI, 16>(A, cfg, s);

@@ -298,6 +298,79 @@ def _audit_counts(part, periodic, groups, sz):
     return msgs, nbytes
 
 
+class _HostPipe:
+    """Per-device staging for host-resident solves: three copy/compute
+    streams and a ring of device buffers (allocated once, reused)."""
+
+    def __init__(self, device):
+        torch = _torch()
+        self.device = device
+        self.h2d = torch.cuda.Stream(device)
+        self.cmp = torch.cuda.Stream(device)
+        self.d2h = torch.cuda.Stream(device)
+        self.bufs = []
+
+    def buffers(self, nelem):
+        torch = _torch()
+        if not self.bufs or self.bufs[0][0].numel() < nelem:
+            self.bufs = [(torch.empty(nelem, dtype=torch.float64, device=self.device),
+                          torch.empty(nelem, dtype=torch.float64, device=self.device))
+                         for _ in range(3)]
+        return self.bufs
+
+
+_PIPES = {}
+PIPE_CHUNK_BYTES = 64 << 20
+
+
+def _pipelined_host_solve(plan, u_host, out_host, groups, sz):
+    """Solve a pinned host field chunk by chunk (lines are independent):
+    H2D of chunk i+1, the kernel on chunk i and D2H of chunk i-1 overlap, so
+    PCIe runs full duplex. Blocks until the result is in out_host."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    pipe = _PIPES.get(dev)
+    if pipe is None:
+        pipe = _PIPES[dev] = _HostPipe(dev)
+    per_group = u_host[0].numel()
+    gchunk = max(1, min(groups, PIPE_CHUNK_BYTES // (8 * per_group)))
+    bufs = pipe.buffers(gchunk * per_group)
+    uf = u_host.view(groups, per_group)
+    of = out_host.view(groups, per_group)
+    cur = torch.cuda.current_stream()
+    for s in (pipe.h2d, pipe.cmp, pipe.d2h):
+        s.wait_stream(cur)
+    free_in = [None] * 3
+    free_out = [None] * 3
+    lib = N.lib()
+    for i, g0 in enumerate(range(0, groups, gchunk)):
+        g1 = min(groups, g0 + gchunk)
+        k = i % 3
+        din, dout = bufs[k][0][:(g1 - g0) * per_group], bufs[k][1][:(g1 - g0) * per_group]
+        if free_in[k] is not None:
+            pipe.h2d.wait_event(free_in[k])
+        with torch.cuda.stream(pipe.h2d):
+            din.copy_(uf[g0:g1].reshape(-1), non_blocking=True)
+        loaded = torch.cuda.Event()
+        loaded.record(pipe.h2d)
+        pipe.cmp.wait_event(loaded)
+        if free_out[k] is not None:
+            pipe.cmp.wait_event(free_out[k])
+        N.check(lib.tds_solve(plan.handle, ctypes.c_void_p(din.data_ptr()),
+                              ctypes.c_void_p(dout.data_ptr()), g1 - g0, sz,
+                              ctypes.c_void_p(pipe.cmp.cuda_stream)), plan.rank_count)
+        solved = torch.cuda.Event()
+        solved.record(pipe.cmp)
+        free_in[k] = solved
+        pipe.d2h.wait_event(solved)
+        with torch.cuda.stream(pipe.d2h):
+            of[g0:g1].reshape(-1).copy_(dout, non_blocking=True)
+        drained = torch.cuda.Event()
+        drained.record(pipe.d2h)
+        free_out[k] = drained
+    pipe.d2h.synchronize()
+
+
 def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
                warn_not_dominant=True, audit=None, *, arithmetic="fast", stream=None,
                out=None):
@@ -327,6 +400,18 @@ def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
                 warnings.warn("local block is not strictly diagonally dominant",
                               NotDominantWarning, stacklevel=2)
     plan = get_plan(sys, stencil, part, -1, arithmetic)
+    torch = _torch()
+    if (isinstance(field_values, torch.Tensor) and not field_values.is_cuda
+            and field_values.is_pinned() and field_values.dtype == torch.float64
+            and field_values.is_contiguous() and groups >= 2):
+        res = out if out is not None else torch.empty(shape, dtype=torch.float64,
+                                                      pin_memory=True)
+        _pipelined_host_solve(plan, field_values, res, groups, sz)
+        if audit is not None and part.rank_count > 1:
+            msgs, nbytes = _audit_counts(part, sys.periodic, groups, sz)
+            audit.update(rounds_per_rank=[2] * part.rank_count, messages_sent=msgs,
+                         bytes_sent=nbytes, max_dropped=float(plan.info.max_dropped))
+        return res
     fld = _Field(field_values)
     if groups * sz == 0:
         return fld.give(fld.empty_like(), out)

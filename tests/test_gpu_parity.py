@@ -270,3 +270,25 @@ def test_operator_accuracy_and_order():
     res2 = T.order_of_accuracy(T.second_derivative_scheme(1.0), T.operator_applier(1),
                                (32, 64, 128, 256))
     assert res2.slope >= 4.0
+
+
+def test_pinned_host_pipeline_matches_oracle(golden):
+    """Pinned CPU tensors take the chunked H2D / kernel / D2H pipeline."""
+    from paper_2411_13532_b200 import distributed as D
+    c = golden_run(golden, "d1p512_P8")
+    s = _sys(c)
+    old = D.PIPE_CHUNK_BYTES
+    D.PIPE_CHUNK_BYTES = 512 * 32 * 8          # one group per chunk: many chunks
+    try:
+        rng = np.random.default_rng(8)
+        f = rng.standard_normal((9, 512, 32))
+        host = torch.from_numpy(f).pin_memory()
+        out = torch.empty_like(host).pin_memory()
+        for sizes in (c["sizes"], (512,)):
+            got = T.run_distd2(s, host, part=T.SubdomainPartition(sizes), stencil=_st(c), out=out)
+            assert got.data_ptr() == out.data_ptr()
+            want = O.run_distd2(c["lower"], c["diag"], c["upper"], c["periodic"], f,
+                                c["stencil"], sizes)
+            assert O.rel_linf(got.numpy(), want) <= TOL
+    finally:
+        D.PIPE_CHUNK_BYTES = old
