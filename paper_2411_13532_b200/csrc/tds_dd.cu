@@ -309,6 +309,10 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     const int wc0 = chunk - (wl / TLT);                // first chunk of my warp
     const bool has_first = wc0 == 0, has_last = wc0 + CW - 1 >= C - 1;
     const bool edge_warp = has_first || has_last;
+    // helper roles of two interior warps (k_dd2 runs only with >= 4 warps per
+    // tile): warp 1 forms and posts g0.Y / g1.Y, warp 2 posts the halo rows
+    const int wt = (t >> 5) % (C * TLT / 32);
+    const int role = wl / TLT;
     const long long sz = p.sz;
     const int r0 = chunk * M;
     const Mail mb{p.lines};
@@ -319,7 +323,8 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     double* sY = tiles + (size_t)tpc * tile_elems;
     const size_t ybuf = (size_t)tpc * K * TLT;
     double* sS = sY + 2 * ybuf;                        // stash: [tpc][2][M+1][32]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sS + (size_t)tpc * 2 * (M + 1) * 32);
+    double* sGY = sS + (size_t)tpc * 2 * (M + 1) * 32; // rank d[0], d[m-1]: [2][tpc][2][TLT]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sGY + (size_t)2 * tpc * 2 * TLT);
     double* stash = sS + ((size_t)(2 * tl + (has_first ? 0 : 1)) * (M + 1)) * 32 + wl;
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
     const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
@@ -339,16 +344,17 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         }
     };
     auto publish_halo = [&](long long item) {
+        if (wt != 2 || role > 1) return;
         const long long ln = (item * tpc + tl) * TLT + lane;
         if (ln >= p.lines) return;
         const double* ub = p.u + line_base(ln, rows, p.sz);
         const long long hb = halo_base(ln, p.sz);
-        if (first_chunk && A.mail_prev) {
+        if (role == 0 && A.mail_prev) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
             post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
         }
-        if (last_chunk && A.mail_next) {
+        if (role == 1 && A.mail_next) {
             const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
             const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
             post(A.mail_next + par + mb.h_lo() + hb, a0);
@@ -356,19 +362,20 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         }
     };
     // finish the stashed item `fi` (edge warps only; warp-synchronous)
-    auto finish = [&](long long fi) {
+    auto finish = [&](long long fi, int fslot) {
+        const double* GY = sGY + ((size_t)fslot * tpc + tl) * 2 * TLT;
         const long long fl = (fi * tpc + tl) * TLT + lane;
         const bool fv = fl < p.lines;
         double us = 0.0, ue = 0.0;
         if (first_chunk) {
-            us = stash[M * 32];
+            us = GY[lane];
             if (fv && p.has_prev) {
                 const double prev_last = take(A.mail + par + mb.d_from_prev() + fl, A, err);
                 us = (us - p.sa_first * prev_last) / p.det_prev;
             }
         }
         if (last_chunk) {
-            ue = stash[M * 32];
+            ue = GY[TLT + lane];
             if (fv && p.has_next) {
                 const double next_first = take(A.mail + par + mb.d_from_next() + fl, A, err);
                 ue = (ue - p.sc_last * next_first) / p.det_next;
@@ -413,7 +420,8 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     uint32_t phase = 0;
     long long prev_item = -1;
 
-    for (int it = 0; item < p.items; item += gridDim.x, ++it) {
+    int it = 0;
+    for (; item < p.items; item += gridDim.x, ++it) {
         const long long line = (item * tpc + tl) * TLT + lane;
         const bool valid = line < p.lines;
         const long long nxt = item + gridDim.x;
@@ -473,30 +481,39 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr, nullptr,
                           F, L);
         if (!edge_warp) {
+            // ROUND 2 posts of this item (helper warp): the rank's d[0] / d[m-1]
+            if (wt == 1 && role < 2 && valid) {
+                const double* g = p.g + role * K;
+                double gy0 = 0.0, gy1 = 0.0;
+                int q = 0;
+                for (; q + 1 < K; q += 2) {
+                    gy0 = fma(__ldg(g + q), Y[q * TLT + lane], gy0);
+                    gy1 = fma(__ldg(g + q + 1), Y[(q + 1) * TLT + lane], gy1);
+                }
+                if (q < K) gy0 = fma(__ldg(g + q), Y[q * TLT + lane], gy0);
+                const double gy = gy0 + gy1;
+                if (role == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
+                if (role == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
+                sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
+            }
             if (valid)
                 chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F,
                                         L, true);
         } else {
-            // ROUND 2 posts of this item: the rank's d[0] / d[m-1]
-            double gy = 0.0;
-            if (valid && (first_chunk || last_chunk)) {
-                const double* g = p.g + (first_chunk ? 0 : K);
-                for (int q = 0; q < K; ++q) gy = fma(__ldg(g + q), Y[q * TLT + lane], gy);
-                if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
-                if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
-            }
-            if (prev_item >= 0) finish(prev_item);
+            if (prev_item >= 0) finish(prev_item, (it & 1) ^ 1);
             __syncwarp();
             stash[0] = F;
 #pragma unroll
             for (int i = 1; i < M - 1; ++i) stash[i * 32] = d[i];
             stash[(M - 1) * 32] = L;
-            stash[M * 32] = gy;
             __syncwarp();
         }
         prev_item = item;
     }
-    if (edge_warp && prev_item >= 0) finish(prev_item);
+    if (prev_item >= 0) {
+        __syncthreads();   // the helper warp's g.Y of the last item
+        if (edge_warp) finish(prev_item, (it - 1) & 1);
+    }
 }
 
 namespace {
@@ -541,7 +558,7 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
 }
 
 size_t dd2_smem(const FastArgs& a, TileCfg c, int M) {
-    return tma_smem(a, c) + (size_t)c.tpc * 2 * (M + 1) * 32 * 8;
+    return tma_smem(a, c) + (size_t)c.tpc * 2 * (M + 1) * 32 * 8 + (size_t)4 * c.tpc * c.tl * 8;
 }
 
 template <int M, bool UNI, int TLT>
