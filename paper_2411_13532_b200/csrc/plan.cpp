@@ -13,6 +13,7 @@
 //   thomas / periodic thomas ... serial.py:26-90
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -230,9 +231,13 @@ vector<double> reduced(const ChunkSet& cs, int k0, int k1, bool wrap) {
     return R;
 }
 
-int pick_chunk(const vector<int>& blocks, int flags) {
+int pick_chunk(const vector<int>& blocks, int flags, bool rank_block = false) {
     if (flags & (TDS_FLAG_STRICT | TDS_FLAG_STAGED)) return 0;
-    for (int M : {32, 16}) {
+    // A/B knob for per-rank blocks (fused kernel): TDS_RANK_CHUNK=32|16.
+    int first = 32;
+    if (const char* e = getenv("TDS_RANK_CHUNK"))
+        if (rank_block) first = atoi(e) == 16 ? 16 : 32;
+    for (int M : {first, 48 - first}) {
         bool ok = true;
         for (int m : blocks)
             if (m % M != 0 || m / M > tds::MAX_CHUNKS) ok = false;
@@ -429,7 +434,7 @@ int build_local(tds_plan* p, const Global& loc, int has_prev, int has_next, doub
         if (std::fabs(det) < tds::PAIR_DET_FLOOR)
             return set_err(TDS_ERR_SINGULAR_PAIR, fmt("boundary determinant %.3e", det),
                            rank_for_errors);
-    int M = pick_chunk({m}, p->flags);
+    int M = pick_chunk({m}, p->flags, true);
     if (M > 0) {
         ChunkSet cs;
         if ((rc = fast_tables(p, loc, M, cs))) return rc;
