@@ -265,15 +265,22 @@ def run_multi(args, torch):
               for d in "xyz"}
     outs = {d: torch.empty_like(fields[d]) for d in "xyz"}
     stream = torch.cuda.current_stream()
+    fused = solver.fused and T._native.lib().tds_fused_eligible(solver.plan.handle, groups, SZ)
 
-    def step():
+    def step(ev=None):
         for d in "xyz":
+            if ev is not None:
+                ev[d][0].record(stream)
             solver.solve(fields[d], outs[d])
+            if ev is not None:
+                ev[d][1].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    evs = [{d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for d in "xyz"} for _ in range(args.steps)]
     clk = Clocks(local)
     clk.start()
     time.sleep(0.3)
@@ -281,18 +288,23 @@ def run_multi(args, torch):
     torch.cuda.synchronize()
     dist.barrier()
     t0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for k in range(args.steps):
+        step(evs[k])
     t1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     clocks = clk.stop()
-    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], device=dev)
+    solver.check()
+    solve_ms = statistics.mean(e[d][0].elapsed_time(e[d][1]) for e in evs for d in "xyz")
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps, solve_ms], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_step = float(ms.item())
+    ms_step, solve_ms = float(ms[0].item()), float(ms[1].item())
     points = n ** 3
     value = 3 * BYTES_PER_POINT * points / (ms_step * 1e-3) / 1e9
     peak, peak_kind = peaks()
+    local_points = groups * m * SZ
+    achieved = BYTES_PER_POINT * local_points / (solve_ms * 1e-3) / 1e9
+    e2e = run_multi_e2e(args, torch, dist, solver, fields, n, world, dev)
     res = None
     if rank == 0:
         res = {
@@ -304,91 +316,164 @@ def run_multi(args, torch):
                                    f"direction over {world} GPUs (BASELINE configs[2])",
                        "n": n, "directions": "x,y,z", "sz": SZ,
                        "partition": list(part.local_sizes), "path": solver.path,
-                       "exchange": "NCCL P2P, 2 neighbour rounds per solve",
+                       "exchange": ("in-kernel NVLink peer stores (k_dd/k_dd2 mailboxes), "
+                                    "2 neighbour rounds per solve" if fused else
+                                    "NCCL P2P, 2 neighbour rounds per solve"),
                        "l2": "inputs > 126 MB L2; no flush", "parallelism": f"dd{world}"},
             "pct_peak": round(100 * value / (world * peak), 2),
             "gdof_per_s": round(3 * points / (ms_step * 1e-3) / 1e9, 2),
-            "roofline": {"bound": "hbm", "kernel": "whole step per GPU",
-                         "achieved": round(value / world, 2), "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(value / world / peak, 4), "traffic": None},
-            "e2e": None, "gpu_launches": 3 * 3 * args.steps, "clocks": clocks,
-            "cpu_baseline": None,
+            "ms_per_solve": round(solve_ms, 5),
+            "roofline": {"bound": "hbm",
+                         "kernel": "k_dd2/k_dd fused per-rank solve" if fused
+                         else "per-rank solve (halo + pass A + pass B)",
+                         "achieved": round(achieved, 2), "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "algorithmic_bytes_per_launch": BYTES_PER_POINT * local_points},
+            "e2e": e2e, "gpu_launches": (1 if fused else 3) * 3 * args.steps,
+            "clocks": clocks, "cpu_baseline": None,
         }
     dist.barrier()
+    solver.close()
     dist.destroy_process_group()
     return res
 
 
+def run_multi_e2e(args, torch, dist, solver, fields, n, world, dev):
+    """Same metric through the per-rank public API with HOST buffers: each
+    rank copies its pinned host slab in, solves, copies the result out."""
+    try:
+        host_in = {d: fields[d].cpu().pin_memory() for d in "xyz"}
+        host_out = {d: torch.empty_like(host_in[d]).pin_memory() for d in "xyz"}
+    except RuntimeError as exc:                         # host memory exhausted
+        return {"value": None, "unavailable": str(exc)[:120]}
+    dev_in = {d: torch.empty_like(fields[d]) for d in "xyz"}
+    dev_out = {d: torch.empty_like(fields[d]) for d in "xyz"}
+    steps = max(2, min(args.steps, args.e2e_steps))
+
+    def step():
+        for d in "xyz":
+            dev_in[d].copy_(host_in[d], non_blocking=True)
+            solver.solve(dev_in[d], dev_out[d])
+            host_out[d].copy_(dev_out[d], non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dist.barrier()
+    dt = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    dt = float(dt.item())
+    nbytes = sum(h.numel() * 8 for h in host_in.values())
+    return {"value": round(3 * BYTES_PER_POINT * n ** 3 / dt / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
+            "ms_per_step": round(dt * 1e3, 3), "steps": steps,
+            "api": "per rank: pinned host slab -> DistD2Rank.solve -> pinned host slab, x3"}
+
+
 # ------------------------------------------------------------ CPU legs
 
-def sample_fields(n, groups, seed):
-    """First `groups` SZ-groups of the x/y/z packings of the same random
-    n^3 field the reference bench would build (layout.py:105-134)."""
-    from oracle import tds_oracle as O
-    u = np.random.default_rng(seed).standard_normal((n, n, n))
-    out = {}
-    for d in "xyz":
-        axes = O._transverse_axes(d)
-        lines = u.transpose(axes).reshape(-1, n)[:groups * SZ]
-        out[d] = np.ascontiguousarray(lines.reshape(groups, SZ, n).transpose(0, 2, 1))
-    return out
+# CPU legs: the reference algorithm (the pinned NumPy port, oracle/) on every
+# host core. The reference's per-position loop holds the GIL, so parallelism
+# is one process per core (fork), each owning a wide batch of lines.
+_W = {}
 
 
-def cpu_time_sample(n, groups, threads, directions="xyz"):
+def _worker_init(n, groups, seed):
     from oracle import tds_oracle as O
-    lo, di, up, st = O.assemble("d1", n, 2 * np.pi / n, True)
-    flds = sample_fields(n, groups, 1234 + 1)
+    rng = np.random.default_rng(seed)
+    _W["op"] = O.assemble("d1", n, 2 * np.pi / n, True)
+    _W["fields"] = {d: rng.standard_normal((groups, n, SZ)) for d in "xyz"}
+
+
+def _worker_step(directions):
+    from oracle import tds_oracle as O
+    lo, di, up, st = _W["op"]
     t0 = time.perf_counter()
     for d in directions:
-        O.run_distd2_threaded(lo, di, up, True, flds[d], st, threads=threads,
-                              groups_per_task=max(1, groups // (4 * threads)))
-    dt = time.perf_counter() - t0
-    pts = len(directions) * groups * n * SZ
-    return BYTES_PER_POINT * pts / dt / 1e9, dt, pts
+        _W["out"] = O.run_distd2(lo, di, up, True, _W["fields"][d], st)
+    return time.perf_counter() - t0
+
+
+class CpuPool:
+    """`procs` forked workers, each with `groups` SZ-groups per direction."""
+
+    def __init__(self, n, groups, procs, seed=1235):
+        import multiprocessing as mp
+        self.n, self.groups, self.procs = n, groups, procs
+        self.pool = mp.get_context("fork").Pool(procs, _worker_init, (n, groups, seed))
+
+    def step(self, directions="xyz"):
+        t0 = time.perf_counter()
+        self.pool.map(_worker_step, [directions] * self.procs)
+        dt = time.perf_counter() - t0
+        pts = len(directions) * self.procs * self.groups * self.n * SZ
+        return BYTES_PER_POINT * pts / dt / 1e9, dt, pts
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def calibrated_pool(n, cores, budget_s, max_groups):
+    """Pick SZ-groups per worker so one x/y/z step takes about budget_s."""
+    pool = CpuPool(n, 8, cores)
+    pool.step()
+    _, dt, _ = pool.step()
+    pool.close()
+    groups = int(max(8, min(max_groups, 8 * budget_s / max(dt, 1e-6))))
+    return CpuPool(n, groups, cores)
 
 
 def cpu_baseline(args, n):
-    threads = len(os.sched_getaffinity(0))
-    groups = args.cpu_groups
-    gbs, dt, pts = cpu_time_sample(n, groups, threads, "x")
-    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"x-direction solve of {groups} of {n * n // SZ} SZ-groups "
-                      f"({pts} points) of the {n}^3 field, oracle/tds_oracle.run_distd2 "
-                      f"(NumPy restatement of reference run_distd2, P=1), {dt:.2f} s"}
+    cores = len(os.sched_getaffinity(0))
+    pool = calibrated_pool(n, cores, 3.0, args.cpu_groups)
+    pool.step("x")
+    gbs, dt, pts = pool.step("x")
+    pool.close()
+    return {"value": round(gbs, 5), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"x-direction solve of {pool.procs}x{pool.groups} SZ-groups ({pts} points) "
+                      f"of the {n}^3 workload, oracle/tds_oracle.run_distd2 (NumPy "
+                      f"restatement of reference run_distd2, P=1), one process per core, "
+                      f"{dt:.2f} s"}
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (pinned NumPy port) on
+    all host cores; each step solves x, y and z on a bounded sample of the
+    workload's lines, sized so the whole run takes about a minute or two."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    n = 512 if args.gpus == 1 else (args.size or 1024)
-    n = args.size or n
-    threads = len(os.sched_getaffinity(0))
-    groups = args.cpu_groups
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_time_sample(n, max(1, groups // 8), threads)
-    times, last = [], None
+    n = args.size or (512 if args.gpus == 1 else 1024)
+    cores = len(os.sched_getaffinity(0))
+    budget = max(0.05, 150.0 / max(1, args.steps + args.warmup))
+    pool = calibrated_pool(n, cores, budget, args.cpu_groups)
+    for _ in range(args.warmup):
+        pool.step()
+    times, pts = [], 0
     for _ in range(args.steps):
-        gbs, dt, pts = cpu_time_sample(n, groups, threads)
+        _, dt, pts = pool.step()
         times.append(dt)
-        last = (gbs, pts)
+    pool.close()
     dt = statistics.mean(times)
-    gbs = BYTES_PER_POINT * last[1] / dt / 1e9
-    sample = (f"x,y,z solves of {groups} of {n * n // SZ} SZ-groups ({last[1]} points) of the "
-              f"{n}^3 field per step, oracle/tds_oracle.run_distd2 (NumPy restatement of "
-              f"reference run_distd2 P=1) on {threads} host threads")
+    gbs = BYTES_PER_POINT * pts / dt / 1e9
+    sample = (f"x,y,z solves of {pool.procs}x{pool.groups} of the {n * n // SZ} SZ-groups "
+              f"({pts} points) of the {n}^3 workload per step, oracle/tds_oracle.run_distd2 "
+              f"(NumPy restatement of reference run_distd2 P=1), one process per core")
     peak, _ = peaks()
-    return {"metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "impl": "reference",
+    return {"metric": METRIC, "value": round(gbs, 5), "unit": "GB/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{n}^3 x/y/z DistD2 solve (sampled lines)", "n": n,
                        "directions": "x,y,z", "sz": SZ},
             "pct_peak": round(100 * gbs / peak, 5),
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads,
+            "cpu_baseline": {"value": round(gbs, 5), "unit": "GB/s", "cores": cores,
                              "kind": "port", "sample": sample},
-            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": round(gbs, 5), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
 
@@ -401,7 +486,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=0, help="grid extent (default 512 / 1024)")
     ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--cpu-groups", type=int, default=512)
+    ap.add_argument("--cpu-groups", type=int, default=256, help="max SZ-groups per CPU worker")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
