@@ -487,11 +487,105 @@ __global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst,
     else dst[c] = src[idx];
 }
 
+// Tiled variant: every direction's permutation is a 2-D transpose between the
+// Cartesian fastest axis k and the field's fastest axis, the LANE axis (j for
+// x lines, i for y and z lines), at fixed third index o (i for x, j for y and
+// z). A 32 x 32 shared-memory tile makes both the Cartesian reads (runs of k)
+// and the field writes (runs of lanes) coalesced. blockIdx = (k tile, lane
+// tile, o); block = 32 x 8 threads.
+__device__ __forceinline__ long long field_index(int i, int j, int k, int nx, int ny, int nz,
+                                                 int sz, int lsz, int dir) {
+    // transverse index < 2^31 for every supported field (lines x sz fits int)
+    unsigned t, pos, n;
+    if (dir == 0) { t = (unsigned)j + (unsigned)ny * (unsigned)k; pos = i; n = nx; }
+    else if (dir == 1) { t = (unsigned)i + (unsigned)nx * (unsigned)k; pos = j; n = ny; }
+    else { t = (unsigned)i + (unsigned)nx * (unsigned)j; pos = k; n = nz; }
+    unsigned g, l;
+    if (lsz >= 0) { g = t >> lsz; l = t & ((1u << lsz) - 1u); }
+    else { g = t / (unsigned)sz; l = t - g * (unsigned)sz; }
+    return ((long long)g * n + pos) * sz + l;
+}
+
+__global__ void k_pack_tiled(const double* __restrict__ src, double* __restrict__ dst, int nx,
+                             int ny, int nz, int sz, int lsz, int dir, bool to_field) {
+    __shared__ double tile[32][33];
+    const int k0 = blockIdx.x * 32;
+    const int a0 = blockIdx.y * 32;
+    const int o = blockIdx.z;
+    const int na = dir == 0 ? ny : nx;     // extent of the lane axis
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    auto ijk = [&](int a, int k, int& i, int& j) {
+        if (dir == 0) { i = o; j = a; }
+        else { i = a; j = o; }
+        (void)k;
+    };
+    if (to_field) {
+#pragma unroll
+        for (int r = ty; r < 32; r += 8) {       // read runs of k: coalesced
+            const int a = a0 + r, k = k0 + tx;
+            if (a < na && k < nz) {
+                int i, j;
+                ijk(a, k, i, j);
+                tile[r][tx] = __ldcs(src + ((long long)i * ny + j) * nz + k);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = ty; r < 32; r += 8) {       // write runs of lanes: coalesced
+            const int a = a0 + tx, k = k0 + r;
+            if (a < na && k < nz) {
+                int i, j;
+                ijk(a, k, i, j);
+                __stcs(dst + field_index(i, j, k, nx, ny, nz, sz, lsz, dir), tile[tx][r]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = ty; r < 32; r += 8) {       // read runs of lanes
+            const int a = a0 + tx, k = k0 + r;
+            if (a < na && k < nz) {
+                int i, j;
+                ijk(a, k, i, j);
+                tile[tx][r] = __ldcs(src + field_index(i, j, k, nx, ny, nz, sz, lsz, dir));
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = ty; r < 32; r += 8) {       // write runs of k
+            const int a = a0 + r, k = k0 + tx;
+            if (a < na && k < nz) {
+                int i, j;
+                ijk(a, k, i, j);
+                __stcs(dst + ((long long)i * ny + j) * nz + k, tile[r][tx]);
+            }
+        }
+    }
+}
+
 int launch_pack(const double* src, double* dst, int nx, int ny, int nz, int sz, int dir,
                 long long groups, bool to_field, cudaStream_t s) {
     const int n = dir == 0 ? nx : (dir == 1 ? ny : nz);
     long long total = groups * sz * n;
     if (total == 0) return TDS_OK;
+    const long long lines = (long long)nx * ny * nz / n;
+    const bool tiled = getenv("TDS_PACK_SIMPLE") == nullptr;
+    if (tiled) {
+        if (to_field && groups * sz > lines) {   // ghost lines are zero
+            int rc = cuda_check(cudaMemsetAsync(dst, 0, (size_t)total * sizeof(double), s),
+                                "cudaMemsetAsync(ghost lines)");
+            if (rc) return rc;
+        }
+        const int na = dir == 0 ? ny : nx;
+        const int no = dir == 0 ? nx : ny;
+        dim3 grid((nz + 31) / 32, (na + 31) / 32, no);
+        int lsz = -1;
+        if ((sz & (sz - 1)) == 0) {
+            lsz = 0;
+            while ((1 << lsz) < sz) ++lsz;
+        }
+        k_pack_tiled<<<grid, dim3(32, 8), 0, s>>>(src, dst, nx, ny, nz, sz, lsz, dir, to_field);
+        return cuda_check(cudaGetLastError(), "k_pack_tiled launch");
+    }
     k_pack<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(src, dst, nx, ny, nz, sz, dir, groups,
                                                           to_field);
     return cuda_check(cudaGetLastError(), "k_pack launch");

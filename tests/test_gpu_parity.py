@@ -292,3 +292,21 @@ def test_pinned_host_pipeline_matches_oracle(golden):
             assert O.rel_linf(got.numpy(), want) <= TOL
     finally:
         D.PIPE_CHUNK_BYTES = old
+
+
+@pytest.mark.parametrize("sz", [8, 16, 32])
+def test_pack_unpack_reorder_ragged_extents(sz):
+    """Tiled reorder kernel on extents that are not multiples of its 32x32
+    tile, all directions, bitwise against the oracle's pack."""
+    cart = np.random.default_rng(sz).standard_normal((48, 40, 72))
+    for d in "xyz":
+        lay = T.LayoutDescriptor(48, 40, 72, sz, d, pad=True)
+        f = T.pack(cart, lay)
+        lines = lay.lines
+        want = O.pack(cart, 1, d).reshape(lines, lay.n)          # (lines, n), sz-free
+        got = f.data.transpose(0, 2, 1).reshape(lay.padded_lines, lay.n)
+        np.testing.assert_array_equal(got[:lines], want)
+        np.testing.assert_array_equal(got[lines:], 0.0)
+        np.testing.assert_array_equal(T.unpack(f), cart)
+        for d2 in "xyz":
+            np.testing.assert_array_equal(T.unpack(T.reorder(f, d2)), cart)
