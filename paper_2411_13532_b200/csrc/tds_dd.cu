@@ -307,12 +307,18 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     const int chunk = (t / TLT) % C;
     const int tl = t / (TLT * C);
     const int wc0 = chunk - (wl / TLT);                // first chunk of my warp
+    const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
     const bool has_first = wc0 == 0, has_last = wc0 + CW - 1 >= C - 1;
     const bool edge_warp = has_first || has_last;
     // helper roles of two interior warps (k_dd2 runs only with >= 4 warps per
     // tile): warp 1 forms and posts g0.Y / g1.Y, warp 2 posts the halo rows
     const int wt = (t >> 5) % (C * TLT / 32);
     const int role = wl / TLT;
+    // with fewer than 4 warps per tile there are no helpers: the first / last
+    // chunk threads post their own halos and ROUND 2
+    const bool helpers = C * TLT / 32 >= 4;
+    const bool halo_lo_poster = helpers ? (wt == 2 && role == 0) : first_chunk;
+    const bool halo_hi_poster = helpers ? (wt == 2 && role == 1) : last_chunk;
     const long long sz = p.sz;
     const int r0 = chunk * M;
     const Mail mb{p.lines};
@@ -327,7 +333,6 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(sGY + (size_t)2 * tpc * 2 * TLT);
     double* stash = sS + ((size_t)(2 * tl + (has_first ? 0 : 1)) * (M + 1)) * 32 + wl;
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
-    const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
 
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
@@ -344,17 +349,17 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         }
     };
     auto publish_halo = [&](long long item) {
-        if (wt != 2 || role > 1) return;
+        if (!halo_lo_poster && !halo_hi_poster) return;
         const long long ln = (item * tpc + tl) * TLT + lane;
         if (ln >= p.lines) return;
         const double* ub = p.u + line_base(ln, rows, p.sz);
         const long long hb = halo_base(ln, p.sz);
-        if (role == 0 && A.mail_prev) {
+        if (halo_lo_poster && A.mail_prev) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
             post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
         }
-        if (role == 1 && A.mail_next) {
+        if (halo_hi_poster && A.mail_next) {
             const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
             const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
             post(A.mail_next + par + mb.h_lo() + hb, a0);
@@ -500,6 +505,17 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                 chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F,
                                         L, true);
         } else {
+            if (!helpers && valid && (first_chunk || last_chunk)) {
+                for (int r = 0; r < 2; ++r) {
+                    if ((r == 0 && !first_chunk) || (r == 1 && !last_chunk)) continue;
+                    const double* g = p.g + r * K;
+                    double gy = 0.0;
+                    for (int q = 0; q < K; ++q) gy = fma(__ldg(g + q), Y[q * TLT + lane], gy);
+                    if (r == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
+                    if (r == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
+                    sGY[(((size_t)(it & 1) * tpc + tl) * 2 + r) * TLT + lane] = gy;
+                }
+            }
             if (prev_item >= 0) finish(prev_item, (it & 1) ^ 1);
             __syncwarp();
             stash[0] = F;
@@ -605,7 +621,9 @@ int launch_dd_m(const DDArgs& A, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(A.t.f);
     // deferral pays only if some warps are interior (chunks > 2 warps' worth)
     const int cw = 32 / (cfg.tl ? cfg.tl : 16);
-    const bool defer = defer_policy() && A.t.f.chunks > 2 * cw &&
+    const char* ev = getenv("TDS_DEFER");
+    const bool force = ev && ev[0] == '2';
+    const bool defer = defer_policy() && (force || A.t.f.chunks > 2 * cw) &&
                        (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
     if (cfg.tl == 8)
         return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);

@@ -60,7 +60,7 @@ def _loopback(n, groups, sz, env, seed=0, epochs=3):
     return O.rel_linf(out.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("env", [{"TDS_DEFER": "0"}, {"TDS_DEFER": "1"},
+@pytest.mark.parametrize("env", [{"TDS_DEFER": "0"}, {"TDS_DEFER": "1"}, {"TDS_DEFER": "2"},
                                  {"TDS_DEFER": "1", "TDS_TL": "8"}])
 @pytest.mark.parametrize("n", [512, 256, 128])
 def test_fused_loopback_matches_periodic_solve(n, env):
