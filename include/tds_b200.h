@@ -184,6 +184,25 @@ int tds_thomas(const double* lower, const double* diag, const double* upper,
                int periodic, const double* rhs, double* out, int n,
                long long groups, int sz, void* stream);
 
+/* ---- momentum-transport RHS (momentum.py:102-169) ------------------------
+ * One (component i, direction j) contribution of the skew-symmetric
+ * transport RHS, -1/2 (u_j du_i/dx_j + d(u_j u_i)/dx_j) + nu d2u_i/dx_j2, in
+ * ONE fused pass over u_i and u_j (both in the j layout): d1 / d2 are P=1
+ * plans of the periodic d/dx and d2/dx2 operators (d2 may be NULL when
+ * nu == 0). accumulate = 1 adds into out. */
+int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2,
+                               const double* u_i, const double* u_j, double* out,
+                               double nu, int accumulate, long long groups, int sz,
+                               void* stream);
+/* elementwise combine of precomputed derivatives (rank-emulated path) */
+int tds_transport_combine(const double* u_j, const double* du, const double* dp,
+                          const double* d2u, double nu, double* out, long long count,
+                          int accumulate, void* stream);
+/* cubic n^3 field: SZ-blocked layout of src_dir -> dst_dir in one pass
+ * (reorder, layout.py:144-152); accumulate = 1 adds into dst */
+int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,
+                int dst_dir, int accumulate, void* stream);
+
 /* ---- layout (layout.py:82-152) -------------------------------------------
  * Cartesian (nx, ny, nz) C-order <-> SZ-blocked (groups, n, sz) field for
  * `direction` ('x'=0,'y'=1,'z'=2). groups*sz may exceed the line count:

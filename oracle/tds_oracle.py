@@ -424,3 +424,40 @@ def rel_linf(got, want):
     got = np.asarray(got)
     want = np.asarray(want)
     return float(np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-300))
+
+
+# --------------------------------------------------------------- momentum.py
+
+def transport_rhs(u3, v3, w3, nu, h, sz):
+    """momentum.py:102-169 (evaluate_transport_rhs with directional_contribution),
+    same operation order: per direction j, per component i,
+    -0.5 * (u_j * d(u_i) + d(u_j * u_i)) [+ nu * d2(u_i)], folded into x-layout
+    accumulators. Inputs / outputs are Cartesian (n, n, n)."""
+    n = u3.shape[0]
+    ops = {k: assemble(k, n, h, True) for k in ("d1", "d2")}
+
+    def diff(vals, kind):
+        lo, di, up, st = ops[kind]
+        return run_distd2(lo, di, up, True, vals, st)
+
+    def contrib(comp, advect):
+        d_comp = diff(comp, "d1")
+        d_prod = diff(advect * comp, "d1")
+        out = -0.5 * (advect * d_comp + d_prod)
+        if nu != 0.0:
+            out = out + nu * diff(comp, "d2")
+        return out
+
+    vel3 = (u3, v3, w3)
+    acc = None
+    for j, dj in enumerate("xyz"):
+        comps = [pack(c, sz, dj) for c in vel3]
+        for i in range(3):
+            c = contrib(comps[i], comps[j])
+            if dj == "x":
+                if acc is None:
+                    acc = [None, None, None]
+                acc[i] = c
+            else:
+                acc[i] = acc[i] + pack(unpack(c, u3.shape, dj), sz, "x")
+    return tuple(unpack(a, u3.shape, "x") for a in acc)

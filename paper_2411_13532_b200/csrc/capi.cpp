@@ -352,3 +352,48 @@ extern "C" int tds_ipc_close(void* ptr) {
 }
 
 extern "C" int tds_ipc_free(void* ptr) { return tds::cuda_check(cudaFree(ptr), "cudaFree"); }
+
+// ------------------------------------------------- transport RHS (k_transport)
+
+namespace tds {
+struct TransportArgs;
+int launch_reorder(const double* src, double* dst, int n, int sz, int src_dir, int dst_dir,
+                   int accumulate, cudaStream_t s);
+int launch_transport_combine(const double* uj, const double* du, const double* dp,
+                             const double* d2u, double nu, double* out, long long count,
+                             int accumulate, cudaStream_t s);
+int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const double* ui,
+                                const double* uj, double* out, double nu, int accumulate,
+                                long long lines, int sz, cudaStream_t s);
+}  // namespace tds
+
+extern "C" int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2,
+                                          const double* u_i, const double* u_j, double* out,
+                                          double nu, int accumulate, long long groups, int sz,
+                                          void* stream) {
+    if (!d1 || !u_i || !u_j || !out) return set_err(TDS_ERR_INVALID, "null argument");
+    const bool ok1 = d1->path == TDS_PATH_FAST && d1->uniform && d1->M == 32 && d1->P == 1 &&
+                     d1->rank < 0;
+    const bool ok2 = !d2 || (d2->path == TDS_PATH_FAST && d2->uniform && d2->M == 32 &&
+                             d2->P == 1 && d2->rank < 0 && d2->C == d1->C);
+    if (!ok1 || !ok2 || (nu != 0.0 && !d2))
+        return set_err(TDS_ERR_UNSUPPORTED,
+                       "fused transport needs uniform P=1 plans with 32-row chunks");
+    return tds::transport_launch_from_plans(d1, nu != 0.0 ? d2 : nullptr, u_i, u_j, out, nu,
+                                            accumulate, groups * sz, sz, S(stream));
+}
+
+extern "C" int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,
+                           int dst_dir, int accumulate, void* stream) {
+    if (!src || !dst || n < 1 || sz < 1 || src_dir < 0 || src_dir > 2 || dst_dir < 0 ||
+        dst_dir > 2)
+        return set_err(TDS_ERR_INVALID, "bad reorder arguments");
+    if ((long long)n * n % sz) return set_err(TDS_ERR_INVALID, "lines not divisible by sz");
+    return tds::launch_reorder(src, dst, n, sz, src_dir, dst_dir, accumulate, S(stream));
+}
+
+extern "C" int tds_transport_combine(const double* uj, const double* du, const double* dp,
+                                     const double* d2u, double nu, double* out, long long count,
+                                     int accumulate, void* stream) {
+    return tds::launch_transport_combine(uj, du, dp, d2u, nu, out, count, accumulate, S(stream));
+}

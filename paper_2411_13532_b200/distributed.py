@@ -170,6 +170,8 @@ class _Field:
             self.host = True
             self.numpy = True
             arr = np.ascontiguousarray(x, dtype=np.float64)
+            if not arr.flags.writeable:          # torch cannot wrap read-only buffers
+                arr = arr.copy()
             self.t = torch.from_numpy(arr).to("cuda", non_blocking=False)
 
     @property

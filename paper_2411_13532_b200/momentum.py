@@ -1,0 +1,194 @@
+"""Momentum-transport right-hand side on a periodic box, on the GPU: the
+consumer of the DistD2 path in the reference (momentum.py:1-222).
+
+    RHS_j of u_i = -1/2 (u_j d(u_i)/dx_j + d(u_j u_i)/dx_j) + nu d2(u_i)/dx_j2
+
+Work is grouped by direction j exactly like the reference: the components
+are re-laid out for j (one-pass `k_reorder`), the three contributions of
+direction j are computed while the fields sit in the j layout, and they fold
+back into the x-layout accumulators (`k_reorder` with accumulate). Each
+(i, j) contribution is ONE fused kernel (`k_transport`): it reads u_i and u_j
+once and runs the three compact solves of every chunk in registers. Field
+data stays on the device (CUDA tensors) for the whole pipeline.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .compact import assemble, second_derivative_scheme, sixth_order_first_derivative
+from .distributed import _stream_handle, get_plan, run_distd2
+from .layout import GroupedField, LayoutDescriptor, pack
+from .system import SubdomainPartition
+
+_COMPONENTS = ("u", "v", "w")
+_DIRECTIONS = ("x", "y", "z")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass(frozen=True)
+class VelocityField:
+    """Three velocity components in one SZ-blocked layout (momentum.py:32-67)."""
+
+    u: GroupedField
+    v: GroupedField
+    w: GroupedField
+    nu: float
+    h: float
+
+    def __post_init__(self):
+        lay = self.u.layout
+        if self.v.layout != lay or self.w.layout != lay:
+            raise ValueError("velocity components must share one layout")
+        if not (lay.nx == lay.ny == lay.nz):
+            raise ValueError("transport demo expects a cubic grid")
+        torch = _torch()
+        for f in (self.u, self.v, self.w):
+            data = f.data
+            finite = (torch.isfinite(data).all().item() if isinstance(data, torch.Tensor)
+                      else np.all(np.isfinite(data)))
+            if not finite:
+                raise ValueError("velocity values must be finite")
+        if self.h <= 0:
+            raise ValueError("grid spacing must be positive")
+
+    @property
+    def layout(self):
+        return self.u.layout
+
+    @property
+    def n(self):
+        return self.layout.nx
+
+    def component(self, i):
+        return (self.u, self.v, self.w)[i]
+
+    @classmethod
+    def from_arrays(cls, u3, v3, w3, nu, h, sz=8, pad=False):
+        """Pack three Cartesian arrays (NumPy or CUDA tensors) for x; the
+        packed data lives on the GPU."""
+        torch = _torch()
+
+        def dev(a):
+            if isinstance(a, torch.Tensor):
+                return a.to("cuda", torch.float64)
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+        u3, v3, w3 = dev(u3), dev(v3), dev(w3)
+        lay = LayoutDescriptor(*u3.shape, sz=sz, direction="x", pad=pad)
+        return cls(pack(u3, lay), pack(v3, lay), pack(w3, lay), nu, h)
+
+
+_OPERATOR_CACHE = {}
+
+
+def _operator(order, h, n):
+    key = (order, h, n)
+    hit = _OPERATOR_CACHE.get(key)
+    if hit is None:
+        scheme = sixth_order_first_derivative(h) if order == 1 else second_derivative_scheme(h)
+        hit = assemble(scheme, n, periodic=True)
+        _OPERATOR_CACHE[key] = hit
+    return hit
+
+
+def _component_index(i):
+    return _COMPONENTS.index(i) if isinstance(i, str) else int(i)
+
+
+def _direction_name(j):
+    return j if isinstance(j, str) else _DIRECTIONS[int(j)]
+
+
+def _contribution_into(ci, dj, fields, out, accumulate, rank_count):
+    """out (=|+=) the (ci, dj) contribution, all arrays in the dj layout."""
+    n = fields.n
+    comp = fields.component(ci).data
+    advect = fields.component(_DIRECTIONS.index(dj)).data
+    groups, _, sz = comp.shape
+    s1, st1 = _operator(1, fields.h, n)
+    s2, st2 = _operator(2, fields.h, n)
+    if rank_count == 1:
+        part = SubdomainPartition((n,))
+        p1 = get_plan(s1, st1, part)
+        p2 = get_plan(s2, st2, part) if fields.nu != 0.0 else None
+        rc = N.lib().tds_transport_contribution(
+            p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
+            float(fields.nu), int(accumulate), groups, sz, _stream_handle())
+        if rc == N.TDS_OK:
+            return
+        if rc != N.TDS_ERR_UNSUPPORTED:
+            N.check(rc)
+    # general path: three DistD2 solves (any size, emulated ranks) + combine
+    d_comp = run_distd2(s1, comp, stencil=st1, rank_count=rank_count)
+    d_prod = run_distd2(s1, advect * comp, stencil=st1, rank_count=rank_count)
+    d2 = (run_distd2(s2, comp, stencil=st2, rank_count=rank_count)
+          if fields.nu != 0.0 else None)
+    N.check(N.lib().tds_transport_combine(
+        _vp(advect), _vp(d_comp), _vp(d_prod), None if d2 is None else _vp(d2),
+        float(fields.nu), _vp(out), out.numel(), int(accumulate), _stream_handle()))
+
+
+def directional_contribution(i, j, fields, rank_count=1, ledger=None, catalog=None):
+    """Direction-j transport contribution to component i, in j layout
+    (momentum.py:102-126)."""
+    torch = _torch()
+    ci = _component_index(i)
+    dj = _direction_name(j)
+    lay = fields.layout
+    if lay.direction != dj:
+        raise ValueError(f"fields are packed for {lay.direction!r}, kernel needs {dj!r}")
+    out = torch.empty_like(fields.component(ci).data)
+    _contribution_into(ci, dj, fields, out, False, rank_count)
+    return GroupedField(lay, out)
+
+
+def _reorder_tensor(data, n, sz, src, dst, out=None, accumulate=False):
+    torch = _torch()
+    res = torch.empty_like(data) if out is None else out
+    N.check(N.lib().tds_reorder(_vp(data), _vp(res), n, sz, _DIRECTIONS.index(src),
+                                _DIRECTIONS.index(dst), int(accumulate), _stream_handle()))
+    return res
+
+
+def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
+    """Full right-hand side of all three components, x-layout results
+    (momentum.py:142-169)."""
+    torch = _torch()
+    if fields.layout.direction != "x":
+        raise ValueError("inputs must arrive in x layout")
+    lay = fields.layout
+    n, sz = lay.nx, lay.sz
+    if lay.pad:
+        raise NotImplementedError("padded layouts are not supported by the GPU transport demo")
+    acc = [torch.empty_like(fields.component(i).data) for i in range(3)]
+    for i in range(3):
+        _contribution_into(i, "x", fields, acc[i], False, rank_count)
+    scratch = torch.empty_like(acc[0])
+    for dj in ("y", "z"):
+        lay_j = LayoutDescriptor(n, n, n, sz, dj)
+        rot = VelocityField(*(GroupedField(lay_j, _reorder_tensor(fields.component(c).data, n,
+                                                                  sz, "x", dj))
+                              for c in range(3)), fields.nu, fields.h)
+        for i in range(3):
+            _contribution_into(i, dj, rot, scratch, False, rank_count)
+            _reorder_tensor(scratch, n, sz, dj, "x", out=acc[i], accumulate=True)
+    return tuple(GroupedField(lay, a) for a in acc)
+
+
+def euler_step(fields, dt, rank_count=1):
+    """u <- u + dt * RHS(u) (momentum.py:216-222)."""
+    rhs = evaluate_transport_rhs(fields, rank_count=rank_count)
+    comps = [GroupedField(fields.layout, fields.component(i).data + dt * rhs[i].data)
+             for i in range(3)]
+    return VelocityField(comps[0], comps[1], comps[2], fields.nu, fields.h)

@@ -181,6 +181,21 @@ def main():
     out.update(c1_field=sub, c1_out=run_distd2(sysm, sub, stencil=StencilCoeffs(st)),
                c1_full_sum=np.array(run_distd2(sysm, fld, stencil=StencilCoeffs(st)).sum()))
 
+    # ---- momentum transport RHS (momentum.py:142-169) ----------------------
+    from tds.momentum import VelocityField, evaluate_transport_rhs
+    from tds.layout import unpack as ref_unpack
+    n = 16
+    x = 2 * np.pi * np.arange(n) / n
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    u3 = np.sin(X) * np.cos(Y) + 0.3 * np.cos(Z) + 0.01 * rng.standard_normal((n, n, n))
+    v3 = np.cos(X) * np.sin(Z) - 0.2 * np.sin(Y)
+    w3 = np.sin(Y) * np.cos(Z) + 0.1 * np.cos(X)
+    out.update(tr_u=u3, tr_v=v3, tr_w=w3)
+    for tag, nu in (("nu", 0.1), ("inviscid", 0.0)):
+        f = VelocityField.from_arrays(u3, v3, w3, nu, 2 * np.pi / n, sz=4)
+        rhs = evaluate_transport_rhs(f)
+        out[f"tr_{tag}_rhs"] = np.stack([ref_unpack(r) for r in rhs])
+
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays, {len(runs)} run_distd2 cases")
 

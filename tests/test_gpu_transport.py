@@ -1,0 +1,80 @@
+"""Momentum-transport RHS (BASELINE config 5's consumer of the DistD2 path):
+GPU pipeline vs the reference's own evaluate_transport_rhs (golden, 16^3) and
+vs the pinned oracle (fused k_transport path, 64^3)."""
+
+import numpy as np
+import pytest
+
+from oracle import tds_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2411_13532_b200 as T  # noqa: E402
+
+TOL = 1e-12
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _rel(got, want):
+    return O.rel_linf(np.asarray(got), want)
+
+
+@pytest.mark.parametrize("tag,nu", [("nu", 0.1), ("inviscid", 0.0)])
+def test_transport_rhs_matches_reference_golden(golden, tag, nu):
+    n = 16
+    f = T.VelocityField.from_arrays(golden["tr_u"], golden["tr_v"], golden["tr_w"], nu,
+                                    2 * np.pi / n, sz=4)
+    rhs = T.evaluate_transport_rhs(f)
+    want = golden[f"tr_{tag}_rhs"]
+    for i in range(3):
+        assert _rel(T.unpack(rhs[i]).cpu().numpy(), want[i]) <= TOL
+
+
+@pytest.mark.parametrize("sz", [32, 8])
+def test_fused_transport_kernel_vs_oracle(sz):
+    n = 64
+    r = np.random.default_rng(sz)
+    u3, v3, w3 = (r.standard_normal((n, n, n)) for _ in range(3))
+    h, nu = 2 * np.pi / n, 0.05
+    f = T.VelocityField.from_arrays(u3, v3, w3, nu, h, sz=sz)
+    rhs = T.evaluate_transport_rhs(f)
+    want = O.transport_rhs(u3, v3, w3, nu, h, sz)
+    for i in range(3):
+        assert _rel(T.unpack(rhs[i]).cpu().numpy(), want[i]) <= TOL
+    # one directional contribution through the public API as well
+    c = T.directional_contribution("v", "x", f)
+    lo, di, up, st = O.assemble("d1", n, h, True)
+    lo2, di2, up2, st2 = O.assemble("d2", n, h, True)
+    pu = O.pack(v3, sz, "x")
+    adv = O.pack(u3, sz, "x")
+    dc = O.run_distd2(lo, di, up, True, pu, st)
+    dp = O.run_distd2(lo, di, up, True, adv * pu, st)
+    ref = -0.5 * (adv * dc + dp) + nu * O.run_distd2(lo2, di2, up2, True, pu, st2)
+    assert _rel(c.data.cpu().numpy(), ref) <= TOL
+
+
+def test_transport_emulated_ranks_and_euler_step():
+    n = 64
+    x = 2 * np.pi * np.arange(n) / n
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    u3 = np.sin(X) * np.cos(Y) + 0.3 * np.cos(Z)
+    v3 = np.cos(X) * np.sin(Z) - 0.2 * np.sin(Y)
+    w3 = np.sin(Y) * np.cos(Z) + 0.1 * np.cos(X)
+    f = T.VelocityField.from_arrays(u3, v3, w3, 0.1, 2 * np.pi / n, sz=32)
+    one = T.evaluate_transport_rhs(f)
+    two = T.evaluate_transport_rhs(f, rank_count=2)   # DistD2 truncation at 2 ranks
+    for a, b in zip(one, two):
+        assert _rel(b.data.cpu().numpy(), a.data.cpu().numpy()) <= 1e-10
+    step = T.euler_step(f, 1e-3)
+    for i in range(3):
+        np.testing.assert_allclose(step.component(i).data.cpu().numpy(),
+                                   (f.component(i).data + 1e-3 * one[i].data).cpu().numpy(),
+                                   rtol=0, atol=1e-15)
+    with pytest.raises(ValueError):
+        T.directional_contribution("u", "y", f)
