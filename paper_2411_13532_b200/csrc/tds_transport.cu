@@ -101,7 +101,7 @@ __device__ __forceinline__ void bounds(const double2* __restrict__ hr, const dou
 }  // namespace
 
 template <int M>
-__global__ void __launch_bounds__(256, 1) k_transport(const __grid_constant__ TransportArgs p) {
+__global__ void __launch_bounds__(512) k_transport(const __grid_constant__ TransportArgs p) {
     extern __shared__ double sY[];                     // [3][tpc][K][TL]
     const int C = p.chunks, K = 2 * C;
     const int t = threadIdx.x;
@@ -114,28 +114,33 @@ __global__ void __launch_bounds__(256, 1) k_transport(const __grid_constant__ Tr
     const long long lb = valid ? line_base(line, p.rows, p.sz) : 0;
     const double* ui = p.ui + lb;
     const double* uj = p.uj + lb;
+    double* ob = p.out + lb + (long long)(chunk * M) * sz;
     const int r0 = chunk * M;
     const size_t ybuf = (size_t)p.tiles_per_cta * K * TL;
     double* Y = sY + (size_t)tl * K * TL;
 
-    double acc[M];
+    // The running contribution lives in `out` (this thread's own rows, kept
+    // in L2 between the three solves), not in registers: each solve needs
+    // the full single-solve register budget.
     double v[M + 4], d[M];
     double F, L;
 
-    // (A) d(u_i)/dx_j  ->  acc = u_j * du_i
+    // (A) d(u_i)/dx_j  ->  out = u_j * du_i
     load_window<M>(ui, sz, r0, p.rows, valid, v);
     sweeps<M>(p.t1, v, d);
     Y[(2 * chunk) * TL + lane] = d[0];
     Y[(2 * chunk + 1) * TL + lane] = d[M - 1];
     __syncthreads();
     bounds(p.H1 + (size_t)chunk * K, Y, K, lane, F, L);
+    if (valid) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-        const double x = i == 0 ? F : (i == M - 1 ? L : fma(-p.t1.sc[i], L, fma(-p.t1.sa[i], F, d[i])));
-        acc[i] = (valid ? __ldg(uj + (long long)(r0 + i) * sz) : 0.0) * x;
+        for (int i = 0; i < M; ++i) {
+            const double x = i == 0 ? F : (i == M - 1 ? L : fma(-p.t1.sc[i], L, fma(-p.t1.sa[i], F, d[i])));
+            ob[(long long)i * sz] = __ldg(uj + (long long)(r0 + i) * sz) * x;
+        }
     }
 
-    // (B) d(u_j u_i)/dx_j  ->  acc += dprod
+    // (B) d(u_j u_i)/dx_j  ->  out = -1/2 (out + dprod)
     load_window_prod<M>(uj, ui, sz, r0, p.rows, valid, v);
     sweeps<M>(p.t1, v, d);
     Y += ybuf;
@@ -143,13 +148,18 @@ __global__ void __launch_bounds__(256, 1) k_transport(const __grid_constant__ Tr
     Y[(2 * chunk + 1) * TL + lane] = d[M - 1];
     __syncthreads();
     bounds(p.H1 + (size_t)chunk * K, Y, K, lane, F, L);
+    const bool last = !p.has_nu;
+    if (valid) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-        const double x = i == 0 ? F : (i == M - 1 ? L : fma(-p.t1.sc[i], L, fma(-p.t1.sa[i], F, d[i])));
-        acc[i] = -0.5 * (acc[i] + x);
+        for (int i = 0; i < M; ++i) {
+            const double x = i == 0 ? F : (i == M - 1 ? L : fma(-p.t1.sc[i], L, fma(-p.t1.sa[i], F, d[i])));
+            const double val = -0.5 * (ob[(long long)i * sz] + x);
+            if (last) __stcs(ob + (long long)i * sz, val);
+            else ob[(long long)i * sz] = val;
+        }
     }
 
-    // (C) nu d2(u_i)/dx_j2
+    // (C) out += nu d2(u_i)/dx_j2
     if (p.has_nu) {
         load_window<M>(ui, sz, r0, p.rows, valid, v);
         sweeps<M>(p.t2, v, d);
@@ -158,25 +168,20 @@ __global__ void __launch_bounds__(256, 1) k_transport(const __grid_constant__ Tr
         Y[(2 * chunk + 1) * TL + lane] = d[M - 1];
         __syncthreads();
         bounds(p.H2 + (size_t)chunk * K, Y, K, lane, F, L);
+        if (valid) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-            const double x = i == 0 ? F : (i == M - 1 ? L : fma(-p.t2.sc[i], L, fma(-p.t2.sa[i], F, d[i])));
-            acc[i] = fma(p.nu, x, acc[i]);
+            for (int i = 0; i < M; ++i) {
+                const double x = i == 0 ? F : (i == M - 1 ? L : fma(-p.t2.sc[i], L, fma(-p.t2.sa[i], F, d[i])));
+                __stcs(ob + (long long)i * sz, fma(p.nu, x, ob[(long long)i * sz]));
+            }
         }
-    }
-    if (!valid) return;
-    double* ob = p.out + lb;
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        double* o = ob + (long long)(r0 + i) * sz;
-        if (p.accumulate) *o = *o + acc[i];
-        else __stcs(o, acc[i]);
     }
 }
 
 int launch_transport(const TransportArgs& a, cudaStream_t s) {
     const int threads = a.tiles_per_cta * a.chunks * TL;
-    if (threads > 256) return set_err(TDS_ERR_UNSUPPORTED, "fused transport: n > 512");
+    if (threads > 512) return set_err(TDS_ERR_UNSUPPORTED, "fused transport: n > 1024");
+    if (a.accumulate) return set_err(TDS_ERR_UNSUPPORTED, "fused transport writes, never accumulates");
     const long long tiles = (a.lines + TL - 1) / TL;
     const long long grid = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
     if (grid <= 0) return TDS_OK;

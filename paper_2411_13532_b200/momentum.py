@@ -23,7 +23,10 @@ from .distributed import _stream_handle, get_plan, run_distd2
 from .layout import GroupedField, LayoutDescriptor, pack
 from .system import SubdomainPartition
 
+import threading
+
 _COMPONENTS = ("u", "v", "w")
+_TRUSTED = threading.local()
 _DIRECTIONS = ("x", "y", "z")
 
 
@@ -52,6 +55,8 @@ class VelocityField:
             raise ValueError("velocity components must share one layout")
         if not (lay.nx == lay.ny == lay.nz):
             raise ValueError("transport demo expects a cubic grid")
+        if getattr(_TRUSTED, "on", False):      # re-laid-out copies of checked data
+            return
         torch = _torch()
         for f in (self.u, self.v, self.w):
             data = f.data
@@ -177,9 +182,13 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     scratch = torch.empty_like(acc[0])
     for dj in ("y", "z"):
         lay_j = LayoutDescriptor(n, n, n, sz, dj)
-        rot = VelocityField(*(GroupedField(lay_j, _reorder_tensor(fields.component(c).data, n,
-                                                                  sz, "x", dj))
-                              for c in range(3)), fields.nu, fields.h)
+        _TRUSTED.on = True
+        try:
+            rot = VelocityField(*(GroupedField(lay_j, _reorder_tensor(fields.component(c).data,
+                                                                      n, sz, "x", dj))
+                                  for c in range(3)), fields.nu, fields.h)
+        finally:
+            _TRUSTED.on = False
         for i in range(3):
             _contribution_into(i, dj, rot, scratch, False, rank_count)
             _reorder_tensor(scratch, n, sz, dj, "x", out=acc[i], accumulate=True)
