@@ -112,6 +112,20 @@ class Clocks:
 
 # ------------------------------------------------------------ GPU arm
 
+def operator(T, args, n):
+    """The solved operator: 6th-order compact d/dx (default) or d2/dx2
+    (compact.py:49-56), periodic unless --open (one-sided closures,
+    compact.py:59-96; d/dx only, as in the reference)."""
+    scheme = (T.sixth_order_first_derivative if args.operator == "d1"
+              else T.second_derivative_scheme)(2 * np.pi / n)
+    return T.assemble(scheme, n, periodic=not args.open)
+
+
+def op_name(args):
+    return (("6th-order compact d/dx" if args.operator == "d1" else "compact d2/dx2")
+            + (", open (one-sided closures)" if args.open else ", periodic"))
+
+
 def make_fields(torch, n, dev, seed):
     """Three SZ-blocked fields (x, y, z) of one random n^3 fp64 field."""
     import paper_2411_13532_b200 as T
@@ -130,7 +144,7 @@ def run_single(args, torch):
     n = args.size or 512
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    sys_, st = T.assemble(T.sixth_order_first_derivative(2 * np.pi / n), n, periodic=True)
+    sys_, st = operator(T, args, n)
     part = T.SubdomainPartition((n,))
     fields = make_fields(torch, n, dev, 1234 + 1)
     outs = {d: torch.empty_like(fields[d]) for d in "xyz"}
@@ -189,8 +203,7 @@ def run_single(args, torch):
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (randn fp64 field, seed 1235), operator = assemble(6th-order d/dx, "
-                "periodic)",
+        "data": f"synthetic (randn fp64 field, seed 1235), operator = assemble({op_name(args)})",
         "config": {"workload": f"{n}^3 x/y/z DistD2 solve, 1 GPU (BASELINE configs[1])",
                    "n": n, "directions": "x,y,z", "sz": SZ, "partition": [n],
                    "path": plan.path, "chunk_rows": plan.info.chunk_rows,
@@ -253,9 +266,9 @@ def run_multi(args, torch):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     n = args.size or 1024
-    sys_, st = T.assemble(T.sixth_order_first_derivative(2 * np.pi / n), n, periodic=True)
+    sys_, st = operator(T, args, n)
     part = T.SubdomainPartition.balanced(n, world)
-    ctx = RankContext.from_process_group(cyclic=True)
+    ctx = RankContext.from_process_group(cyclic=sys_.periodic)
     solver = T.DistD2Rank(sys_, st, part, ctx)
     m = part.local_sizes[rank]
     groups = n * n // SZ
@@ -311,7 +324,7 @@ def run_multi(args, torch):
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (randn fp64 local slabs)",
+            "dtype": "f64", "data": f"synthetic (randn fp64 local slabs), operator = {op_name(args)}",
             "config": {"workload": f"{n}^3 x/y/z DistD2 solve decomposed along the solve "
                                    f"direction over {world} GPUs (BASELINE configs[2])",
                        "n": n, "directions": "x,y,z", "sz": SZ,
@@ -485,6 +498,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=0, help="grid extent (default 512 / 1024)")
+    ap.add_argument("--operator", default="d1", choices=["d1", "d2"])
+    ap.add_argument("--open", action="store_true", help="non-periodic (d1 only)")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-groups", type=int, default=256, help="max SZ-groups per CPU worker")
     args = ap.parse_args()

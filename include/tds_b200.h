@@ -55,7 +55,9 @@ typedef struct {
     int strict;         /* 1 if TDS_FLAG_STRICT                               */
     int chunk_rows;     /* M (fast path)                                      */
     int chunks;         /* C = block_rows / M (fast path)                     */
-    int uniform;        /* 1: every chunk shares one coefficient table        */
+    int uniform;        /* 1: every chunk shares one coefficient table;       *
+                         * 2: all but a special first / last chunk do       *
+                         *    (one-sided closures); 0: per-row table        */
     int periodic;
     double max_dropped; /* max |dropped coupling| over ranks (audit)          */
     double dominance_margin; /* system.py:163-167 of the global system        */

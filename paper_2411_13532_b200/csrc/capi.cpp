@@ -41,6 +41,10 @@ tds::FastArgs fast_args(const tds_plan* p, long long lines, int sz) {
     a.det_prev = p->det_prev;
     a.det_next = p->det_next;
     a.ut = p->ut;
+    a.special_first = p->special_first;
+    a.e_first = p->e_first;
+    a.e_last = p->e_last;
+    a.special_last = p->special_last;
     a.dd_defer16 = p->dd_defer[0];
     a.dd_defer8 = p->dd_defer[1];
     return a;
@@ -373,9 +377,10 @@ extern "C" int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2
                                           void* stream) {
     if (!d1 || !u_i || !u_j || !out) return set_err(TDS_ERR_INVALID, "null argument");
     const bool ok1 = d1->path == TDS_PATH_FAST && d1->uniform && d1->M == 32 && d1->P == 1 &&
-                     d1->rank < 0;
+                     d1->rank < 0 && !d1->special_first && !d1->special_last;
     const bool ok2 = !d2 || (d2->path == TDS_PATH_FAST && d2->uniform && d2->M == 32 &&
-                             d2->P == 1 && d2->rank < 0 && d2->C == d1->C);
+                             d2->P == 1 && d2->rank < 0 && d2->C == d1->C &&
+                             !d2->special_first && !d2->special_last);
     if (!ok1 || !ok2 || (nu != 0.0 && !d2))
         return set_err(TDS_ERR_UNSUPPORTED,
                        "fused transport needs uniform P=1 plans with 32-row chunks");

@@ -319,18 +319,43 @@ int fast_tables(tds_plan* p, const Global& g, int M, ChunkSet& cs) {
             t[8] = (i == 0 || i == M - 1) ? 0.0 : co.sa[i];
             t[9] = (i == 0 || i == M - 1) ? 0.0 : co.sc[i];
         }
-    bool uni = M <= tds::MMAX_UNIFORM;
-    for (int row = 0; row < p->block_rows && uni; ++row) {
-        const double* t = &tab[size_t(row) * tds::NCOEF];
-        const double* t0 = &tab[size_t(row % M) * tds::NCOEF];
-        if (std::memcmp(t + 5, t0 + 5, 5 * sizeof(double)) != 0) uni = false;
-        if (std::memcmp(t, &tab[0], 5 * sizeof(double)) != 0) uni = false;
+    // Uniform table: every chunk (and stencil row) bitwise identical to a
+    // reference chunk. The first / last chunk may differ (one-sided closures
+    // of open operators, rank-edge rows): they are flagged and read the
+    // global table while all other chunks use the kernel-parameter copy.
+    const int C = cs.C;
+    const int ref = C >= 3 ? 1 : 0;
+    auto chunk_is_ref = [&](int k) {
+        for (int i = 0; i < M; ++i) {
+            const double* t = &tab[size_t(k * M + i) * tds::NCOEF];
+            const double* t0 = &tab[size_t(ref * M + i) * tds::NCOEF];
+            if (std::memcmp(t + 5, t0 + 5, 5 * sizeof(double)) != 0) return false;
+            if (std::memcmp(t, &tab[size_t(ref * M) * tds::NCOEF], 5 * sizeof(double)) != 0)
+                return false;
+        }
+        return true;
+    };
+    bool uni = M <= tds::MMAX_UNIFORM && chunk_is_ref(ref);
+    for (int k = 1; k + 1 < C && uni; ++k)
+        if (!chunk_is_ref(k)) uni = false;
+    p->special_first = p->special_last = 0;
+    if (uni && C >= 3) {
+        p->special_first = chunk_is_ref(0) ? 0 : 1;
+        p->special_last = chunk_is_ref(C - 1) ? 0 : 1;
+        for (int i = 0; i < M; ++i)
+            for (int o = 0; o < tds::NCOEF; ++o) {
+                p->e_first.c[i][o] = tab[size_t(i) * tds::NCOEF + o];
+                p->e_last.c[i][o] = tab[size_t((C - 1) * M + i) * tds::NCOEF + o];
+            }
+    } else if (uni) {
+        for (int k = 0; k < C && uni; ++k)
+            if (!chunk_is_ref(k)) uni = false;
     }
     p->uniform = uni;
     if (uni) {
-        for (int o = 0; o < 5; ++o) p->ut.st[o] = tab[o];
+        for (int o = 0; o < 5; ++o) p->ut.st[o] = tab[size_t(ref * M) * tds::NCOEF + o];
         for (int i = 0; i < M; ++i) {
-            const double* t = &tab[size_t(i) * tds::NCOEF];
+            const double* t = &tab[size_t(ref * M + i) * tds::NCOEF];
             p->ut.f[i] = t[5];
             p->ut.r[i] = t[6];
             p->ut.w[i] = t[7];
@@ -736,7 +761,7 @@ extern "C" int tds_plan_query(const tds_plan* p, tds_plan_info* info) {
     info->strict = (p->flags & TDS_FLAG_STRICT) ? 1 : 0;
     info->chunk_rows = p->M;
     info->chunks = p->C;
-    info->uniform = p->uniform ? 1 : 0;
+    info->uniform = !p->uniform ? 0 : (p->special_first || p->special_last) ? 2 : 1;
     info->periodic = p->periodic;
     info->max_dropped = p->max_dropped;
     info->dominance_margin = p->margin;

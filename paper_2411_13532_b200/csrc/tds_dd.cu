@@ -106,8 +106,9 @@ __device__ __forceinline__ double take(double* slot, const DDArgs& A, unsigned l
 
 }  // namespace
 
-template <int M, bool UNIFORM, int TLT>
+template <int M, int TAB, int TLT>
 __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
+    constexpr bool UNIFORM = TAB != TAB_GLOBAL;
     const FastArgs& p = A.t.f;
     extern __shared__ __align__(1024) unsigned char smem[];
     const int C = p.chunks;
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         }
 
         double d[M];
-        chunk_sweeps<M, UNIFORM>(p, tb, v, d);
+        chunk_sweeps_any<M, TAB>(p, tb, v, d, chunk);
 
         double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TLT;
         Y[(2 * chunk) * TLT + lane] = d[0];
@@ -278,8 +279,8 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             L = fma(h0.y, us, fma(hl.y, ue, L));
         }
         if (valid)
-            chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F, L,
-                                    A.t.store_cs != 0);
+            chunk_store_any<M, TAB>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F, L,
+                                        A.t.store_cs != 0, chunk);
     }
 }
 
@@ -292,8 +293,9 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
 // their chunks (F', L', d rows, g.Y) in shared memory, and finish item t-1
 // -- whose neighbour values arrived an iteration ago -- so the NVLink round
 // trip is off the critical path.
-template <int M, bool UNIFORM, int TLT>
+template <int M, int TAB, int TLT>
 __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
+    constexpr bool UNIFORM = TAB != TAB_GLOBAL;
     const FastArgs& p = A.t.f;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int CW = 32 / TLT;                       // chunks per warp
@@ -366,6 +368,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
         }
     };
+    auto edge_finish = [&](const EdgeTable& T, double* ob, double F, double L) {
+        __stcs(ob + (long long)r0 * sz, F);
+#pragma unroll
+        for (int i = 1; i < M - 1; ++i)
+            __stcs(ob + (long long)(r0 + i) * sz,
+                   fma(-T.c[i][9], L, fma(-T.c[i][8], F, stash[i * 32])));
+        __stcs(ob + (long long)(r0 + M - 1) * sz, L);
+    };
     // finish the stashed item `fi` (edge warps only; warp-synchronous)
     auto finish = [&](long long fi, int fslot) {
         const double* GY = sGY + ((size_t)fslot * tpc + tl) * 2 * TLT;
@@ -402,6 +412,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         }
         if (!fv) return;
         double* ob = p.out + line_base(fl, rows, p.sz);
+        if (TAB == TAB_EDGES && p.special_first && first_chunk) {
+            edge_finish(p.e_first, ob, F, L);
+            return;
+        }
+        if (TAB == TAB_EDGES && p.special_last && last_chunk) {
+            edge_finish(p.e_last, ob, F, L);
+            return;
+        }
         __stcs(ob + (long long)r0 * sz, F);
 #pragma unroll
         for (int i = 1; i < M - 1; ++i) {
@@ -474,7 +492,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         }
 
         double d[M];
-        chunk_sweeps<M, UNIFORM>(p, tb, v, d);
+        chunk_sweeps_any<M, TAB>(p, tb, v, d, chunk);
 
         double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TLT;
         Y[(2 * chunk) * TLT + lane] = d[0];
@@ -503,7 +521,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             }
             if (valid)
                 chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F,
-                                        L, true);
+                                        L, true);   // interior warps: never a special chunk
         } else {
             if (!helpers && valid && (first_chunk || last_chunk)) {
                 for (int r = 0; r < 2; ++r) {
@@ -538,7 +556,7 @@ size_t dd_smem(const FastArgs& a, TileCfg c) {
     return tma_smem(a, c) + (size_t)c.tpc * 2 * c.tl * 8;
 }
 
-template <int M, bool UNI, int TLT>
+template <int M, int UNI, int TLT>
 int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     DDArgs A = A0;
     FastArgs& a = A.t.f;
@@ -577,7 +595,7 @@ size_t dd2_smem(const FastArgs& a, TileCfg c, int M) {
     return tma_smem(a, c) + (size_t)c.tpc * 2 * (M + 1) * 32 * 8 + (size_t)4 * c.tpc * c.tl * 8;
 }
 
-template <int M, bool UNI, int TLT>
+template <int M, int UNI, int TLT>
 int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     DDArgs A = A0;
     FastArgs& a = A.t.f;
@@ -616,7 +634,7 @@ bool defer_policy() {
     return true;
 }
 
-template <int M, bool UNI>
+template <int M, int UNI>
 int launch_dd_m(const DDArgs& A, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(A.t.f);
     // deferral pays only if some warps are interior (chunks > 2 warps' worth)
@@ -652,8 +670,15 @@ int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail
     A.timeout_ns = 10ULL * 1000 * 1000 * 1000;   // 10 s: a stall records an error
     if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
         A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
-    if (M == 32) return uniform ? launch_dd_m<32, true>(A, s) : launch_dd_m<32, false>(A, s);
-    if (M == 16) return uniform ? launch_dd_m<16, true>(A, s) : launch_dd_m<16, false>(A, s);
+    const int tab = !uniform ? TAB_GLOBAL
+                    : (a.special_first || a.special_last) ? TAB_EDGES : TAB_UNIFORM;
+#define DISPATCH_TAB(MM)                                                                \
+    return tab == TAB_UNIFORM ? launch_dd_m<MM, TAB_UNIFORM>(A, s)                      \
+           : tab == TAB_EDGES ? launch_dd_m<MM, TAB_EDGES>(A, s)                        \
+                              : launch_dd_m<MM, TAB_GLOBAL>(A, s);
+    if (M == 32) { DISPATCH_TAB(32) }
+    if (M == 16) { DISPATCH_TAB(16) }
+#undef DISPATCH_TAB
     return set_err(TDS_ERR_UNSUPPORTED, "unsupported chunk size");
 }
 

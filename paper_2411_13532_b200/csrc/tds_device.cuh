@@ -181,5 +181,69 @@ __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __r
     }
 }
 
+// Sweeps / store of a special (edge) chunk of a uniform plan: per-row
+// coefficients from an EdgeTable in kernel-parameter space, so they stay
+// constant-bank operands like the uniform table (no global loads to hoist).
+template <int M>
+__device__ __forceinline__ void edge_sweeps(const EdgeTable& T, const double (&v)[M + 4],
+                                            double (&d)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const double* c = T.c[i];
+        double rhs = c[0] * v[i];
+        rhs = fma(c[1], v[i + 1], rhs);
+        rhs = fma(c[2], v[i + 2], rhs);
+        rhs = fma(c[3], v[i + 3], rhs);
+        rhs = fma(c[4], v[i + 4], rhs);
+        if (i < 2) d[i] = rhs * c[6];
+        else d[i] = fma(-c[6], d[i - 1], rhs) * c[5];
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) d[i] = fma(-T.c[i][7], d[i + 1], d[i]);
+    d[0] = fma(-T.c[0][7], d[1], d[0]) * T.c[0][5];
+}
+
+template <int M>
+__device__ __forceinline__ void edge_store(const EdgeTable& T, double* __restrict__ ob,
+                                           long long sz, int r0, const double (&d)[M], double F,
+                                           double L, bool stream) {
+    if (stream) {
+        __stcs(ob + (long long)r0 * sz, F);
+#pragma unroll
+        for (int i = 1; i < M - 1; ++i)
+            __stcs(ob + (long long)(r0 + i) * sz, fma(-T.c[i][9], L, fma(-T.c[i][8], F, d[i])));
+        __stcs(ob + (long long)(r0 + M - 1) * sz, L);
+    } else {
+        ob[(long long)r0 * sz] = F;
+#pragma unroll
+        for (int i = 1; i < M - 1; ++i)
+            ob[(long long)(r0 + i) * sz] = fma(-T.c[i][9], L, fma(-T.c[i][8], F, d[i]));
+        ob[(long long)(r0 + M - 1) * sz] = L;
+    }
+}
+
+// Chunk sweeps / store of a (possibly edge-special) chunk.
+template <int M, int TAB>
+__device__ __forceinline__ void chunk_sweeps_any(const FastArgs& p, const double* __restrict__ tb,
+                                                 const double (&v)[M + 4], double (&d)[M],
+                                                 int chunk) {
+    if (TAB == TAB_EDGES && p.special_first && chunk == 0) edge_sweeps<M>(p.e_first, v, d);
+    else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
+        edge_sweeps<M>(p.e_last, v, d);
+    else chunk_sweeps<M, TAB != TAB_GLOBAL>(p, tb, v, d);
+}
+
+template <int M, int TAB>
+__device__ __forceinline__ void chunk_store_any(const FastArgs& p, const double* __restrict__ tb,
+                                                double* __restrict__ ob, long long sz, int r0,
+                                                const double (&d)[M], double F, double L,
+                                                bool stream, int chunk) {
+    if (TAB == TAB_EDGES && p.special_first && chunk == 0)
+        edge_store<M>(p.e_first, ob, sz, r0, d, F, L, stream);
+    else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
+        edge_store<M>(p.e_last, ob, sz, r0, d, F, L, stream);
+    else chunk_store<M, TAB != TAB_GLOBAL>(p, tb, ob, sz, r0, d, F, L, stream);
+}
+
 }  // namespace dev
 }  // namespace tds

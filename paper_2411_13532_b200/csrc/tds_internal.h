@@ -29,6 +29,18 @@ struct UniformTable {
     double sa[MMAX_UNIFORM], sc[MMAX_UNIFORM];
 };
 
+// Per-row table of one special chunk (first / last chunk of an otherwise
+// uniform plan: one-sided closures of open operators). Row i holds the
+// stencil s0..s4, f, r, w, sa, sc -- the layout of the global `tab`.
+struct EdgeTable {
+    double c[MMAX_UNIFORM][NCOEF];
+};
+
+// Coefficient source of the fast kernels (template parameter TAB): the
+// global per-row table, the uniform table, or the uniform table with an
+// EdgeTable for a special first / last chunk.
+enum { TAB_GLOBAL = 0, TAB_UNIFORM = 1, TAB_EDGES = 2 };
+
 struct FastArgs {
     const double* u;
     double* out;
@@ -52,8 +64,10 @@ struct FastArgs {
     int edge_mode;
     int has_prev, has_next;
     int dd_defer16, dd_defer8;   // deferred-edge fused kernel allowed (see plan.cpp)
+    int special_first, special_last;   // uniform plan whose first / last chunk uses e_first / e_last
     double sa_first, sc_last, prev_sc_last, next_sa_first, det_prev, det_next;
     UniformTable ut;
+    EdgeTable e_first, e_last;
 };
 
 // Staged (reference-arithmetic) kernels: one thread per (line, block).
@@ -135,7 +149,9 @@ struct tds_plan {
     // fast path
     int M = 0, C = 0, K = 0;
     bool uniform = false;
+    int special_first = 0, special_last = 0;
     tds::UniformTable ut{};
+    tds::EdgeTable e_first{}, e_last{};
     double* d_tab = nullptr;
     double2* d_Hp = nullptr;
     double* d_g = nullptr;

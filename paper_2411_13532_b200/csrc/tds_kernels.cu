@@ -193,6 +193,8 @@ static int launch_fast_t(const FastArgs& a, long long tiles, cudaStream_t s) {
 int launch_fast(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
                 cudaStream_t s) {
     if (tma_eligible(M, a)) return launch_tma(M, mode, uniform, a, tiles, s);
+    // k_fast has no per-chunk table switch: edge-special plans use the table path
+    if (a.special_first || a.special_last) uniform = false;
 #define DISPATCH_MODE(MM)                                                             \
     switch (mode) {                                                                   \
         case MODE_SOLVE:                                                              \

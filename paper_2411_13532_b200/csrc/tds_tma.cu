@@ -27,8 +27,9 @@ namespace tds {
 
 using namespace dev;
 
-template <int M, int MODE, bool UNIFORM, int TLT>
+template <int M, int MODE, int TAB, int TLT>
 __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) {
+    constexpr bool UNIFORM = TAB != TAB_GLOBAL;
     const FastArgs& p = A.f;
     extern __shared__ __align__(1024) unsigned char smem[];
     const int C = p.chunks;
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         }
 
         double d[M];
-        chunk_sweeps<M, UNIFORM>(p, tb, v, d);
+        chunk_sweeps_any<M, TAB>(p, tb, v, d, chunk);
 
         double* Y = sY + (it & 1) * ybuf + (size_t)tl * K * TLT;
         double y0 = d[0], yL = d[M - 1];
@@ -149,14 +150,14 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         double F, L;
         chunk_bounds<TLT>(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
         if (valid)
-            chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, p.rows, p.sz), sz, r0, d, F,
-                                    L, A.store_cs != 0);
+            chunk_store_any<M, TAB>(p, tb, p.out + line_base(line, p.rows, p.sz), sz, r0, d, F,
+                                        L, A.store_cs != 0, chunk);
     }
 }
 
 namespace {
 
-template <int M, int MODE, bool UNI, int TLT>
+template <int M, int MODE, int UNI, int TLT>
 int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     TmaArgs A;
     A.f = a;
@@ -189,7 +190,7 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     return cuda_check(cudaGetLastError(), "k_tma launch");
 }
 
-template <int M, int MODE, bool UNI>
+template <int M, int MODE, int UNI>
 int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(a);
     if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
@@ -277,21 +278,22 @@ bool tma_eligible(int M, const FastArgs& a) {
 
 int launch_tma(int M, int mode, bool uniform, const FastArgs& a, long long /*tiles*/,
                cudaStream_t s) {
+    const int tab = !uniform ? TAB_GLOBAL
+                    : (a.special_first || a.special_last) ? TAB_EDGES : TAB_UNIFORM;
+#define DISPATCH_TAB(MM, MO)                                                            \
+    return tab == TAB_UNIFORM ? launch_tma_m<MM, MO, TAB_UNIFORM>(a, s)                 \
+           : tab == TAB_EDGES ? launch_tma_m<MM, MO, TAB_EDGES>(a, s)                   \
+                              : launch_tma_m<MM, MO, TAB_GLOBAL>(a, s);
 #define DISPATCH_MODE(MM)                                                               \
     switch (mode) {                                                                     \
-        case MODE_SOLVE:                                                                \
-            return uniform ? launch_tma_m<MM, MODE_SOLVE, true>(a, s)                   \
-                           : launch_tma_m<MM, MODE_SOLVE, false>(a, s);                 \
-        case MODE_PASS_A:                                                               \
-            return uniform ? launch_tma_m<MM, MODE_PASS_A, true>(a, s)                  \
-                           : launch_tma_m<MM, MODE_PASS_A, false>(a, s);                \
-        default:                                                                        \
-            return uniform ? launch_tma_m<MM, MODE_PASS_B, true>(a, s)                  \
-                           : launch_tma_m<MM, MODE_PASS_B, false>(a, s);                \
+        case MODE_SOLVE: DISPATCH_TAB(MM, MODE_SOLVE)                                   \
+        case MODE_PASS_A: DISPATCH_TAB(MM, MODE_PASS_A)                                 \
+        default: DISPATCH_TAB(MM, MODE_PASS_B)                                          \
     }
     if (M == 32) { DISPATCH_MODE(32) }
     if (M == 16) { DISPATCH_MODE(16) }
 #undef DISPATCH_MODE
+#undef DISPATCH_TAB
     return set_err(TDS_ERR_UNSUPPORTED, "unsupported chunk size");
 }
 

@@ -69,9 +69,26 @@ def test_fast_path_is_taken_for_benchmark_shapes(golden):
     c = golden_run(golden, "d1p512_P1")
     plan = T.get_plan(_sys(c), _st(c), T.SubdomainPartition(c["sizes"]))
     assert plan.path == "fast" and plan.info.uniform == 1 and plan.info.chunk_rows == 32
+    # open closures only touch the first / last chunk: uniform table + two
+    # edge tables (uniform == 2), not the per-row global table
     c = golden_run(golden, "d1o512_P8")
     plan = T.get_plan(_sys(c), _st(c), T.SubdomainPartition(c["sizes"]))
-    assert plan.path == "fast" and plan.info.uniform == 0
+    assert plan.path == "fast" and plan.info.uniform == 2
+
+
+@pytest.mark.parametrize("sz,groups", [(32, 64), (16, 48), (8, 40)])
+def test_open_edge_chunks_tma_sizes(sz, groups):
+    """Config 4 (open d/dx, one-sided closures) at sizes that take the
+    TMA-staged kernel with edge-special chunk tables, vs the oracle."""
+    n = 512
+    lo, di, up, st = O.assemble("d1", n, 2 * np.pi / n, False)
+    s = T.TridiagonalSystem(lo, di, up, periodic=False)
+    fld = np.random.default_rng(sz).standard_normal((groups, n, sz))
+    plan = T.get_plan(s, T.StencilCoeffs(st), T.SubdomainPartition([n]))
+    assert plan.info.uniform == 2
+    want = O.run_distd2(lo, di, up, False, fld, st)
+    got = T.run_distd2(s, torch.from_numpy(fld).cuda(), stencil=T.StencilCoeffs(st))
+    assert O.rel_linf(got.cpu().numpy(), want) <= TOL
 
 
 def test_device_tensor_in_device_tensor_out(golden):
