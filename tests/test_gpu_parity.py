@@ -71,9 +71,13 @@ def test_fast_path_is_taken_for_benchmark_shapes(golden):
     assert plan.path == "fast" and plan.info.uniform == 1 and plan.info.chunk_rows == 32
     # open closures only touch the first / last chunk: uniform table + two
     # edge tables (uniform == 2), not the per-row global table
-    c = golden_run(golden, "d1o512_P8")
+    c = golden_run(golden, "d1o512_P1")
     plan = T.get_plan(_sys(c), _st(c), T.SubdomainPartition(c["sizes"]))
     assert plan.path == "fast" and plan.info.uniform == 2
+    # emulated P = 8: rank-edge chunks differ too -> per-row table
+    c = golden_run(golden, "d1o512_P8")
+    plan = T.get_plan(_sys(c), _st(c), T.SubdomainPartition(c["sizes"]))
+    assert plan.path == "fast" and plan.info.uniform == 0
 
 
 @pytest.mark.parametrize("sz,groups", [(32, 64), (16, 48), (8, 40)])
