@@ -204,6 +204,10 @@ int tds_transport_combine(const double* u_j, const double* du, const double* dp,
  * (reorder, layout.py:144-152); accumulate = 1 adds into dst */
 int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,
                 int dst_dir, int accumulate, void* stream);
+/* the same for an (nx, ny, nz) block (a rank's slab of the transport step);
+ * both layouts must be unpadded (lines divisible by sz) */
+int tds_reorder3(const double* src, double* dst, int nx, int ny, int nz, int sz,
+                 int src_dir, int dst_dir, int accumulate, void* stream);
 
 /* ---- layout (layout.py:82-152) -------------------------------------------
  * Cartesian (nx, ny, nz) C-order <-> SZ-blocked (groups, n, sz) field for

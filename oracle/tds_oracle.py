@@ -428,17 +428,23 @@ def rel_linf(got, want):
 
 # --------------------------------------------------------------- momentum.py
 
-def transport_rhs(u3, v3, w3, nu, h, sz):
+def transport_rhs(u3, v3, w3, nu, h, sz, rank_counts=(1, 1, 1)):
     """momentum.py:102-169 (evaluate_transport_rhs with directional_contribution),
     same operation order: per direction j, per component i,
     -0.5 * (u_j * d(u_i) + d(u_j * u_i)) [+ nu * d2(u_i)], folded into x-layout
-    accumulators. Inputs / outputs are Cartesian (n, n, n)."""
+    accumulators. Inputs / outputs are Cartesian (n, n, n).
+    rank_counts: DistD2 ranks per direction, each solve partitioned with
+    balanced_sizes (momentum.py:84-87 passes one rank_count to every
+    direction; (P, P, P) is the reference's evaluate_transport_rhs(rank_count=P),
+    (1, 1, P) the z-slab multi-GPU decomposition)."""
     n = u3.shape[0]
     ops = {k: assemble(k, n, h, True) for k in ("d1", "d2")}
+    cur = {"dir": "x"}
 
     def diff(vals, kind):
         lo, di, up, st = ops[kind]
-        return run_distd2(lo, di, up, True, vals, st)
+        p = rank_counts["xyz".index(cur["dir"])]
+        return run_distd2(lo, di, up, True, vals, st, balanced_sizes(n, p))
 
     def contrib(comp, advect):
         d_comp = diff(comp, "d1")
@@ -451,6 +457,7 @@ def transport_rhs(u3, v3, w3, nu, h, sz):
     vel3 = (u3, v3, w3)
     acc = None
     for j, dj in enumerate("xyz"):
+        cur["dir"] = dj
         comps = [pack(c, sz, dj) for c in vel3]
         for i in range(3):
             c = contrib(comps[i], comps[j])

@@ -361,8 +361,8 @@ extern "C" int tds_ipc_free(void* ptr) { return tds::cuda_check(cudaFree(ptr), "
 
 namespace tds {
 struct TransportArgs;
-int launch_reorder(const double* src, double* dst, int n, int sz, int src_dir, int dst_dir,
-                   int accumulate, cudaStream_t s);
+int launch_reorder(const double* src, double* dst, int nx, int ny, int nz, int sz, int src_dir,
+                   int dst_dir, int accumulate, cudaStream_t s);
 int launch_transport_combine(const double* uj, const double* du, const double* dp,
                              const double* d2u, double nu, double* out, long long count,
                              int accumulate, cudaStream_t s);
@@ -388,13 +388,23 @@ extern "C" int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2
                                             accumulate, groups * sz, sz, S(stream));
 }
 
+extern "C" int tds_reorder3(const double* src, double* dst, int nx, int ny, int nz, int sz,
+                            int src_dir, int dst_dir, int accumulate, void* stream) {
+    if (!src || !dst || nx < 1 || ny < 1 || nz < 1 || nz > 65535 || sz < 1 || src_dir < 0 ||
+        src_dir > 2 || dst_dir < 0 || dst_dir > 2)
+        return set_err(TDS_ERR_INVALID, "bad reorder arguments");
+    const long long pts = (long long)nx * ny * nz;
+    const int ns[3] = {nx, ny, nz};
+    if (pts / ns[src_dir] % sz || pts / ns[dst_dir] % sz)
+        return set_err(TDS_ERR_INVALID, "lines not divisible by sz");
+    if (pts / ns[src_dir] > 0xffffffffLL || pts / ns[dst_dir] > 0xffffffffLL)
+        return set_err(TDS_ERR_INVALID, "too many lines for 32-bit line indices");
+    return tds::launch_reorder(src, dst, nx, ny, nz, sz, src_dir, dst_dir, accumulate, S(stream));
+}
+
 extern "C" int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,
                            int dst_dir, int accumulate, void* stream) {
-    if (!src || !dst || n < 1 || sz < 1 || src_dir < 0 || src_dir > 2 || dst_dir < 0 ||
-        dst_dir > 2)
-        return set_err(TDS_ERR_INVALID, "bad reorder arguments");
-    if ((long long)n * n % sz) return set_err(TDS_ERR_INVALID, "lines not divisible by sz");
-    return tds::launch_reorder(src, dst, n, sz, src_dir, dst_dir, accumulate, S(stream));
+    return tds_reorder3(src, dst, n, n, n, sz, src_dir, dst_dir, accumulate, stream);
 }
 
 extern "C" int tds_transport_combine(const double* uj, const double* du, const double* dp,

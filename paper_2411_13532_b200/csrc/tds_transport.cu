@@ -192,22 +192,24 @@ int launch_transport(const TransportArgs& a, cudaStream_t s) {
 
 // ----------------------------------------------------------- re-layout
 
-__device__ __forceinline__ long long fidx(int i, int j, int k, int n, int sz, int lsz, int dir) {
-    unsigned t, pos;
-    if (dir == 0) { t = (unsigned)j + (unsigned)n * (unsigned)k; pos = i; }
-    else if (dir == 1) { t = (unsigned)i + (unsigned)n * (unsigned)k; pos = j; }
-    else { t = (unsigned)i + (unsigned)n * (unsigned)j; pos = k; }
+__device__ __forceinline__ long long fidx(int i, int j, int k, int nx, int ny, int nz, int sz,
+                                          int lsz, int dir) {
+    unsigned t, pos, n;
+    if (dir == 0) { t = (unsigned)j + (unsigned)ny * (unsigned)k; pos = i; n = nx; }
+    else if (dir == 1) { t = (unsigned)i + (unsigned)nx * (unsigned)k; pos = j; n = ny; }
+    else { t = (unsigned)i + (unsigned)nx * (unsigned)j; pos = k; n = nz; }
     unsigned g, l;
     if (lsz >= 0) { g = t >> lsz; l = t & ((1u << lsz) - 1u); }
     else { g = t / (unsigned)sz; l = t - g * (unsigned)sz; }
     return ((long long)g * n + pos) * sz + l;
 }
 
-// cubic n^3 field in `src_dir` layout -> `dst_dir` layout (dst = or +=).
+// (nx, ny, nz) field in `src_dir` layout -> `dst_dir` layout (dst = or +=).
 // The fastest field axis is j for x layouts and i for y / z layouts, so a
 // 32 x 32 (i, j) tile at fixed k serves every pair of directions.
-__global__ void k_reorder(const double* __restrict__ src, double* __restrict__ dst, int n, int sz,
-                          int lsz, int src_dir, int dst_dir, int accumulate) {
+__global__ void k_reorder(const double* __restrict__ src, double* __restrict__ dst, int nx,
+                          int ny, int nz, int sz, int lsz, int src_dir, int dst_dir,
+                          int accumulate) {
     __shared__ double tile[32][33];                   // [jj][ii]
     const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32, k = blockIdx.z;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -216,15 +218,16 @@ __global__ void k_reorder(const double* __restrict__ src, double* __restrict__ d
     for (int r = ty; r < 32; r += 8) {
         const int ii = src_fast_i ? tx : r, jj = src_fast_i ? r : tx;
         const int i = i0 + ii, j = j0 + jj;
-        if (i < n && j < n) tile[jj][ii] = __ldcs(src + fidx(i, j, k, n, sz, lsz, src_dir));
+        if (i < nx && j < ny)
+            tile[jj][ii] = __ldcs(src + fidx(i, j, k, nx, ny, nz, sz, lsz, src_dir));
     }
     __syncthreads();
 #pragma unroll
     for (int r = ty; r < 32; r += 8) {
         const int ii = dst_fast_i ? tx : r, jj = dst_fast_i ? r : tx;
         const int i = i0 + ii, j = j0 + jj;
-        if (i < n && j < n) {
-            double* o = dst + fidx(i, j, k, n, sz, lsz, dst_dir);
+        if (i < nx && j < ny) {
+            double* o = dst + fidx(i, j, k, nx, ny, nz, sz, lsz, dst_dir);
             const double v = tile[jj][ii];
             if (accumulate) *o = *o + v;
             else __stcs(o, v);
@@ -232,15 +235,16 @@ __global__ void k_reorder(const double* __restrict__ src, double* __restrict__ d
     }
 }
 
-int launch_reorder(const double* src, double* dst, int n, int sz, int src_dir, int dst_dir,
-                   int accumulate, cudaStream_t s) {
+int launch_reorder(const double* src, double* dst, int nx, int ny, int nz, int sz, int src_dir,
+                   int dst_dir, int accumulate, cudaStream_t s) {
     int lsz = -1;
     if ((sz & (sz - 1)) == 0) {
         lsz = 0;
         while ((1 << lsz) < sz) ++lsz;
     }
-    dim3 grid((n + 31) / 32, (n + 31) / 32, n);
-    k_reorder<<<grid, dim3(32, 8), 0, s>>>(src, dst, n, sz, lsz, src_dir, dst_dir, accumulate);
+    dim3 grid((nx + 31) / 32, (ny + 31) / 32, nz);
+    k_reorder<<<grid, dim3(32, 8), 0, s>>>(src, dst, nx, ny, nz, sz, lsz, src_dir, dst_dir,
+                                           accumulate);
     return cuda_check(cudaGetLastError(), "k_reorder launch");
 }
 

@@ -195,6 +195,132 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     return tuple(GroupedField(lay, a) for a in acc)
 
 
+def _local_contribution(comp, advect, out, n, h, nu, accumulate):
+    """out (=|+=) the contribution along a direction whose lines are whole on
+    this device: comp, advect, out are (groups, n, sz) tensors."""
+    torch = _torch()
+    groups, rows, sz = comp.shape
+    s1, st1 = _operator(1, h, n)
+    s2, st2 = _operator(2, h, n)
+    part = SubdomainPartition((n,))
+    p1 = get_plan(s1, st1, part)
+    p2 = get_plan(s2, st2, part) if nu != 0.0 else None
+    rc = N.lib().tds_transport_contribution(
+        p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
+        float(nu), int(accumulate), groups, sz, _stream_handle())
+    if rc == N.TDS_OK:
+        return
+    if rc != N.TDS_ERR_UNSUPPORTED:
+        N.check(rc)
+    d_comp = run_distd2(s1, comp, stencil=st1)
+    d_prod = run_distd2(s1, torch.mul(advect, comp), stencil=st1)
+    d2 = run_distd2(s2, comp, stencil=st2) if nu != 0.0 else None
+    N.check(N.lib().tds_transport_combine(
+        _vp(advect), _vp(d_comp), _vp(d_prod), None if d2 is None else _vp(d2),
+        float(nu), _vp(out), out.numel(), int(accumulate), _stream_handle()))
+
+
+class SlabTransport:
+    """The transport right-hand side (BASELINE config 5) on P GPUs, one
+    process per GPU: rank r owns the z-slab [off_r, off_r + m_r) of the
+    periodic n^3 box (SubdomainPartition.balanced(n, P), system.py:148-155).
+
+    * x and y lines are whole on every rank: those contributions are local
+      (fused k_transport when n <= 512, else three solves + combine);
+    * z lines are split across the ranks: each z contribution is three
+      DistD2 solves along the rank chain (DistD2Rank: the fused k_dd/k_dd2
+      kernels with in-kernel NVLink exchange) + k_transport_combine -- the
+      reference's evaluate_transport_rhs (momentum.py:142-169) with its
+      rank_count applied to z, the direction the box is decomposed along.
+    Local fields are x-layout (n*m/sz, n, sz) tensors of the rank's slab,
+    i.e. pack(u3[:, :, off:off+m], LayoutDescriptor(n, n, m, sz, 'x')).
+    The layouts of the slab (x, y: whole lines; z: this rank's rows of every
+    global z line) are reached with the one-pass k_reorder (tds_reorder3)."""
+
+    def __init__(self, n, sz, nu, h, ctx=None):
+        from .rank import DistD2Rank
+        self.n, self.sz, self.nu, self.h, self.ctx = n, sz, float(nu), float(h), ctx
+        p = 1 if ctx is None else ctx.rank_count
+        self.part = SubdomainPartition.balanced(n, p)
+        r = 0 if ctx is None else ctx.rank_id
+        self.m = self.part.local_sizes[r]
+        self.off = self.part.offsets()[r]
+        self.lay = {d: LayoutDescriptor(n, n, self.m, sz, d) for d in _DIRECTIONS}
+        self._rank = None
+        if p > 1:
+            if not ctx.cyclic:
+                raise ValueError("the transport box is periodic: the rank chain must be a ring")
+            s1, st1 = _operator(1, self.h, n)
+            s2, st2 = _operator(2, self.h, n)
+            self._rank = (DistD2Rank(s1, st1, self.part, ctx),
+                          DistD2Rank(s2, st2, self.part, ctx) if self.nu != 0.0 else None)
+
+    def local_slab(self, u3):
+        """Pack this rank's slab of a global Cartesian (n, n, n) array for x."""
+        torch = _torch()
+        t = u3 if isinstance(u3, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(u3))
+        slab = t[:, :, self.off:self.off + self.m].to("cuda", torch.float64).contiguous()
+        return pack(slab, self.lay["x"]).data
+
+    def _reorder(self, src, a, b, out=None, accumulate=False):
+        torch = _torch()
+        dst = self.lay[b]
+        res = (torch.empty((dst.n_groups, dst.n, dst.sz), dtype=torch.float64,
+                           device=src.device) if out is None else out)
+        N.check(N.lib().tds_reorder3(_vp(src), _vp(res), self.n, self.n, self.m, self.sz,
+                                     _DIRECTIONS.index(a), _DIRECTIONS.index(b),
+                                     int(accumulate), _stream_handle()))
+        return res
+
+    def _z_contribution(self, comp, advect, out):
+        torch = _torch()
+        if self._rank is None:
+            _local_contribution(comp, advect, out, self.m, self.h, self.nu, False)
+            return
+        r1, r2 = self._rank
+        d_comp = r1.solve(comp)
+        d_prod = r1.solve(torch.mul(advect, comp))
+        d2 = r2.solve(comp) if r2 is not None else None
+        N.check(N.lib().tds_transport_combine(
+            _vp(advect), _vp(d_comp), _vp(d_prod), None if d2 is None else _vp(d2),
+            self.nu, _vp(out), out.numel(), 0, _stream_handle()))
+
+    def rhs(self, u, v, w):
+        """Local x-layout slabs of u, v, w -> local x-layout RHS of each
+        component (momentum.py:142-169, same per-direction grouping)."""
+        torch = _torch()
+        vel = (u, v, w)
+        acc = [torch.empty_like(u) for _ in range(3)]
+        for i in range(3):
+            _local_contribution(vel[i], vel[0], acc[i], self.n, self.h, self.nu, False)
+        rot = [self._reorder(c, "x", "y") for c in vel]
+        scratch = torch.empty_like(rot[0])
+        for i in range(3):
+            _local_contribution(rot[i], rot[1], scratch, self.n, self.h, self.nu, False)
+            self._reorder(scratch, "y", "x", out=acc[i], accumulate=True)
+        rot = [self._reorder(c, "x", "z") for c in vel]
+        scratch = torch.empty_like(rot[0])
+        for i in range(3):
+            self._z_contribution(rot[i], rot[2], scratch)
+            self._reorder(scratch, "z", "x", out=acc[i], accumulate=True)
+        return tuple(acc)
+
+    def euler_step(self, u, v, w, dt):
+        """u <- u + dt * RHS(u) on this rank's slab (momentum.py:216-222)."""
+        rhs = self.rhs(u, v, w)
+        return tuple(c + dt * r for c, r in zip((u, v, w), rhs))
+
+    def check(self):
+        for r in self._rank or ():
+            if r is not None:
+                r.check()
+
+    def close(self):
+        for r in self._rank or ():
+            if r is not None:
+                r.close()
+
+
 def euler_step(fields, dt, rank_count=1):
     """u <- u + dt * RHS(u) (momentum.py:216-222)."""
     rhs = evaluate_transport_rhs(fields, rank_count=rank_count)

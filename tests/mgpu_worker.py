@@ -84,6 +84,38 @@ def main():
          groups=3, seed=4)
     lo, di, up, st = O.assemble("d1", 1024, 2 * np.pi / 1024, True)
     case("d1 periodic strict", lo, di, up, True, st, 1024, arith="strict", seed=5)
+
+    # config 5: transport RHS on a z-slab decomposition (SlabTransport)
+    for nu in (0.02, 0.0):
+        n, sz = 128, 16
+        rng = np.random.default_rng(77)
+        u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
+        ctx = RankContext.from_process_group(cyclic=True)
+        tr = T.SlabTransport(n, sz, nu, 2 * np.pi / n, ctx)
+        loc = [tr.local_slab(a) for a in (u3, v3, w3)]
+        rhs = tr.rhs(*loc)
+        rhs2 = tr.rhs(*loc)
+        torch.cuda.synchronize()
+        tr.check()
+        same = all(bool(torch.equal(a, b)) for a, b in zip(rhs, rhs2))
+        fulls = []
+        for comp in rhs:
+            cart = T.unpack(T.GroupedField(tr.lay["x"], comp))          # (n, n, m)
+            g = gather_to_root(ctx, cart.permute(2, 0, 1).unsqueeze(0).contiguous())
+            fulls.append(None if g is None else g[0].permute(1, 2, 0).cpu().numpy())
+        tr.close()
+        if rank == 0:
+            want = O.transport_rhs(u3, v3, w3, nu, 2 * np.pi / n, sz, rank_counts=(1, 1, world))
+            errs = [O.rel_linf(g, w) for g, w in zip(fulls, want)]
+            ref_p = O.transport_rhs(u3, v3, w3, nu, 2 * np.pi / n, sz,
+                                    rank_counts=(world, world, world))
+            errs_p = [O.rel_linf(g, w) for g, w in zip(fulls, ref_p)]
+            ok = same and max(errs) <= 1e-12 and max(errs_p) <= 1e-12
+            print(f"[transport slab nu={nu}] P={world} m={tr.m} fused_z={tr._rank[0].fused} "
+                  f"rel(1,1,P)={max(errs):.3e} rel(P,P,P)={max(errs_p):.3e} repeat_same={same} "
+                  f"{'OK' if ok else 'FAIL'}", flush=True)
+            if not ok:
+                failures.append(f"transport nu={nu}")
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:

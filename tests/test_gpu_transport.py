@@ -78,3 +78,43 @@ def test_transport_emulated_ranks_and_euler_step():
                                    rtol=0, atol=1e-15)
     with pytest.raises(ValueError):
         T.directional_contribution("u", "y", f)
+
+
+@pytest.mark.parametrize("extents,sz", [((64, 48, 16), 16), ((40, 24, 8), 8), ((32, 32, 96), 32)])
+def test_reorder3_block_bitwise(extents, sz):
+    """One-pass k_reorder on non-cubic blocks (a rank's slab): bitwise equal
+    to unpack + pack, and accumulate adds exactly."""
+    rng = np.random.default_rng(sum(extents))
+    cart = rng.standard_normal(extents)
+    for a in "xyz":
+        f = T.pack(cart, T.LayoutDescriptor(*extents, sz, a))
+        for b in "xyz":
+            want = T.pack(cart, T.LayoutDescriptor(*extents, sz, b)).data
+            got = T.reorder(f, b)
+            np.testing.assert_array_equal(got.data, want)
+    fx = torch.from_numpy(T.pack(cart, T.LayoutDescriptor(*extents, sz, "x")).data).cuda()
+    lz = T.LayoutDescriptor(*extents, sz, "z")
+    acc = torch.from_numpy(T.pack(cart, lz).data).cuda()
+    import ctypes
+    from paper_2411_13532_b200 import _native as N
+    N.check(N.lib().tds_reorder3(ctypes.c_void_p(fx.data_ptr()), ctypes.c_void_p(acc.data_ptr()),
+                                 *extents, sz, 0, 2, 1, None))
+    np.testing.assert_array_equal(acc.cpu().numpy(), 2 * T.pack(cart, lz).data)
+
+
+@pytest.mark.parametrize("nu", [0.05, 0.0])
+def test_slab_transport_single_rank(nu):
+    """SlabTransport with one rank (whole box on this GPU) vs the oracle and
+    vs evaluate_transport_rhs."""
+    n, sz = 64, 16
+    rng = np.random.default_rng(21)
+    u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
+    tr = T.SlabTransport(n, sz, nu, 2 * np.pi / n)
+    rhs = tr.rhs(*(tr.local_slab(a) for a in (u3, v3, w3)))
+    want = O.transport_rhs(u3, v3, w3, nu, 2 * np.pi / n, sz)
+    f = T.VelocityField.from_arrays(u3, v3, w3, nu, 2 * np.pi / n, sz=sz)
+    ev = T.evaluate_transport_rhs(f)
+    for i in range(3):
+        got = T.unpack(T.GroupedField(tr.lay["x"], rhs[i])).cpu().numpy()
+        assert _rel(got, want[i]) <= TOL
+        assert torch.equal(rhs[i], ev[i].data)
