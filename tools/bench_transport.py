@@ -1,8 +1,14 @@
-"""Momentum-transport RHS evaluation time on one GPU (BASELINE config 5's
-per-step kernel pipeline, single device): evaluate_transport_rhs on an n^3
-velocity field, CUDA events, best of 5.
+"""Momentum-transport RHS evaluation time (BASELINE config 5's per-step
+kernel pipeline).
 
-Logical traffic of the pipeline per grid point (fp64, 8 B per access):
+Single GPU (default): evaluate_transport_rhs on an n^3 velocity field.
+Multi-GPU (under torchrun): SlabTransport, rank r owning the z-slab
+[off_r, off_r + m) of the n^3 box; z contributions run DistD2 along the
+rank ring (fused k_dd/k_dd2), x/y contributions are local.
+CUDA events, best of `--reps`, max over ranks.
+
+Logical traffic of the single-GPU fused pipeline per grid point (fp64, 8 B
+per access):
   x:      3 contributions, fused (diagonal 16 B, off-diagonal 24 B)  =  64 B
   y, z:   3 one-pass input reorders (16 B each)                       =  48 B
           3 contributions into scratch                                =  64 B
@@ -10,6 +16,8 @@ Logical traffic of the pipeline per grid point (fp64, 8 B per access):
   total   64 + 2 * 184                                                = 432 B
 
     python tools/bench_transport.py [--n 512] [--sz 32] [--nu 0.01]
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
+        --master-port 29533 tools/bench_transport.py --n 1024 --slab
 """
 import argparse
 import json
@@ -30,30 +38,77 @@ def main():
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--sz", type=int, default=32)
     ap.add_argument("--nu", type=float, default=0.01)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--slab", action="store_true",
+                    help="SlabTransport (z-slab decomposition; implied under torchrun)")
     args = ap.parse_args()
     n = args.n
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    ctx = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2411_13532_b200.transport import RankContext
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ctx = RankContext.from_process_group(cyclic=True)
     g = torch.Generator(device="cuda")
-    g.manual_seed(5)
-    u3, v3, w3 = (torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
-                  for _ in range(3))
-    f = T.VelocityField.from_arrays(u3, v3, w3, args.nu, 2 * np.pi / n, sz=args.sz)
-    del u3, v3, w3
-    T.evaluate_transport_rhs(f)
+    g.manual_seed(5 + rank)
+    h = 2 * np.pi / n
+    if world > 1 or args.slab:
+        tr = T.SlabTransport(n, args.sz, args.nu, h, ctx)
+        lay = tr.lay["x"]
+        vel = [torch.randn((lay.n_groups, lay.n, lay.sz), dtype=torch.float64, device="cuda",
+                           generator=g) for _ in range(3)]
+
+        def step():
+            return tr.rhs(*vel)
+        pts_local = n * n * tr.m
+        what = f"SlabTransport z-slabs m={tr.m}, fused_z={bool(tr._rank and tr._rank[0].fused)}"
+    else:
+        u3, v3, w3 = (torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
+                      for _ in range(3))
+        f = T.VelocityField.from_arrays(u3, v3, w3, args.nu, h, sz=args.sz)
+        del u3, v3, w3
+
+        def step():
+            return T.evaluate_transport_rhs(f)
+        pts_local = n ** 3
+        what = "evaluate_transport_rhs"
+    step()
+    torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     best = 1e9
-    for _ in range(5):
+    for _ in range(args.reps):
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         ev[0].record()
-        T.evaluate_transport_rhs(f)
+        step()
         ev[1].record()
         torch.cuda.synchronize()
-        best = min(best, ev[0].elapsed_time(ev[1]))
-    pts = n ** 3
-    print(json.dumps({"workload": f"transport RHS {n}^3, sz={args.sz}, nu={args.nu}",
-                      "ms_per_rhs": round(best, 3),
-                      "gdof_per_s": round(pts / (best * 1e-3) / 1e9, 2),
-                      "logical_gbs": round(BYTES_PER_POINT * pts / (best * 1e-3) / 1e9, 1),
-                      "bytes_per_point": BYTES_PER_POINT}))
+        t = ev[0].elapsed_time(ev[1])
+        if world > 1:
+            tt = torch.tensor([t], device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt.item())
+        best = min(best, t)
+    if world > 1:
+        tr.check()
+        tr.close()
+    if rank == 0:
+        pts = n ** 3
+        print(json.dumps({"workload": f"transport RHS {n}^3 on {world} GPU(s), sz={args.sz}, "
+                                      f"nu={args.nu}: {what}",
+                          "ms_per_rhs": round(best, 3),
+                          "gdof_per_s": round(pts / (best * 1e-3) / 1e9, 2),
+                          "gdof_per_s_per_gpu": round(pts_local / (best * 1e-3) / 1e9, 2),
+                          "logical_gbs_432B": round(BYTES_PER_POINT * pts / (best * 1e-3) / 1e9, 1)}),
+              flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":
