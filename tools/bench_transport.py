@@ -15,9 +15,9 @@ per access):
           3 reorder-accumulates into x (24 B each)                    =  72 B
   total   64 + 2 * 184                                                = 432 B
 
-    python tools/bench_transport.py [--n 512] [--sz 32] [--nu 0.01]
+    python tools/bench_transport.py [--grid 512] [--sz 32] [--nu 0.01]
     python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
-        --master-port 29533 tools/bench_transport.py --n 1024 --slab
+        --master-port 29533 tools/bench_transport.py --grid 1024
 """
 import argparse
 import json
@@ -35,14 +35,14 @@ BYTES_PER_POINT = 432
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--grid", type=int, default=512, help="n of the n^3 box")
     ap.add_argument("--sz", type=int, default=32)
     ap.add_argument("--nu", type=float, default=0.01)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--slab", action="store_true",
                     help="SlabTransport (z-slab decomposition; implied under torchrun)")
     args = ap.parse_args()
-    n = args.n
+    n = args.grid
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     ctx = None
