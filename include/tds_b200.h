@@ -39,6 +39,8 @@ extern "C" {
 #define TDS_FLAG_STRICT 1   /* reference arithmetic order, no FMA: bit-identical
                                to the reference (staged kernels)              */
 #define TDS_FLAG_STAGED 2   /* force the staged (multi-pass) kernels           */
+#define TDS_FLAG_CHUNK16 4  /* prefer 16-row chunks (register-light consumers:
+                               the TMA-staged fused transport kernel)         */
 
 /* execution paths reported by tds_plan_query */
 #define TDS_PATH_FAST 0     /* single-pass chunked kernel (16 B/pt)           */

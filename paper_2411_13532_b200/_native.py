@@ -27,6 +27,7 @@ TDS_ERR_UNSUPPORTED = 6
 
 TDS_FLAG_STRICT = 1
 TDS_FLAG_STAGED = 2
+TDS_FLAG_CHUNK16 = 4
 TDS_PATH_FAST = 0
 TDS_PATH_STAGED = 1
 

@@ -376,14 +376,14 @@ extern "C" int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2
                                           double nu, int accumulate, long long groups, int sz,
                                           void* stream) {
     if (!d1 || !u_i || !u_j || !out) return set_err(TDS_ERR_INVALID, "null argument");
-    const bool ok1 = d1->path == TDS_PATH_FAST && d1->uniform && d1->M == 32 && d1->P == 1 &&
-                     d1->rank < 0 && !d1->special_first && !d1->special_last;
-    const bool ok2 = !d2 || (d2->path == TDS_PATH_FAST && d2->uniform && d2->M == 32 &&
+    const bool ok1 = d1->path == TDS_PATH_FAST && d1->uniform && (d1->M == 32 || d1->M == 16) &&
+                     d1->P == 1 && d1->rank < 0 && !d1->special_first && !d1->special_last;
+    const bool ok2 = !d2 || (d2->path == TDS_PATH_FAST && d2->uniform && d2->M == d1->M &&
                              d2->P == 1 && d2->rank < 0 && d2->C == d1->C &&
                              !d2->special_first && !d2->special_last);
     if (!ok1 || !ok2 || (nu != 0.0 && !d2))
         return set_err(TDS_ERR_UNSUPPORTED,
-                       "fused transport needs uniform P=1 plans with 32-row chunks");
+                       "fused transport needs uniform P=1 plans with 16- or 32-row chunks");
     return tds::transport_launch_from_plans(d1, nu != 0.0 ? d2 : nullptr, u_i, u_j, out, nu,
                                             accumulate, groups * sz, sz, S(stream));
 }

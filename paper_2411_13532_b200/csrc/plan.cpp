@@ -234,7 +234,7 @@ vector<double> reduced(const ChunkSet& cs, int k0, int k1, bool wrap) {
 int pick_chunk(const vector<int>& blocks, int flags, bool rank_block = false) {
     if (flags & (TDS_FLAG_STRICT | TDS_FLAG_STAGED)) return 0;
     // A/B knob for per-rank blocks (fused kernel): TDS_RANK_CHUNK=32|16.
-    int first = 32;
+    int first = (flags & TDS_FLAG_CHUNK16) ? 16 : 32;
     if (const char* e = getenv("TDS_RANK_CHUNK"))
         if (rank_block) first = atoi(e) == 16 ? 16 : 32;
     for (int M : {first, 48 - first}) {

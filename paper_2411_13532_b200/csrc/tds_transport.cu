@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "tds_device.cuh"
+#include "tds_tma.h"
 
 namespace tds {
 
@@ -190,6 +191,257 @@ int launch_transport(const TransportArgs& a, cudaStream_t s) {
     return cuda_check(cudaGetLastError(), "k_transport launch");
 }
 
+// ------------------------------------------------ TMA-staged k_transport
+//
+// k_transport_tma<M, TLT>: persistent CTAs; the u_i and u_j tiles of TLT
+// lines arrive by TMA (3-D tensor maps, one mbarrier) and ALL three solves
+// read them from shared memory, so HBM sees u_i and u_j once and `out`
+// once (24 B/pt, 16 on the diagonal). 16-row chunks keep the running
+// contribution in registers (acc[16] + d[16]); every solve streams its
+// stencil window straight out of shared memory, and the next item's TMA is
+// issued as soon as the last solve's sweeps have read the tiles.
+struct TransportTmaArgs {
+    TransportArgs p;
+    CUtensorMap map_i, map_j;
+    int boxr;
+    long long items;
+};
+
+namespace {
+
+template <int M, typename Src>
+__device__ __forceinline__ void sweeps_src(const UniformTable& T, Src v, double (&d)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double rhs = T.st[0] * v(i);
+        rhs = fma(T.st[1], v(i + 1), rhs);
+        rhs = fma(T.st[2], v(i + 2), rhs);
+        rhs = fma(T.st[3], v(i + 3), rhs);
+        rhs = fma(T.st[4], v(i + 4), rhs);
+        if (i < 2) d[i] = rhs * T.r[i];
+        else d[i] = fma(-T.r[i], d[i - 1], rhs) * T.f[i];
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) d[i] = fma(-T.w[i], d[i + 1], d[i]);
+    d[0] = fma(-T.w[0], d[1], d[0]) * T.f[0];
+}
+
+__device__ __forceinline__ double subst(const UniformTable& T, int i, int M, double F, double L,
+                                        double di) {
+    return i == 0 ? F : (i == M - 1 ? L : fma(-T.sc[i], L, fma(-T.sa[i], F, di)));
+}
+
+}  // namespace
+
+template <int M, int TLT>
+__global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant__ TransportTmaArgs A) {
+    const TransportArgs& p = A.p;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int C = p.chunks, K = 2 * C, rows = p.rows, tpc = p.tiles_per_cta;
+    const int t = threadIdx.x;
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
+    const long long sz = p.sz;
+    const int r0 = chunk * M;
+    const size_t tile_elems = (size_t)rows * TLT;
+    double* ti = reinterpret_cast<double*>(smem);
+    double* tj = ti + (size_t)tpc * tile_elems;
+    double* sY = tj + (size_t)tpc * tile_elems;          // [3][tpc][K][TLT]
+    const size_t ybuf = (size_t)tpc * K * TLT;
+    // coefficient tables in shared memory: read per use inside the item
+    // loop (a kernel-parameter table would be hoisted out of the persistent
+    // loop into registers and spill)
+    UniformTable* sT = reinterpret_cast<UniformTable*>(sY + 3 * ybuf);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sT + 2);
+    const bool diag = p.ui == p.uj;
+    {
+        const double* src1 = reinterpret_cast<const double*>(&p.t1);
+        const double* src2 = reinterpret_cast<const double*>(&p.t2);
+        double* dst = reinterpret_cast<double*>(sT);
+        constexpr int W = sizeof(UniformTable) / sizeof(double);
+        for (int k = t; k < 2 * W; k += blockDim.x) dst[k] = k < W ? src1[k] : src2[k - W];
+    }
+    const UniformTable& T1 = sT[0];
+    const UniformTable& T2 = sT[1];
+
+    auto issue = [&](long long item) {
+        uint32_t bytes = 0;
+        for (int j = 0; j < tpc; ++j)
+            if ((item * tpc + j) * TLT < p.lines)
+                bytes += (uint32_t)((diag ? 1 : 2) * tile_elems * sizeof(double));
+        mbar_expect_tx(bar, bytes);
+        for (int j = 0; j < tpc; ++j) {
+            const long long first = (item * tpc + j) * TLT;
+            if (first >= p.lines) break;
+            const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
+            for (int b = 0; b * A.boxr < rows; ++b) {
+                tma_load_3d(ti + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_i, bar, l0,
+                            b * A.boxr, g);
+                if (!diag)
+                    tma_load_3d(tj + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_j, bar,
+                                l0, b * A.boxr, g);
+            }
+        }
+    };
+
+    if (t == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    long long item = blockIdx.x;
+    if (t == 0 && item < A.items) issue(item);
+    uint32_t phase = 0;
+    const double* Ti = ti + tl * tile_elems;
+    const double* Tj = (diag ? ti : tj) + tl * tile_elems;
+    // stencil window of row r0 - 2 + i: rows r0 .. r0+M-1 at immediate
+    // offsets from `base`, the 2 + 2 periodic halo rows at wrapped offsets
+    const int base = r0 * TLT + lane;
+    const int lo = (chunk == 0 ? rows - 2 : r0 - 2) * TLT + lane;
+    const int hi = (chunk == C - 1 ? 0 : r0 + M) * TLT + lane;
+    auto wrap = [&](int i) {
+        return i < 2 ? lo + i * TLT : (i >= M + 2 ? hi + (i - M - 2) * TLT : base + (i - 2) * TLT);
+    };
+    double* Y0 = sY + (size_t)tl * K * TLT;
+    // every thread has read its last tile value: hand the buffers to the
+    // next item's TMA (it overlaps the reduced solve, substitution, stores)
+    auto release = [&](long long nxt) {
+        __syncthreads();
+        if (t == 0 && nxt < A.items) {
+            fence_proxy_async();
+            issue(nxt);
+        }
+    };
+
+    for (; item < A.items; item += gridDim.x) {
+        const long long line = (item * tpc + tl) * TLT + lane;
+        const bool valid = line < p.lines;
+        const long long nxt = item + gridDim.x;
+        while (!mbar_try_wait(bar, phase)) {
+        }
+        phase ^= 1u;
+        double acc[M], d[M];
+        double F, L;
+
+        // (A) d(u_i)/dx_j -> acc = u_j * du_i
+        sweeps_src<M>(T1, [&](int i) { return Ti[wrap(i)]; }, d);
+        double* Y = Y0;
+        Y[(2 * chunk) * TLT + lane] = d[0];
+        Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+        __syncthreads();
+        chunk_bounds<TLT>(p.H1 + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+#pragma unroll
+        for (int i = 0; i < M; ++i) acc[i] = Tj[base + i * TLT] * subst(T1, i, M, F, L, d[i]);
+
+        // (B) d(u_j u_i)/dx_j -> acc = -1/2 (acc + dprod)
+        sweeps_src<M>(T1, [&](int i) { const int o = wrap(i); return Tj[o] * Ti[o]; }, d);
+        if (!p.has_nu) release(nxt);
+        Y += ybuf;
+        Y[(2 * chunk) * TLT + lane] = d[0];
+        Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+        __syncthreads();
+        chunk_bounds<TLT>(p.H1 + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+#pragma unroll
+        for (int i = 0; i < M; ++i) acc[i] = -0.5 * (acc[i] + subst(T1, i, M, F, L, d[i]));
+
+        // (C) acc += nu d2(u_i)/dx_j2
+        if (p.has_nu) {
+            sweeps_src<M>(T2, [&](int i) { return Ti[wrap(i)]; }, d);
+            release(nxt);
+            Y += ybuf;
+            Y[(2 * chunk) * TLT + lane] = d[0];
+            Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            __syncthreads();
+            chunk_bounds<TLT>(p.H2 + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+#pragma unroll
+            for (int i = 0; i < M; ++i) acc[i] = fma(p.nu, subst(T2, i, M, F, L, d[i]), acc[i]);
+        }
+        if (valid) {
+            double* ob = p.out + line_base(line, rows, p.sz) + (long long)r0 * sz;
+#pragma unroll
+            for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
+        }
+    }
+}
+
+namespace {
+
+template <int M, int TLT>
+int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
+    TransportTmaArgs A;
+    A.p = a;
+    const int per_tile = a.chunks * TLT;
+    A.p.tiles_per_cta = per_tile >= 256 ? 1 : 256 / per_tile;
+    const long long tiles = (a.lines + TLT - 1) / TLT;
+    A.items = (tiles + A.p.tiles_per_cta - 1) / A.p.tiles_per_cta;
+    if (A.items <= 0) return TDS_OK;
+    FastArgs fi{}, fj{};
+    fi.u = a.ui;
+    fj.u = a.uj;
+    fi.rows = fj.rows = a.rows;
+    fi.sz = fj.sz = a.sz;
+    fi.lines = fj.lines = a.lines;
+    int rc = encode_field_map(fi, M, TLT, &A.map_i, &A.boxr);
+    if (rc) return rc;
+    rc = encode_field_map(fj, M, TLT, &A.map_j, &A.boxr);
+    if (rc) return rc;
+    const int threads = A.p.tiles_per_cta * per_tile;
+    const size_t smem = (size_t)A.p.tiles_per_cta *
+                            (2 * (size_t)a.rows * TLT + 3 * (size_t)2 * a.chunks * TLT) *
+                            sizeof(double) + 2 * sizeof(UniformTable) + 16;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        rc = cuda_check(cudaFuncSetAttribute(k_transport_tma<M, TLT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem),
+                        "cudaFuncSetAttribute(k_transport_tma)");
+        if (rc) return rc;
+        smem_set = smem;
+    }
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_transport_tma<M, TLT>, threads, smem);
+    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_tma does not fit on an SM");
+    long long grid = (long long)nb * sms;
+    if (grid > A.items) grid = A.items;
+    k_transport_tma<M, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_transport_tma launch");
+}
+
+}  // namespace
+
+// TMA transport eligibility: 16-row chunks, tiles of 8 / 16 lines that fit.
+static int transport_tma_tl(const TransportArgs& a) {
+    if (const char* e = getenv("TDS_TRANSPORT_TMA"))
+        if (e[0] == '0') return 0;
+    if (reinterpret_cast<uintptr_t>(a.ui) % 16 || reinterpret_cast<uintptr_t>(a.uj) % 16 ||
+        reinterpret_cast<uintptr_t>(a.out) % 16)
+        return 0;
+    if (box_rows(a.rows, 16) == 0) return 0;
+    int pref = 16;
+    if (const char* e = getenv("TDS_TRANSPORT_TL")) pref = atoi(e) == 8 ? 8 : 16;
+    for (int tl : {pref, 24 - pref}) {
+        if (a.sz % tl) continue;
+        const int per_tile = a.chunks * tl;
+        if (per_tile > 512) continue;
+        const int tpc = per_tile >= 256 ? 1 : 256 / per_tile;
+        const size_t smem =
+            (size_t)tpc * (2 * (size_t)a.rows * tl + 6 * (size_t)a.chunks * tl) * 8 +
+            2 * sizeof(UniformTable) + 16;
+        if (smem <= 200 * 1024) return tl;
+    }
+    return 0;
+}
+
+int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
+    const int tl = transport_tma_tl(a);
+    if (tl == 16) return launch_transport_tma_t<16, 16>(a, s);
+    if (tl == 8) return launch_transport_tma_t<16, 8>(a, s);
+    return set_err(TDS_ERR_UNSUPPORTED, "fused transport: shape not TMA-tileable");
+}
+
 // ----------------------------------------------------------- re-layout
 
 __device__ __forceinline__ long long fidx(int i, int j, int k, int nx, int ny, int nz, int sz,
@@ -293,6 +545,10 @@ int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const do
     a.nu = nu;
     a.t1 = d1->ut;
     a.t2 = d2 ? d2->ut : d1->ut;
+    if (d1->M == 16) {
+        if (accumulate) return set_err(TDS_ERR_UNSUPPORTED, "fused transport never accumulates");
+        return launch_transport_tma(a, s);
+    }
     return launch_transport(a, s);
 }
 

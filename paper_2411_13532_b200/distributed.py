@@ -271,18 +271,20 @@ def _flags(arithmetic):
     raise ValueError(f"arithmetic must be 'fast', 'strict' or 'staged', got {arithmetic!r}")
 
 
-def get_plan(sys, stencil, part, rank=-1, arithmetic="fast"):
-    """Cached plan for (operator, partition, rank, arithmetic, device)."""
+def get_plan(sys, stencil, part, rank=-1, arithmetic="fast", chunk_rows=None):
+    """Cached plan for (operator, partition, rank, arithmetic, device).
+    chunk_rows=16 asks for 16-row chunks (TDS_FLAG_CHUNK16)."""
     torch = _torch()
     st = None if stencil is None else stencil.c
     key = (sys.lower.tobytes(), sys.diag.tobytes(), sys.upper.tobytes(), bool(sys.periodic),
            None if st is None else st.tobytes(), part.local_sizes, rank, arithmetic,
-           torch.cuda.current_device())
+           chunk_rows, torch.cuda.current_device())
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
             _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
-        plan = Plan.create(sys, st, part.local_sizes, rank, _flags(arithmetic))
+        flags = _flags(arithmetic) | (N.TDS_FLAG_CHUNK16 if chunk_rows == 16 else 0)
+        plan = Plan.create(sys, st, part.local_sizes, rank, flags)
         _PLAN_CACHE[key] = plan
     return plan
 

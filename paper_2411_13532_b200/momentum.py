@@ -115,6 +115,30 @@ def _direction_name(j):
     return j if isinstance(j, str) else _DIRECTIONS[int(j)]
 
 
+def _fused_contribution(comp, advect, out, n, h, nu, accumulate):
+    """One fused k_transport launch if the shape allows it: the TMA-staged
+    16-row-chunk kernel first, then the 32-row kernel. False = not fused."""
+    groups, _, sz = comp.shape
+    s1, st1 = _operator(1, h, n)
+    s2, st2 = _operator(2, h, n)
+    part = SubdomainPartition((n,))
+    for rows in (16, 32):
+        if accumulate and rows == 16:
+            continue
+        p1 = get_plan(s1, st1, part, chunk_rows=rows)
+        if p1.info.chunk_rows != rows:
+            continue
+        p2 = get_plan(s2, st2, part, chunk_rows=rows) if nu != 0.0 else None
+        rc = N.lib().tds_transport_contribution(
+            p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
+            float(nu), int(accumulate), groups, sz, _stream_handle())
+        if rc == N.TDS_OK:
+            return True
+        if rc != N.TDS_ERR_UNSUPPORTED:
+            N.check(rc)
+    return False
+
+
 def _contribution_into(ci, dj, fields, out, accumulate, rank_count):
     """out (=|+=) the (ci, dj) contribution, all arrays in the dj layout."""
     n = fields.n
@@ -123,17 +147,9 @@ def _contribution_into(ci, dj, fields, out, accumulate, rank_count):
     groups, _, sz = comp.shape
     s1, st1 = _operator(1, fields.h, n)
     s2, st2 = _operator(2, fields.h, n)
-    if rank_count == 1:
-        part = SubdomainPartition((n,))
-        p1 = get_plan(s1, st1, part)
-        p2 = get_plan(s2, st2, part) if fields.nu != 0.0 else None
-        rc = N.lib().tds_transport_contribution(
-            p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
-            float(fields.nu), int(accumulate), groups, sz, _stream_handle())
-        if rc == N.TDS_OK:
-            return
-        if rc != N.TDS_ERR_UNSUPPORTED:
-            N.check(rc)
+    if rank_count == 1 and _fused_contribution(comp, advect, out, n, fields.h, fields.nu,
+                                                accumulate):
+        return
     # general path: three DistD2 solves (any size, emulated ranks) + combine
     d_comp = run_distd2(s1, comp, stencil=st1, rank_count=rank_count)
     d_prod = run_distd2(s1, advect * comp, stencil=st1, rank_count=rank_count)
@@ -199,19 +215,10 @@ def _local_contribution(comp, advect, out, n, h, nu, accumulate):
     """out (=|+=) the contribution along a direction whose lines are whole on
     this device: comp, advect, out are (groups, n, sz) tensors."""
     torch = _torch()
-    groups, rows, sz = comp.shape
+    if _fused_contribution(comp, advect, out, n, h, nu, accumulate):
+        return
     s1, st1 = _operator(1, h, n)
     s2, st2 = _operator(2, h, n)
-    part = SubdomainPartition((n,))
-    p1 = get_plan(s1, st1, part)
-    p2 = get_plan(s2, st2, part) if nu != 0.0 else None
-    rc = N.lib().tds_transport_contribution(
-        p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
-        float(nu), int(accumulate), groups, sz, _stream_handle())
-    if rc == N.TDS_OK:
-        return
-    if rc != N.TDS_ERR_UNSUPPORTED:
-        N.check(rc)
     d_comp = run_distd2(s1, comp, stencil=st1)
     d_prod = run_distd2(s1, torch.mul(advect, comp), stencil=st1)
     d2 = run_distd2(s2, comp, stencil=st2) if nu != 0.0 else None
