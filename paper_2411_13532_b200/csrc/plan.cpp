@@ -375,6 +375,54 @@ int upload_H(tds_plan* p, const vector<double>& H, const vector<double>& gv) {
                 make_double2(H[size_t(2 * k) * K + q], H[size_t(2 * k + 1) * K + q]);
     int rc = upload(p, &p->d_Hp, Hp.data(), Hp.size());
     if (rc) return rc;
+    // Banded copy of H for register-light consumers (k_transport_tma): the
+    // entries of a diagonally dominant reduced map decay geometrically away
+    // from the chunk's own columns. Per chunk, the shortest cyclic window of
+    // columns holding every entry above 2^-70 x the chunk's largest entry;
+    // all chunks use the longest window (padding keeps real entries).
+    {
+        const double rel = std::ldexp(1.0, -70);
+        vector<int> start(C), len(C);
+        int nb = 1;
+        for (int k = 0; k < C; ++k) {
+            double mx = 0.0;
+            for (int q = 0; q < K; ++q)
+                mx = std::max({mx, std::fabs(Hp[size_t(k) * K + q].x),
+                               std::fabs(Hp[size_t(k) * K + q].y)});
+            vector<char> sig(K);
+            int nsig = 0;
+            for (int q = 0; q < K; ++q) {
+                const double2 h = Hp[size_t(k) * K + q];
+                sig[q] = std::fabs(h.x) > rel * mx || std::fabs(h.y) > rel * mx;
+                nsig += sig[q];
+            }
+            if (nsig == 0) { start[k] = 2 * k; len[k] = 1; continue; }
+            // longest cyclic run of insignificant columns -> window = complement
+            int best = 0, best_end = -1, run = 0;
+            for (int q = 0; q < 2 * K; ++q) {
+                if (!sig[q % K]) {
+                    if (++run > best && run <= K) { best = run; best_end = q % K; }
+                } else {
+                    run = 0;
+                }
+            }
+            start[k] = best == 0 ? 0 : (best_end + 1) % K;
+            len[k] = K - best;
+            nb = std::max(nb, len[k]);
+        }
+        vector<double2> Hb(size_t(C) * nb);
+        vector<int> q0(C);
+        for (int k = 0; k < C; ++k) {
+            // centre the padding: widen the window evenly on both sides
+            int st = start[k] - (nb - len[k]) / 2;
+            st = ((st % K) + K) % K;
+            q0[k] = st;
+            for (int j = 0; j < nb; ++j) Hb[size_t(k) * nb + j] = Hp[size_t(k) * K + (st + j) % K];
+        }
+        p->band_n = nb;
+        if ((rc = upload(p, &p->d_Hb, Hb.data(), Hb.size()))) return rc;
+        if ((rc = upload(p, &p->d_bq0, q0.data(), q0.size()))) return rc;
+    }
     return upload(p, &p->d_g, gv.data(), gv.size());
 }
 

@@ -154,6 +154,9 @@ struct tds_plan {
     tds::EdgeTable e_first{}, e_last{};
     double* d_tab = nullptr;
     double2* d_Hp = nullptr;
+    double2* d_Hb = nullptr;   // banded H: C x band_n, columns d_bq0[k] + j (mod K)
+    int* d_bq0 = nullptr;
+    int band_n = 0;
     double* d_g = nullptr;
     double sa_first = 0, sc_last = 0, prev_sc_last = 0, next_sa_first = 0;
     double det_prev = 1, det_next = 1;

@@ -36,6 +36,11 @@ struct TransportArgs {
     int has_nu;
     double nu;
     UniformTable t1, t2;   // chunk tables of the two periodic operators
+    const double2* Hb1;    // banded reduced maps (plan.cpp upload_H)
+    const double2* Hb2;
+    const int* bq1;
+    const int* bq2;
+    int nb1, nb2;
 };
 
 namespace {
@@ -226,6 +231,34 @@ __device__ __forceinline__ void sweeps_src(const UniformTable& T, Src v, double 
     d[0] = fma(-T.w[0], d[1], d[0]) * T.f[0];
 }
 
+// (F, L) of a chunk from the banded reduced map: nb columns starting at q0
+// (cyclic), Y in shared memory with stride TLT
+template <int TLT>
+__device__ __forceinline__ void band_bounds(const double2* __restrict__ hb, int q0, int nb,
+                                            const double* Y, int K, int lane, double& F,
+                                            double& L) {
+    double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
+    int q = q0, j = 0;
+    for (; j + 1 < nb; j += 2) {
+        const double2 h0 = __ldg(hb + j), h1 = __ldg(hb + j + 1);
+        const int qb = q + 1 == K ? 0 : q + 1;
+        const double ya = Y[q * TLT + lane], yb = Y[qb * TLT + lane];
+        F0 = fma(h0.x, ya, F0);
+        L0 = fma(h0.y, ya, L0);
+        F1 = fma(h1.x, yb, F1);
+        L1 = fma(h1.y, yb, L1);
+        q = qb + 1 == K ? 0 : qb + 1;
+    }
+    if (j < nb) {
+        const double2 h0 = __ldg(hb + j);
+        const double ya = Y[q * TLT + lane];
+        F0 = fma(h0.x, ya, F0);
+        L0 = fma(h0.y, ya, L0);
+    }
+    F = F0 + F1;
+    L = L0 + L1;
+}
+
 __device__ __forceinline__ double subst(const UniformTable& T, int i, int M, double F, double L,
                                         double di) {
     return i == 0 ? F : (i == M - 1 ? L : fma(-T.sc[i], L, fma(-T.sa[i], F, di)));
@@ -264,6 +297,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
     }
     const UniformTable& T1 = sT[0];
     const UniformTable& T2 = sT[1];
+    const int bq1 = __ldg(p.bq1 + chunk), bq2 = __ldg(p.bq2 + chunk);
 
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
@@ -330,7 +364,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         Y[(2 * chunk) * TLT + lane] = d[0];
         Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
         __syncthreads();
-        chunk_bounds<TLT>(p.H1 + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+        band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, Y, K, lane, F, L);
 #pragma unroll
         for (int i = 0; i < M; ++i) acc[i] = Tj[base + i * TLT] * subst(T1, i, M, F, L, d[i]);
 
@@ -341,7 +375,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         Y[(2 * chunk) * TLT + lane] = d[0];
         Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
         __syncthreads();
-        chunk_bounds<TLT>(p.H1 + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+        band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, Y, K, lane, F, L);
 #pragma unroll
         for (int i = 0; i < M; ++i) acc[i] = -0.5 * (acc[i] + subst(T1, i, M, F, L, d[i]));
 
@@ -353,7 +387,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
             Y[(2 * chunk) * TLT + lane] = d[0];
             Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
             __syncthreads();
-            chunk_bounds<TLT>(p.H2 + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+            band_bounds<TLT>(p.Hb2 + (size_t)chunk * p.nb2, bq2, p.nb2, Y, K, lane, F, L);
 #pragma unroll
             for (int i = 0; i < M; ++i) acc[i] = fma(p.nu, subst(T2, i, M, F, L, d[i]), acc[i]);
         }
@@ -545,6 +579,12 @@ int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const do
     a.nu = nu;
     a.t1 = d1->ut;
     a.t2 = d2 ? d2->ut : d1->ut;
+    a.Hb1 = d1->d_Hb;
+    a.Hb2 = d2 ? d2->d_Hb : d1->d_Hb;
+    a.bq1 = d1->d_bq0;
+    a.bq2 = d2 ? d2->d_bq0 : d1->d_bq0;
+    a.nb1 = d1->band_n;
+    a.nb2 = d2 ? d2->band_n : d1->band_n;
     if (d1->M == 16) {
         if (accumulate) return set_err(TDS_ERR_UNSUPPORTED, "fused transport never accumulates");
         return launch_transport_tma(a, s);
