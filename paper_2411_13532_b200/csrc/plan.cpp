@@ -11,6 +11,7 @@
 //   rank topology .............. transport.py:113-119
 //   pair determinant ........... distributed.py:288-290
 //   thomas / periodic thomas ... serial.py:26-90
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
