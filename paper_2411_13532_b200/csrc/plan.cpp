@@ -238,10 +238,13 @@ int pick_chunk(const vector<int>& blocks, int flags, bool rank_block = false) {
     int first = (flags & TDS_FLAG_CHUNK16) ? 16 : 32;
     if (const char* e = getenv("TDS_RANK_CHUNK"))
         if (rank_block) first = atoi(e) == 16 ? 16 : 32;
+    // 16-row plans asked for by TDS_FLAG_CHUNK16 (the fused transport kernel,
+    // 8-line tiles) may hold up to 64 chunks
+    const int cmax = (flags & TDS_FLAG_CHUNK16) ? 2 * tds::MAX_CHUNKS : tds::MAX_CHUNKS;
     for (int M : {first, 48 - first}) {
         bool ok = true;
         for (int m : blocks)
-            if (m % M != 0 || m / M > tds::MAX_CHUNKS) ok = false;
+            if (m % M != 0 || m / M > (M == 16 ? cmax : tds::MAX_CHUNKS)) ok = false;
         if (ok) return M;
     }
     return 0;

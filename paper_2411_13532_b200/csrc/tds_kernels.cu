@@ -182,6 +182,8 @@ __global__ void __launch_bounds__(512) k_fast(const __grid_constant__ FastArgs p
 template <int M, int MODE, bool UNI>
 static int launch_fast_t(const FastArgs& a, long long tiles, cudaStream_t s) {
     const int threads = a.tiles_per_cta * a.chunks * TL;
+    if (threads > 512)
+        return set_err(TDS_ERR_UNSUPPORTED, "plans with more than 32 chunks need 8-line TMA tiles");
     const long long grid = (tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
     const size_t smem = (size_t)a.tiles_per_cta * 2 * a.chunks * TL * sizeof(double);
     if (grid <= 0) return TDS_OK;

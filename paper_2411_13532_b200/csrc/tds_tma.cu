@@ -216,6 +216,7 @@ TileCfg tile_cfg(const FastArgs& a) {
     int tl = 16;
     if (const char* e = getenv("TDS_TL")) tl = atoi(e) == 8 ? 8 : 16;
     if (a.sz % tl != 0) tl = (a.sz % 8 == 0) ? 8 : 0;
+    if (tl && a.chunks * tl > 512) tl = (a.chunks * 8 <= 512 && a.sz % 8 == 0) ? 8 : 0;
     TileCfg c{tl, 1};
     if (tl) {
         const int per_tile = a.chunks * tl;
