@@ -241,10 +241,15 @@ int pick_chunk(const vector<int>& blocks, int flags, bool rank_block = false) {
     // 16-row plans asked for by TDS_FLAG_CHUNK16 (the fused transport kernel,
     // 8-line tiles) may hold up to 64 chunks
     const int cmax = (flags & TDS_FLAG_CHUNK16) ? 2 * tds::MAX_CHUNKS : tds::MAX_CHUNKS;
+    // every block chunk-aligned, and the whole line (all blocks: one device
+    // runs every emulated rank) within the chunks of one tile
+    long long total = 0;
+    for (int m : blocks) total += m;
     for (int M : {first, 48 - first}) {
-        bool ok = true;
+        const int lim = M == 16 ? cmax : tds::MAX_CHUNKS;
+        bool ok = total / M <= lim;
         for (int m : blocks)
-            if (m % M != 0 || m / M > (M == 16 ? cmax : tds::MAX_CHUNKS)) ok = false;
+            if (m % M != 0) ok = false;
         if (ok) return M;
     }
     return 0;

@@ -184,6 +184,7 @@ def test_512_lines_all_directions_vs_oracle(direction):
 
 @pytest.mark.parametrize("n,p,periodic,kind", [
     (512, 1, False, "d1"), (512, 2, True, "d1"), (1024, 4, True, "d1"), (1024, 8, False, "d1"),
+    (2048, 8, True, "d1"), (2048, 1, True, "d1"),
     (256, 1, True, "d2"), (256, 4, True, "d2"), (96, 3, True, "rd"), (48, 1, False, "rd"),
     (80, 5, False, "rd"), (64, 2, True, "rd")])
 def test_fast_vs_oracle_sweep(n, p, periodic, kind):
