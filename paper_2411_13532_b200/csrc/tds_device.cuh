@@ -89,11 +89,16 @@ __device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __
             s0 = p.ut.st[0]; s1 = p.ut.st[1]; s2 = p.ut.st[2]; s3 = p.ut.st[3]; s4 = p.ut.st[4];
             f = p.ut.f[i]; r = p.ut.r[i];
         } else {
-            const double2 c01 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF));
-            const double2 c23 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 2));
-            const double2 c4f = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 4));
+            // tb: the per-row table in global or (k_tma) shared memory. The
+            // empty asm ties row i's loads to d[i - 2]: without it the
+            // compiler issues all 32 rows' loads up front and spills.
+            const double* tr = tb + i * NCOEF;
+            if (i >= 2) asm volatile("" : "+l"(tr) : "d"(d[i - 2]));
+            const double2 c01 = *reinterpret_cast<const double2*>(tr);
+            const double2 c23 = *reinterpret_cast<const double2*>(tr + 2);
+            const double2 c4f = *reinterpret_cast<const double2*>(tr + 4);
             s0 = c01.x; s1 = c01.y; s2 = c23.x; s3 = c23.y; s4 = c4f.x; f = c4f.y;
-            r = __ldg(tb + i * NCOEF + 6);
+            r = tr[6];
         }
         double rhs = s0 * v[i];
         rhs = fma(s1, v[i + 1], rhs);
@@ -105,11 +110,18 @@ __device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __
     }
 #pragma unroll
     for (int i = M - 3; i >= 1; --i) {
-        const double w = UNIFORM ? p.ut.w[i] : __ldg(tb + i * NCOEF + 7);
+        double w;
+        if (UNIFORM) {
+            w = p.ut.w[i];
+        } else {
+            const double* tr = tb + i * NCOEF + 7;
+            if (i + 3 < M) asm volatile("" : "+l"(tr) : "d"(d[i + 3]));
+            w = *tr;
+        }
         d[i] = fma(-w, d[i + 1], d[i]);
     }
-    const double w0 = UNIFORM ? p.ut.w[0] : __ldg(tb + 7);
-    const double f0 = UNIFORM ? p.ut.f[0] : __ldg(tb + 5);
+    const double w0 = UNIFORM ? p.ut.w[0] : tb[7];
+    const double f0 = UNIFORM ? p.ut.f[0] : tb[5];
     d[0] = fma(-w0, d[1], d[0]) * f0;
 }
 
@@ -164,8 +176,8 @@ __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __r
         __stcs(ob + (long long)r0 * sz, F);
 #pragma unroll
         for (int i = 1; i < M - 1; ++i) {
-            const double sa = UNIFORM ? p.ut.sa[i] : __ldg(tb + i * NCOEF + 8);
-            const double sc = UNIFORM ? p.ut.sc[i] : __ldg(tb + i * NCOEF + 9);
+            const double sa = UNIFORM ? p.ut.sa[i] : tb[i * NCOEF + 8];
+            const double sc = UNIFORM ? p.ut.sc[i] : tb[i * NCOEF + 9];
             __stcs(ob + (long long)(r0 + i) * sz, fma(-sc, L, fma(-sa, F, d[i])));
         }
         __stcs(ob + (long long)(r0 + M - 1) * sz, L);
@@ -173,8 +185,8 @@ __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __r
         ob[(long long)r0 * sz] = F;
 #pragma unroll
         for (int i = 1; i < M - 1; ++i) {
-            const double sa = UNIFORM ? p.ut.sa[i] : __ldg(tb + i * NCOEF + 8);
-            const double sc = UNIFORM ? p.ut.sc[i] : __ldg(tb + i * NCOEF + 9);
+            const double sa = UNIFORM ? p.ut.sa[i] : tb[i * NCOEF + 8];
+            const double sc = UNIFORM ? p.ut.sc[i] : tb[i * NCOEF + 9];
             ob[(long long)(r0 + i) * sz] = fma(-sc, L, fma(-sa, F, d[i]));
         }
         ob[(long long)(r0 + M - 1) * sz] = L;

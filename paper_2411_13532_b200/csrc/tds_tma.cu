@@ -46,8 +46,15 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     const size_t tile_elems = (size_t)rows * TLT;
     double* sY = tiles + (size_t)tpc * tile_elems;
     const size_t ybuf = (size_t)tpc * K * TLT;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sY + 2 * ybuf);
-    const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
+    // TAB_GLOBAL: the block's per-row table (shared by every line) is staged
+    // in shared memory once per CTA when it fits
+    double* stab = sY + 2 * ybuf;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        stab + (TAB == TAB_GLOBAL && A.tab_smem ? (size_t)rows * NCOEF : 0));
+    if (TAB == TAB_GLOBAL && A.tab_smem)
+        for (int k = t; k < rows * NCOEF; k += blockDim.x) stab[k] = __ldg(p.tab + k);
+    const double* __restrict__ tb =
+        (TAB == TAB_GLOBAL && A.tab_smem ? stab : p.tab) + (size_t)r0 * NCOEF;
 
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
@@ -169,7 +176,11 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     if (rc) return rc;
     A.store_cs = store_policy();
     const int threads = cfg.tpc * a.chunks * TLT;
-    const size_t smem = tma_smem(a, cfg);
+    size_t smem = tma_smem(a, cfg);
+    const size_t tab_bytes = (size_t)a.rows * NCOEF * sizeof(double);
+    A.tab_smem = UNI == TAB_GLOBAL && smem + tab_bytes <= 227 * 1024 &&
+                 !(getenv("TDS_TAB_SMEM") && getenv("TDS_TAB_SMEM")[0] == '0');
+    if (A.tab_smem) smem += tab_bytes;
     static size_t smem_set = 0;
     if (smem > smem_set) {
         rc = cuda_check(cudaFuncSetAttribute(k_tma<M, MODE, UNI, TLT>,

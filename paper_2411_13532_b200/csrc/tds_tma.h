@@ -13,6 +13,7 @@ struct TmaArgs {
     CUtensorMap map;
     int boxr;          // rows per TMA box (divides rows)
     int store_cs;      // streaming stores (A/B knob TDS_STCS)
+    int tab_smem;      // TAB_GLOBAL: per-row table staged in shared memory
 };
 
 // lines per tile (8 or 16; 0 = not TMA-eligible) and tiles per CTA
