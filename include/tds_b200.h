@@ -202,6 +202,15 @@ int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2,
 int tds_transport_combine(const double* u_j, const double* du, const double* dp,
                           const double* d2u, double nu, double* out, long long count,
                           int accumulate, void* stream);
+/* acc += the (i, z) contribution for a cubic n^3 box, everything in the
+ * x layout (groups = n^2/sz, n, sz): the z lines are read in place through a
+ * 4-D tensor map and the result is added into acc, replacing the reference's
+ * reorder(x->z) + contribution + reorder/accumulate(z->x) of one z term
+ * (momentum.py:129-169). Plans: 16-row-chunk P=1 d/dx (d1) and d2/dx2 (d2)
+ * operators of the z lines (TDS_FLAG_CHUNK16); sz | n. */
+int tds_transport_contribution_z(const tds_plan* d1, const tds_plan* d2, const double* u_i,
+                                 const double* u_j, double* acc, double nu, int n, int sz,
+                                 void* stream);
 /* cubic n^3 field: SZ-blocked layout of src_dir -> dst_dir in one pass
  * (reorder, layout.py:144-152); accumulate = 1 adds into dst */
 int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,

@@ -41,7 +41,15 @@ struct TransportArgs {
     const int* bq1;
     const int* bq2;
     int nb1, nb2;
+    int geom;              // GEOM_LINES, or GEOM_XZ: z lines of an x-layout n^3 box
 };
+
+// Tile geometry of k_transport_tma: GEOM_LINES reads / writes the field in
+// its own (groups, rows, sz) layout; GEOM_XZ reads the z lines of a cubic
+// x-layout box in place (4-D tensor map: lanes, x, y-group, z) and ADDS the
+// contribution into an x-layout accumulator -- the z direction of the
+// transport RHS without re-layout passes.
+enum { GEOM_LINES = 0, GEOM_XZ = 1 };
 
 namespace {
 
@@ -266,7 +274,7 @@ __device__ __forceinline__ double subst(const UniformTable& T, int i, int M, dou
 
 }  // namespace
 
-template <int M, int TLT>
+template <int M, int TLT, int GEOM>
 __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant__ TransportTmaArgs A) {
     const TransportArgs& p = A.p;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -308,6 +316,22 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         for (int j = 0; j < tpc; ++j) {
             const long long first = (item * tpc + j) * TLT;
             if (first >= p.lines) break;
+            if (GEOM == GEOM_XZ) {
+                // line = lane-block + sz * (y-group + (n/sz) * x): z line (x, y)
+                const long long tile = first / TLT;
+                const int nlb = p.sz / TLT, ngj = rows / p.sz;
+                const int l0 = (int)(tile % nlb) * TLT;
+                const int gj = (int)((tile / nlb) % ngj);
+                const int x = (int)(tile / ((long long)nlb * ngj));
+                for (int b = 0; b * A.boxr < rows; ++b) {
+                    tma_load_4d(ti + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_i, bar, l0,
+                                x, gj, b * A.boxr);
+                    if (!diag)
+                        tma_load_4d(tj + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_j,
+                                    bar, l0, x, gj, b * A.boxr);
+                }
+                continue;
+            }
             const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
             for (int b = 0; b * A.boxr < rows; ++b) {
                 tma_load_3d(ti + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_i, bar, l0,
@@ -391,7 +415,17 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < M; ++i) acc[i] = fma(p.nu, subst(T2, i, M, F, L, d[i]), acc[i]);
         }
-        if (valid) {
+        if (valid && GEOM == GEOM_XZ) {
+            // x-layout address of (x, y, z): ((y-group + z n/sz) n + x) sz + lane
+            const long long tile = line / TLT;
+            const int nlb = p.sz / TLT, ngj = rows / p.sz;
+            const long long x = tile / ((long long)nlb * ngj);
+            const long long gj = (tile / nlb) % ngj;
+            const long long rs = (long long)rows * rows;        // z stride: n^2
+            double* ob = p.out + (gj * rows + x) * sz + (tile % nlb) * TLT + lane + r0 * rs;
+#pragma unroll
+            for (int i = 0; i < M; ++i) ob[i * rs] = ob[i * rs] + acc[i];
+        } else if (valid) {
             double* ob = p.out + line_base(line, rows, p.sz) + (long long)r0 * sz;
 #pragma unroll
             for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
@@ -401,7 +435,24 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
 
 namespace {
 
-template <int M, int TLT>
+// 4-D view of a cubic x-layout box (G = n^2/sz, n, sz): (lane, x, y-group, z)
+// with group = y-group + z * n/sz; box TLT lanes x 1 x 1 x boxr z-rows.
+int encode_xz_map(const double* u, int n, int sz, int M, int tl, CUtensorMap* map, int* boxr) {
+    *boxr = box_rows(n, M);
+    cuuint64_t dims[4] = {(cuuint64_t)sz, (cuuint64_t)n, (cuuint64_t)(n / sz), (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)sz * 8, (cuuint64_t)n * sz * 8,
+                             (cuuint64_t)n * (cuuint64_t)n * 8};
+    cuuint32_t box[4] = {(cuuint32_t)tl, 1, 1, (cuuint32_t)*boxr};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(u),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_err(TDS_ERR_CUDA, "cuTensorMapEncodeTiled (xz) failed");
+    return TDS_OK;
+}
+
+template <int M, int TLT, int GEOM>
 int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     TransportTmaArgs A;
     A.p = a;
@@ -416,17 +467,21 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     fi.rows = fj.rows = a.rows;
     fi.sz = fj.sz = a.sz;
     fi.lines = fj.lines = a.lines;
-    int rc = encode_field_map(fi, M, TLT, &A.map_i, &A.boxr);
-    if (rc) return rc;
-    rc = encode_field_map(fj, M, TLT, &A.map_j, &A.boxr);
-    if (rc) return rc;
+    int rc;
+    if (GEOM == GEOM_XZ) {
+        if ((rc = encode_xz_map(a.ui, a.rows, a.sz, M, TLT, &A.map_i, &A.boxr))) return rc;
+        if ((rc = encode_xz_map(a.uj, a.rows, a.sz, M, TLT, &A.map_j, &A.boxr))) return rc;
+    } else {
+        if ((rc = encode_field_map(fi, M, TLT, &A.map_i, &A.boxr))) return rc;
+        if ((rc = encode_field_map(fj, M, TLT, &A.map_j, &A.boxr))) return rc;
+    }
     const int threads = A.p.tiles_per_cta * per_tile;
     const size_t smem = (size_t)A.p.tiles_per_cta *
                             (2 * (size_t)a.rows * TLT + 3 * (size_t)2 * a.chunks * TLT) *
                             sizeof(double) + 2 * sizeof(UniformTable) + 16;
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_transport_tma<M, TLT>,
+        rc = cuda_check(cudaFuncSetAttribute(k_transport_tma<M, TLT, GEOM>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem),
                         "cudaFuncSetAttribute(k_transport_tma)");
@@ -436,11 +491,12 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     int dev = 0, sms = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_transport_tma<M, TLT>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_transport_tma<M, TLT, GEOM>, threads,
+                                                  smem);
     if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_tma does not fit on an SM");
     long long grid = (long long)nb * sms;
     if (grid > A.items) grid = A.items;
-    k_transport_tma<M, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_transport_tma<M, TLT, GEOM><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_transport_tma launch");
 }
 
@@ -471,8 +527,14 @@ static int transport_tma_tl(const TransportArgs& a) {
 
 int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
     const int tl = transport_tma_tl(a);
-    if (tl == 16) return launch_transport_tma_t<16, 16>(a, s);
-    if (tl == 8) return launch_transport_tma_t<16, 8>(a, s);
+    if (a.geom == GEOM_XZ) {
+        if (a.rows % a.sz) return set_err(TDS_ERR_UNSUPPORTED, "xz transport: sz must divide n");
+        if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_XZ>(a, s);
+        if (tl == 8) return launch_transport_tma_t<16, 8, GEOM_XZ>(a, s);
+    } else {
+        if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_LINES>(a, s);
+        if (tl == 8) return launch_transport_tma_t<16, 8, GEOM_LINES>(a, s);
+    }
     return set_err(TDS_ERR_UNSUPPORTED, "fused transport: shape not TMA-tileable");
 }
 
@@ -561,8 +623,9 @@ namespace tds {
 
 int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const double* ui,
                                 const double* uj, double* out, double nu, int accumulate,
-                                long long lines, int sz, cudaStream_t s) {
+                                long long lines, int sz, cudaStream_t s, int geom) {
     TransportArgs a;
+    a.geom = geom;
     a.ui = ui;
     a.uj = uj;
     a.out = out;
@@ -586,9 +649,11 @@ int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const do
     a.nb1 = d1->band_n;
     a.nb2 = d2 ? d2->band_n : d1->band_n;
     if (d1->M == 16) {
-        if (accumulate) return set_err(TDS_ERR_UNSUPPORTED, "fused transport never accumulates");
+        if (accumulate != (geom == GEOM_XZ))
+            return set_err(TDS_ERR_UNSUPPORTED, "fused transport: lines layout writes, xz adds");
         return launch_transport_tma(a, s);
     }
+    if (geom != GEOM_LINES) return set_err(TDS_ERR_UNSUPPORTED, "xz transport needs 16-row chunks");
     return launch_transport(a, s);
 }
 

@@ -196,7 +196,8 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     for i in range(3):
         _contribution_into(i, "x", fields, acc[i], False, rank_count)
     scratch = torch.empty_like(acc[0])
-    for dj in ("y", "z"):
+    z_direct = rank_count == 1 and _z_plans(fields) is not None
+    for dj in (("y",) if z_direct else ("y", "z")):
         lay_j = LayoutDescriptor(n, n, n, sz, dj)
         _TRUSTED.on = True
         try:
@@ -208,7 +209,36 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
         for i in range(3):
             _contribution_into(i, dj, rot, scratch, False, rank_count)
             _reorder_tensor(scratch, n, sz, dj, "x", out=acc[i], accumulate=True)
+    if z_direct:
+        p1, p2 = _z_plans(fields)
+        w = fields.component(2).data
+        for i in range(3):
+            N.check(N.lib().tds_transport_contribution_z(
+                p1.handle, None if p2 is None else p2.handle, _vp(fields.component(i).data),
+                _vp(w), _vp(acc[i]), float(fields.nu), n, sz, _stream_handle()))
     return tuple(GroupedField(lay, a) for a in acc)
+
+
+def _z_plans(fields):
+    """16-row-chunk plans for the in-place z contributions (k_transport_tma,
+    GEOM_XZ), or None when the box / layout does not allow them."""
+    import os
+    lay = fields.layout
+    n, sz = lay.nx, lay.sz
+    if lay.pad or n % sz or sz % 8 or n % 16 or os.environ.get("TDS_TRANSPORT_Z") == "0":
+        return None
+    part = SubdomainPartition((n,))
+    s1, st1 = _operator(1, fields.h, n)
+    p1 = get_plan(s1, st1, part, chunk_rows=16)
+    if p1.info.chunk_rows != 16 or p1.info.uniform != 1:
+        return None
+    p2 = None
+    if fields.nu != 0.0:
+        s2, st2 = _operator(2, fields.h, n)
+        p2 = get_plan(s2, st2, part, chunk_rows=16)
+        if p2.info.chunk_rows != 16 or p2.info.uniform != 1:
+            return None
+    return p1, p2
 
 
 def _local_contribution(comp, advect, out, n, h, nu, accumulate):

@@ -118,3 +118,24 @@ def test_slab_transport_single_rank(nu):
         got = T.unpack(T.GroupedField(tr.lay["x"], rhs[i])).cpu().numpy()
         assert _rel(got, want[i]) <= TOL
         assert torch.equal(rhs[i], ev[i].data)
+
+
+@pytest.mark.parametrize("n,sz,nu", [(64, 32, 0.05), (64, 8, 0.0), (128, 16, 0.02)])
+def test_z_in_place_bitwise_equals_reorder_pipeline(monkeypatch, n, sz, nu):
+    """z contributions read in place from the x layout and added into the
+    accumulators (tds_transport_contribution_z) give the same bits as the
+    reference-shaped reorder -> contribution -> reorder/accumulate pipeline."""
+    rng = np.random.default_rng(n + sz)
+    u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
+    f = T.VelocityField.from_arrays(u3, v3, w3, nu, 2 * np.pi / n, sz=sz)
+    from paper_2411_13532_b200 import momentum
+    assert momentum._z_plans(f) is not None
+    direct = T.evaluate_transport_rhs(f)
+    monkeypatch.setenv("TDS_TRANSPORT_Z", "0")
+    assert momentum._z_plans(f) is None
+    staged = T.evaluate_transport_rhs(f)
+    for a, b in zip(direct, staged):
+        assert torch.equal(a.data, b.data)
+    want = O.transport_rhs(u3, v3, w3, nu, 2 * np.pi / n, sz)
+    for i in range(3):
+        assert _rel(T.unpack(direct[i]).cpu().numpy(), want[i]) <= TOL
