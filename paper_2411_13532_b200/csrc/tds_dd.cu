@@ -215,10 +215,12 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         }
 #pragma unroll
         for (int i = 0; i < M + 4; ++i) {
+            // only the 2 + 2 outer window rows can leave the block (first /
+            // last chunk): the interior rows are plain tile reads
             const int row = r0 - 2 + i;
             double x;
-            if (row < 0) x = (i == 0) ? h0 : h1;
-            else if (row >= rows) x = (row == rows) ? h2 : h3;
+            if (i < 2) x = first_chunk ? (i == 0 ? h0 : h1) : tl_tile[row * TLT + lane];
+            else if (i >= M + 2) x = last_chunk ? (i == M + 2 ? h2 : h3) : tl_tile[row * TLT + lane];
             else x = tl_tile[row * TLT + lane];
             v[i] = x;
         }
@@ -478,10 +480,12 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         }
 #pragma unroll
         for (int i = 0; i < M + 4; ++i) {
+            // only the 2 + 2 outer window rows can leave the block (first /
+            // last chunk): the interior rows are plain tile reads
             const int row = r0 - 2 + i;
             double x;
-            if (row < 0) x = (i == 0) ? h0 : h1;
-            else if (row >= rows) x = (row == rows) ? h2 : h3;
+            if (i < 2) x = first_chunk ? (i == 0 ? h0 : h1) : tl_tile[row * TLT + lane];
+            else if (i >= M + 2) x = last_chunk ? (i == M + 2 ? h2 : h3) : tl_tile[row * TLT + lane];
             else x = tl_tile[row * TLT + lane];
             v[i] = x;
         }
