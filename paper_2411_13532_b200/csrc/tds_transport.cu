@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "tds_device.cuh"
 #include "tds_tma.h"
@@ -554,31 +555,42 @@ __device__ __forceinline__ long long fidx(int i, int j, int k, int nx, int ny, i
 
 // (nx, ny, nz) field in `src_dir` layout -> `dst_dir` layout (dst = or +=).
 // The fastest field axis is j for x layouts and i for y / z layouts, so a
-// 32 x 32 (i, j) tile at fixed k serves every pair of directions.
-__global__ void k_reorder(const double* __restrict__ src, double* __restrict__ dst, int nx,
-                          int ny, int nz, int sz, int lsz, int src_dir, int dst_dir,
-                          int accumulate) {
-    __shared__ double tile[32][33];                   // [jj][ii]
-    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32, k = blockIdx.z;
+// 32 x 32 (i, j) tile at fixed k serves every pair of directions. KB
+// k-slices per block keep KB tiles of loads in flight per thread.
+template <int KB>
+__global__ void __launch_bounds__(256) k_reorder(const double* __restrict__ src,
+                                                 double* __restrict__ dst, int nx, int ny,
+                                                 int nz, int sz, int lsz, int src_dir,
+                                                 int dst_dir, int accumulate) {
+    __shared__ double tile[KB][32][33];               // [kk][jj][ii]
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32, k0 = blockIdx.z * KB;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const bool src_fast_i = src_dir != 0, dst_fast_i = dst_dir != 0;
 #pragma unroll
-    for (int r = ty; r < 32; r += 8) {
-        const int ii = src_fast_i ? tx : r, jj = src_fast_i ? r : tx;
-        const int i = i0 + ii, j = j0 + jj;
-        if (i < nx && j < ny)
-            tile[jj][ii] = __ldcs(src + fidx(i, j, k, nx, ny, nz, sz, lsz, src_dir));
+    for (int kk = 0; kk < KB; ++kk) {
+        const int k = k0 + kk;
+#pragma unroll
+        for (int r = ty; r < 32; r += 8) {
+            const int ii = src_fast_i ? tx : r, jj = src_fast_i ? r : tx;
+            const int i = i0 + ii, j = j0 + jj;
+            if (i < nx && j < ny && k < nz)
+                tile[kk][jj][ii] = __ldcs(src + fidx(i, j, k, nx, ny, nz, sz, lsz, src_dir));
+        }
     }
     __syncthreads();
 #pragma unroll
-    for (int r = ty; r < 32; r += 8) {
-        const int ii = dst_fast_i ? tx : r, jj = dst_fast_i ? r : tx;
-        const int i = i0 + ii, j = j0 + jj;
-        if (i < nx && j < ny) {
-            double* o = dst + fidx(i, j, k, nx, ny, nz, sz, lsz, dst_dir);
-            const double v = tile[jj][ii];
-            if (accumulate) *o = *o + v;
-            else __stcs(o, v);
+    for (int kk = 0; kk < KB; ++kk) {
+        const int k = k0 + kk;
+#pragma unroll
+        for (int r = ty; r < 32; r += 8) {
+            const int ii = dst_fast_i ? tx : r, jj = dst_fast_i ? r : tx;
+            const int i = i0 + ii, j = j0 + jj;
+            if (i < nx && j < ny && k < nz) {
+                double* o = dst + fidx(i, j, k, nx, ny, nz, sz, lsz, dst_dir);
+                const double v = tile[kk][jj][ii];
+                if (accumulate) *o = *o + v;
+                else __stcs(o, v);
+            }
         }
     }
 }
@@ -590,9 +602,19 @@ int launch_reorder(const double* src, double* dst, int nx, int ny, int nz, int s
         lsz = 0;
         while ((1 << lsz) < sz) ++lsz;
     }
-    dim3 grid((nx + 31) / 32, (ny + 31) / 32, nz);
-    k_reorder<<<grid, dim3(32, 8), 0, s>>>(src, dst, nx, ny, nz, sz, lsz, src_dir, dst_dir,
-                                           accumulate);
+    int kb = 1;   // measured: 2 / 4 k-slices per block are no faster
+    if (const char* e = getenv("TDS_REORDER_KB")) kb = atoi(e);
+    const dim3 blk(32, 8);
+    if (kb == 4) {
+        k_reorder<4><<<dim3((nx + 31) / 32, (ny + 31) / 32, (nz + 3) / 4), blk, 0, s>>>(
+            src, dst, nx, ny, nz, sz, lsz, src_dir, dst_dir, accumulate);
+    } else if (kb == 2) {
+        k_reorder<2><<<dim3((nx + 31) / 32, (ny + 31) / 32, (nz + 1) / 2), blk, 0, s>>>(
+            src, dst, nx, ny, nz, sz, lsz, src_dir, dst_dir, accumulate);
+    } else {
+        k_reorder<1><<<dim3((nx + 31) / 32, (ny + 31) / 32, nz), blk, 0, s>>>(
+            src, dst, nx, ny, nz, sz, lsz, src_dir, dst_dir, accumulate);
+    }
     return cuda_check(cudaGetLastError(), "k_reorder launch");
 }
 

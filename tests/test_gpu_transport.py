@@ -139,3 +139,23 @@ def test_z_in_place_bitwise_equals_reorder_pipeline(monkeypatch, n, sz, nu):
     want = O.transport_rhs(u3, v3, w3, nu, 2 * np.pi / n, sz)
     for i in range(3):
         assert _rel(T.unpack(direct[i]).cpu().numpy(), want[i]) <= TOL
+
+
+@pytest.mark.parametrize("n,sz,groups", [(1024, 8, 3), (1024, 16, 2), (512, 32, 2), (256, 8, 4)])
+def test_fused_contribution_kernel_sizes_vs_oracle(n, sz, groups):
+    """The fused contribution kernel (16-row chunks, 8/16-line tiles, up to
+    64 chunks at n = 1024) on a few groups of lines vs three oracle solves."""
+    from paper_2411_13532_b200 import momentum
+    rng = np.random.default_rng(n + sz)
+    ui = torch.from_numpy(rng.standard_normal((groups, n, sz))).cuda()
+    uj = torch.from_numpy(rng.standard_normal((groups, n, sz))).cuda()
+    out = torch.empty_like(ui)
+    h, nu = 2 * np.pi / n, 0.03
+    assert momentum._fused_contribution(ui, uj, out, n, h, nu, False)
+    lo, di, up, st = O.assemble("d1", n, h, True)
+    lo2, di2, up2, st2 = O.assemble("d2", n, h, True)
+    a, b = ui.cpu().numpy(), uj.cpu().numpy()
+    ref = (-0.5 * (b * O.run_distd2(lo, di, up, True, a, st)
+                   + O.run_distd2(lo, di, up, True, b * a, st))
+           + nu * O.run_distd2(lo2, di2, up2, True, a, st2))
+    assert _rel(out.cpu().numpy(), ref) <= TOL

@@ -42,6 +42,13 @@ def main():
         f = T.pack(cart, lay)
         res[f"pack_{d}"] = gb / (timed(lambda: T.pack(cart, lay)) * 1e-3)
         res[f"unpack_{d}"] = gb / (timed(lambda: T.unpack(f)) * 1e-3)
+    from paper_2411_13532_b200 import momentum
+    fx = T.pack(cart, T.LayoutDescriptor(n, n, n, sz, "x")).data
+    fy = torch.empty_like(fx)
+    for a, b in (("x", "y"), ("x", "z"), ("y", "x"), ("z", "x")):
+        res[f"reorder_{a}{b}"] = gb / (timed(lambda: momentum._reorder_tensor(fx, n, sz, a, b, out=fy)) * 1e-3)
+        res[f"reorder_acc_{a}{b}"] = 1.5 * gb / (timed(
+            lambda: momentum._reorder_tensor(fx, n, sz, a, b, out=fy, accumulate=True)) * 1e-3)
     copy = torch.empty_like(cart)
     res["torch_copy"] = gb / (timed(lambda: copy.copy_(cart)) * 1e-3)
     print(json.dumps({k: round(v, 1) for k, v in res.items()}))
