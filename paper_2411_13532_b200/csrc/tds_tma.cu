@@ -204,13 +204,16 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
 template <int M, int MODE, int UNI>
 int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(a);
-    // 32-line tiles (one chunk per warp: no divergence between a special edge
-    // chunk and a uniform one; 256-byte row segments) when a tile's chunks fit
-    // 512 threads and sz allows. Measured at 512^3: 6041 vs 5811 GB/s periodic,
-    // 5051 vs 4752 open. A/B knob TDS_TMA_TL32=0.
-    if (MODE == MODE_SOLVE && a.sz % 32 == 0 && a.chunks * 32 <= 512 &&
-        (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 <= 200 * 1024 &&
-        !(getenv("TDS_TMA_TL32") && getenv("TDS_TMA_TL32")[0] == '0'))
+    // 32-line tiles: one chunk per warp, so a special edge chunk (TAB_EDGES)
+    // or a per-row table chunk (TAB_GLOBAL) never diverges from its warp
+    // neighbour; 1 CTA of 512 threads per SM. Uniform plans keep 16-line
+    // tiles (2 CTAs/SM): at 512^3 under the sustained-load power cap (~1700
+    // MHz) 16-line tiles measured 5827 vs 5750 GB/s, at full clock 32-line
+    // tiles 5977 vs 5631. A/B knob TDS_TMA_TL32 = 0 (never) / 1 (always).
+    const char* e32 = getenv("TDS_TMA_TL32");
+    const bool want32 = e32 ? e32[0] == '1' : UNI != TAB_UNIFORM;
+    if (want32 && MODE == MODE_SOLVE && a.sz % 32 == 0 && a.chunks * 32 <= 512 &&
+        (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 <= 200 * 1024)
         return launch_tma_t<M, MODE, UNI, 32>(a, TileCfg{32, 1}, s);
     if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
     return launch_tma_t<M, MODE, UNI, 16>(a, cfg, s);
