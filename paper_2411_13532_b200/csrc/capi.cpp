@@ -388,10 +388,11 @@ extern "C" int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2
                                             accumulate, groups * sz, sz, S(stream), 0);
 }
 
-extern "C" int tds_transport_contribution_z(const tds_plan* d1, const tds_plan* d2,
-                                            const double* u_i, const double* u_j, double* acc,
-                                            double nu, int n, int sz, void* stream) {
+extern "C" int tds_transport_contribution_in_x(const tds_plan* d1, const tds_plan* d2,
+                                               const double* u_i, const double* u_j, double* acc,
+                                               double nu, int n, int sz, int dir, void* stream) {
     if (!d1 || !u_i || !u_j || !acc) return set_err(TDS_ERR_INVALID, "null argument");
+    if (dir != 1 && dir != 2) return set_err(TDS_ERR_INVALID, "dir must be 1 (y) or 2 (z)");
     const bool ok1 = d1->path == TDS_PATH_FAST && d1->uniform && d1->M == 16 && d1->P == 1 &&
                      d1->rank < 0 && !d1->special_first && !d1->special_last &&
                      d1->block_rows == n;
@@ -400,9 +401,9 @@ extern "C" int tds_transport_contribution_z(const tds_plan* d1, const tds_plan* 
                              !d2->special_first && !d2->special_last);
     if (!ok1 || !ok2 || (nu != 0.0 && !d2) || sz < 1 || n % sz)
         return set_err(TDS_ERR_UNSUPPORTED,
-                       "z transport needs uniform P=1 plans with 16-row chunks and sz | n");
+                       "in-place transport needs uniform P=1 plans with 16-row chunks and sz | n");
     return tds::transport_launch_from_plans(d1, nu != 0.0 ? d2 : nullptr, u_i, u_j, acc, nu, 1,
-                                            (long long)n * n, sz, S(stream), 1);
+                                            (long long)n * n, sz, S(stream), dir == 2 ? 1 : 2);
 }
 
 extern "C" int tds_reorder3(const double* src, double* dst, int nx, int ny, int nz, int sz,

@@ -42,15 +42,19 @@ struct TransportArgs {
     const int* bq1;
     const int* bq2;
     int nb1, nb2;
-    int geom;              // GEOM_LINES, or GEOM_XZ: z lines of an x-layout n^3 box
+    int geom;              // GEOM_LINES, GEOM_XZ / GEOM_XY: z / y lines of an x-layout box
 };
 
 // Tile geometry of k_transport_tma: GEOM_LINES reads / writes the field in
 // its own (groups, rows, sz) layout; GEOM_XZ reads the z lines of a cubic
 // x-layout box in place (4-D tensor map: lanes, x, y-group, z) and ADDS the
 // contribution into an x-layout accumulator -- the z direction of the
-// transport RHS without re-layout passes.
-enum { GEOM_LINES = 0, GEOM_XZ = 1 };
+// transport RHS without re-layout passes. GEOM_XY does the same for the y
+// lines (sz = 32): a tile is 16 y lines (consecutive x at one z), loaded as
+// two 16-lane halves with the 128-byte TMA swizzle so that the 16 lines of
+// a warp read distinct banks; the window is read 16 bytes (two rows) at a
+// time.
+enum { GEOM_LINES = 0, GEOM_XZ = 1, GEOM_XY = 2 };
 
 namespace {
 
@@ -317,6 +321,20 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         for (int j = 0; j < tpc; ++j) {
             const long long first = (item * tpc + j) * TLT;
             if (first >= p.lines) break;
+            if (GEOM == GEOM_XY) {
+                // tile = x-block + (n/TLT) * z; halves of 16 lanes, all y-groups
+                const long long tile = first / TLT;
+                const int nxb = rows / TLT;
+                const int x0 = (int)(tile % nxb) * TLT, z = (int)(tile / nxb);
+                const size_t half = tile_elems / 2;
+                for (int h = 0; h < 2; ++h) {
+                    tma_load_4d(ti + j * tile_elems + h * half, &A.map_i, bar, h * 16, x0, 0, z);
+                    if (!diag)
+                        tma_load_4d(tj + j * tile_elems + h * half, &A.map_j, bar, h * 16, x0, 0,
+                                    z);
+                }
+                continue;
+            }
             if (GEOM == GEOM_XZ) {
                 // line = lane-block + sz * (y-group + (n/sz) * x): z line (x, y)
                 const long long tile = first / TLT;
@@ -356,10 +374,25 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
     const double* Tj = (diag ? ti : tj) + tl * tile_elems;
     // stencil window of row r0 - 2 + i: rows r0 .. r0+M-1 at immediate
     // offsets from `base`, the 2 + 2 periodic halo rows at wrapped offsets
-    const int base = r0 * TLT + lane;
-    const int lo = (chunk == 0 ? rows - 2 : r0 - 2) * TLT + lane;
-    const int hi = (chunk == C - 1 ? 0 : r0 + M) * TLT + lane;
+    // GEOM_XY: row y of line `lane` in the swizzled [half][y-group][line][16]
+    // tile: 16-byte unit (y & 15) / 2 of the 128-byte row (group, line) sits at
+    // unit ^ (line & 7)
+    const int xy_half = rows * TLT / 2;
+    auto xy_off = [&](int y) {
+        return ((y >> 4) & 1) * xy_half + (((y >> 5) * TLT + lane) << 4) +
+               ((((y & 15) >> 1) ^ (lane & 7)) << 1) + (y & 1);
+    };
+    const int base = GEOM == GEOM_XY ? xy_off(r0) - ((lane & 7) << 1) : r0 * TLT + lane;
+    const int lo = GEOM == GEOM_XY ? 0 : (chunk == 0 ? rows - 2 : r0 - 2) * TLT + lane;
+    const int hi = GEOM == GEOM_XY ? 0 : (chunk == C - 1 ? 0 : r0 + M) * TLT + lane;
+    const int ylo = chunk == 0 ? rows - 2 : r0 - 2, yhi = chunk == C - 1 ? 0 : r0 + M;
     auto wrap = [&](int i) {
+        if (GEOM == GEOM_XY) {
+            if (i < 2) return xy_off(ylo + i);
+            if (i >= M + 2) return xy_off(yhi + i - M - 2);
+            const int l = i - 2;   // row r0 + l, r0 % 16 == 0
+            return base + ((((l >> 1) ^ (lane & 7))) << 1) + (l & 1);
+        }
         return i < 2 ? lo + i * TLT : (i >= M + 2 ? hi + (i - M - 2) * TLT : base + (i - 2) * TLT);
     };
     double* Y0 = sY + (size_t)tl * K * TLT;
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         __syncthreads();
         band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, Y, K, lane, F, L);
 #pragma unroll
-        for (int i = 0; i < M; ++i) acc[i] = Tj[base + i * TLT] * subst(T1, i, M, F, L, d[i]);
+        for (int i = 0; i < M; ++i) acc[i] = Tj[wrap(i + 2)] * subst(T1, i, M, F, L, d[i]);
 
         // (B) d(u_j u_i)/dx_j -> acc = -1/2 (acc + dprod)
         sweeps_src<M>(T1, [&](int i) { const int o = wrap(i); return Tj[o] * Ti[o]; }, d);
@@ -416,7 +449,21 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < M; ++i) acc[i] = fma(p.nu, subst(T2, i, M, F, L, d[i]), acc[i]);
         }
-        if (valid && GEOM == GEOM_XZ) {
+        if (valid && GEOM == GEOM_XY) {
+            // x-layout address of (x, y, z): ((y/sz + z n/sz) n + x) sz + y % sz
+            const long long tile = line / TLT;
+            const int nxb = rows / TLT;
+            const long long x = (tile % nxb) * TLT + lane, z = tile / nxb;
+            double2* ob = reinterpret_cast<double2*>(
+                p.out + (((long long)(r0 >> 5) + z * (rows / p.sz)) * rows + x) * sz + (r0 & 31));
+#pragma unroll
+            for (int i = 0; i < M / 2; ++i) {
+                double2 o = ob[i];
+                o.x += acc[2 * i];
+                o.y += acc[2 * i + 1];
+                ob[i] = o;
+            }
+        } else if (valid && GEOM == GEOM_XZ) {
             // x-layout address of (x, y, z): ((y-group + z n/sz) n + x) sz + lane
             const long long tile = line / TLT;
             const int nlb = p.sz / TLT, ngj = rows / p.sz;
@@ -453,6 +500,22 @@ int encode_xz_map(const double* u, int n, int sz, int M, int tl, CUtensorMap* ma
     return TDS_OK;
 }
 
+// The same 4-D view, box 16 lanes x TLT x-positions x all y-groups x 1 z,
+// 128-byte swizzle (GEOM_XY tiles).
+int encode_xy_map(const double* u, int n, int sz, int tl, CUtensorMap* map) {
+    cuuint64_t dims[4] = {(cuuint64_t)sz, (cuuint64_t)n, (cuuint64_t)(n / sz), (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)sz * 8, (cuuint64_t)n * sz * 8,
+                             (cuuint64_t)n * (cuuint64_t)n * 8};
+    cuuint32_t box[4] = {16, (cuuint32_t)tl, (cuuint32_t)(n / sz), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(u),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_err(TDS_ERR_CUDA, "cuTensorMapEncodeTiled (xy) failed");
+    return TDS_OK;
+}
+
 template <int M, int TLT, int GEOM>
 int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     TransportTmaArgs A;
@@ -469,7 +532,11 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     fi.sz = fj.sz = a.sz;
     fi.lines = fj.lines = a.lines;
     int rc;
-    if (GEOM == GEOM_XZ) {
+    if (GEOM == GEOM_XY) {
+        if ((rc = encode_xy_map(a.ui, a.rows, a.sz, TLT, &A.map_i))) return rc;
+        if ((rc = encode_xy_map(a.uj, a.rows, a.sz, TLT, &A.map_j))) return rc;
+        A.boxr = a.rows;
+    } else if (GEOM == GEOM_XZ) {
         if ((rc = encode_xz_map(a.ui, a.rows, a.sz, M, TLT, &A.map_i, &A.boxr))) return rc;
         if ((rc = encode_xz_map(a.uj, a.rows, a.sz, M, TLT, &A.map_j, &A.boxr))) return rc;
     } else {
@@ -528,6 +595,11 @@ static int transport_tma_tl(const TransportArgs& a) {
 
 int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
     const int tl = transport_tma_tl(a);
+    if (a.geom == GEOM_XY) {
+        if (a.sz != 32 || a.rows % 32 || tl != 16)
+            return set_err(TDS_ERR_UNSUPPORTED, "xy transport: sz = 32, 32 | n, 16-line tiles");
+        return launch_transport_tma_t<16, 16, GEOM_XY>(a, s);
+    }
     if (a.geom == GEOM_XZ) {
         if (a.rows % a.sz) return set_err(TDS_ERR_UNSUPPORTED, "xz transport: sz must divide n");
         if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_XZ>(a, s);
@@ -671,7 +743,7 @@ int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const do
     a.nb1 = d1->band_n;
     a.nb2 = d2 ? d2->band_n : d1->band_n;
     if (d1->M == 16) {
-        if (accumulate != (geom == GEOM_XZ))
+        if (accumulate != (geom != GEOM_LINES))
             return set_err(TDS_ERR_UNSUPPORTED, "fused transport: lines layout writes, xz adds");
         return launch_transport_tma(a, s);
     }

@@ -196,8 +196,19 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     for i in range(3):
         _contribution_into(i, "x", fields, acc[i], False, rank_count)
     scratch = torch.empty_like(acc[0])
-    z_direct = rank_count == 1 and _z_plans(fields) is not None
-    for dj in (("y",) if z_direct else ("y", "z")):
+    # y / z contributions read in place from the x layout and added into the
+    # accumulators (k_transport_tma GEOM_XY / GEOM_XZ) when the box allows
+    in_place = {dj: rank_count == 1 and _in_x_plans(fields, dj) is not None for dj in ("y", "z")}
+    for dj in ("y", "z"):
+        if in_place[dj]:
+            p1, p2 = _in_x_plans(fields, dj)
+            adv = fields.component(_DIRECTIONS.index(dj)).data
+            for i in range(3):
+                N.check(N.lib().tds_transport_contribution_in_x(
+                    p1.handle, None if p2 is None else p2.handle,
+                    _vp(fields.component(i).data), _vp(adv), _vp(acc[i]), float(fields.nu), n,
+                    sz, _DIRECTIONS.index(dj), _stream_handle()))
+            continue
         lay_j = LayoutDescriptor(n, n, n, sz, dj)
         _TRUSTED.on = True
         try:
@@ -209,23 +220,21 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
         for i in range(3):
             _contribution_into(i, dj, rot, scratch, False, rank_count)
             _reorder_tensor(scratch, n, sz, dj, "x", out=acc[i], accumulate=True)
-    if z_direct:
-        p1, p2 = _z_plans(fields)
-        w = fields.component(2).data
-        for i in range(3):
-            N.check(N.lib().tds_transport_contribution_z(
-                p1.handle, None if p2 is None else p2.handle, _vp(fields.component(i).data),
-                _vp(w), _vp(acc[i]), float(fields.nu), n, sz, _stream_handle()))
     return tuple(GroupedField(lay, a) for a in acc)
 
 
-def _z_plans(fields):
-    """16-row-chunk plans for the in-place z contributions (k_transport_tma,
-    GEOM_XZ), or None when the box / layout does not allow them."""
+def _in_x_plans(fields, dj):
+    """16-row-chunk plans for the in-place y / z contributions
+    (k_transport_tma GEOM_XY / GEOM_XZ), or None when the box / layout does
+    not allow them. A/B knobs: TDS_TRANSPORT_Y=0, TDS_TRANSPORT_Z=0."""
     import os
     lay = fields.layout
     n, sz = lay.nx, lay.sz
-    if lay.pad or n % sz or sz % 8 or n % 16 or os.environ.get("TDS_TRANSPORT_Z") == "0":
+    if lay.pad or n % sz or sz % 8 or n % 16:
+        return None
+    if os.environ.get("TDS_TRANSPORT_" + dj.upper()) == "0":
+        return None
+    if dj == "y" and (sz != 32 or n % 32):
         return None
     part = SubdomainPartition((n,))
     s1, st1 = _operator(1, fields.h, n)

@@ -120,19 +120,23 @@ def test_slab_transport_single_rank(nu):
         assert torch.equal(rhs[i], ev[i].data)
 
 
-@pytest.mark.parametrize("n,sz,nu", [(64, 32, 0.05), (64, 8, 0.0), (128, 16, 0.02)])
-def test_z_in_place_bitwise_equals_reorder_pipeline(monkeypatch, n, sz, nu):
-    """z contributions read in place from the x layout and added into the
-    accumulators (tds_transport_contribution_z) give the same bits as the
-    reference-shaped reorder -> contribution -> reorder/accumulate pipeline."""
+@pytest.mark.parametrize("n,sz,nu", [(64, 32, 0.05), (64, 8, 0.0), (128, 16, 0.02),
+                                     (128, 32, 0.0), (96, 32, 0.01)])
+def test_in_place_y_z_bitwise_equals_reorder_pipeline(monkeypatch, n, sz, nu):
+    """y / z contributions read in place from the x layout and added into the
+    accumulators (tds_transport_contribution_in_x; y needs sz = 32) give the
+    same bits as the reference-shaped reorder -> contribution ->
+    reorder/accumulate pipeline, and match the oracle."""
     rng = np.random.default_rng(n + sz)
     u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
     f = T.VelocityField.from_arrays(u3, v3, w3, nu, 2 * np.pi / n, sz=sz)
     from paper_2411_13532_b200 import momentum
-    assert momentum._z_plans(f) is not None
+    assert momentum._in_x_plans(f, "z") is not None
+    assert (momentum._in_x_plans(f, "y") is not None) == (sz == 32 and n % 32 == 0)
     direct = T.evaluate_transport_rhs(f)
+    monkeypatch.setenv("TDS_TRANSPORT_Y", "0")
     monkeypatch.setenv("TDS_TRANSPORT_Z", "0")
-    assert momentum._z_plans(f) is None
+    assert momentum._in_x_plans(f, "z") is None and momentum._in_x_plans(f, "y") is None
     staged = T.evaluate_transport_rhs(f)
     for a, b in zip(direct, staged):
         assert torch.equal(a.data, b.data)
