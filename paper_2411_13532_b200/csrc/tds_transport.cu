@@ -386,10 +386,12 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
     const int lo = GEOM == GEOM_XY ? 0 : (chunk == 0 ? rows - 2 : r0 - 2) * TLT + lane;
     const int hi = GEOM == GEOM_XY ? 0 : (chunk == C - 1 ? 0 : r0 + M) * TLT + lane;
     const int ylo = chunk == 0 ? rows - 2 : r0 - 2, yhi = chunk == C - 1 ? 0 : r0 + M;
+    const int xh0 = GEOM == GEOM_XY ? xy_off(ylo) : 0, xh1 = GEOM == GEOM_XY ? xy_off(ylo + 1) : 0;
+    const int xh2 = GEOM == GEOM_XY ? xy_off(yhi) : 0, xh3 = GEOM == GEOM_XY ? xy_off(yhi + 1) : 0;
     auto wrap = [&](int i) {
         if (GEOM == GEOM_XY) {
-            if (i < 2) return xy_off(ylo + i);
-            if (i >= M + 2) return xy_off(yhi + i - M - 2);
+            if (i < 2) return i == 0 ? xh0 : xh1;
+            if (i >= M + 2) return i == M + 2 ? xh2 : xh3;
             const int l = i - 2;   // row r0 + l, r0 % 16 == 0
             return base + ((((l >> 1) ^ (lane & 7))) << 1) + (l & 1);
         }
