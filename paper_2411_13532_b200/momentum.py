@@ -198,17 +198,23 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     scratch = torch.empty_like(acc[0])
     # y / z contributions read in place from the x layout and added into the
     # accumulators (k_transport_tma GEOM_XY / GEOM_XZ) when the box allows
-    in_place = {dj: rank_count == 1 and _in_x_plans(fields, dj) is not None for dj in ("y", "z")}
     for dj in ("y", "z"):
-        if in_place[dj]:
-            p1, p2 = _in_x_plans(fields, dj)
+        plans = _in_x_plans(fields, dj) if rank_count == 1 else None
+        if plans is not None:
+            p1, p2 = plans
             adv = fields.component(_DIRECTIONS.index(dj)).data
+            done = 0
             for i in range(3):
-                N.check(N.lib().tds_transport_contribution_in_x(
+                rc = N.lib().tds_transport_contribution_in_x(
                     p1.handle, None if p2 is None else p2.handle,
                     _vp(fields.component(i).data), _vp(adv), _vp(acc[i]), float(fields.nu), n,
-                    sz, _DIRECTIONS.index(dj), _stream_handle()))
-            continue
+                    sz, _DIRECTIONS.index(dj), _stream_handle())
+                if rc == N.TDS_ERR_UNSUPPORTED and i == 0:
+                    break                     # shape not tileable: reorder path below
+                N.check(rc)
+                done += 1
+            if done == 3:
+                continue
         lay_j = LayoutDescriptor(n, n, n, sz, dj)
         _TRUSTED.on = True
         try:
