@@ -106,7 +106,7 @@ __device__ __forceinline__ double take(double* slot, const DDArgs& A, unsigned l
 
 }  // namespace
 
-template <int M, int TAB, int TLT>
+template <int M, int TAB, int TLT, int SZC>
 __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     constexpr bool UNIFORM = TAB != TAB_GLOBAL;
     const FastArgs& p = A.t.f;
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     const int lane = t % TLT;
     const int chunk = (t / TLT) % C;
     const int tl = t / (TLT * C);
-    const long long sz = p.sz;
+    const long long sz = SZC ? SZC : p.sz;
     const int r0 = chunk * M;
     const Mail mb{p.lines};
     const long long par = mb.half(A.epoch);
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
     auto publish_halo = [&](long long item) {
         const long long ln = (item * tpc + tl) * TLT + lane;
         if (ln >= p.lines) return;
-        const double* ub = p.u + line_base(ln, rows, p.sz);
-        const long long hb = halo_base(ln, p.sz);
+        const double* ub = p.u + line_base_t<SZC>(ln, rows, p.sz);
+        const long long hb = halo_base_t<SZC>(ln, p.sz);
         if (first_chunk && A.mail_prev) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         const long long nxt = item + gridDim.x;
         if (nxt < p.items) publish_halo(nxt);          // one item ahead
         // halo slots of this item: loads in flight across the TMA wait
-        const long long hb = valid ? halo_base(line, p.sz) : 0;
+        const long long hb = valid ? halo_base_t<SZC>(line, p.sz) : 0;
         double* hlo = (valid && first_chunk && A.mail_prev) ? A.mail + par + mb.h_lo() + hb : nullptr;
         double* hhi = (valid && last_chunk && A.mail_next) ? A.mail + par + mb.h_hi() + hb : nullptr;
         unsigned long long a0 = SENTINEL, a1 = SENTINEL, b0 = SENTINEL, b1 = SENTINEL;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             L = fma(h0.y, us, fma(hl.y, ue, L));
         }
         if (valid)
-            chunk_store_any<M, TAB>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F, L,
+            chunk_store_any<M, TAB>(p, tb, p.out + line_base_t<SZC>(line, rows, p.sz), sz, r0, d, F, L,
                                         A.t.store_cs != 0, chunk);
     }
 }
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
 // their chunks (F', L', d rows, g.Y) in shared memory, and finish item t-1
 // -- whose neighbour values arrived an iteration ago -- so the NVLink round
 // trip is off the critical path.
-template <int M, int TAB, int TLT>
+template <int M, int TAB, int TLT, int SZC>
 __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     constexpr bool UNIFORM = TAB != TAB_GLOBAL;
     const FastArgs& p = A.t.f;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     const bool helpers = C * TLT / 32 >= 4;
     const bool halo_lo_poster = helpers ? (wt == 2 && role == 0) : first_chunk;
     const bool halo_hi_poster = helpers ? (wt == 2 && role == 1) : last_chunk;
-    const long long sz = p.sz;
+    const long long sz = SZC ? SZC : p.sz;
     const int r0 = chunk * M;
     const Mail mb{p.lines};
     const long long par = mb.half(A.epoch);
@@ -356,8 +356,8 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         if (!halo_lo_poster && !halo_hi_poster) return;
         const long long ln = (item * tpc + tl) * TLT + lane;
         if (ln >= p.lines) return;
-        const double* ub = p.u + line_base(ln, rows, p.sz);
-        const long long hb = halo_base(ln, p.sz);
+        const double* ub = p.u + line_base_t<SZC>(ln, rows, p.sz);
+        const long long hb = halo_base_t<SZC>(ln, p.sz);
         if (halo_lo_poster && A.mail_prev) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             L = fma(hl.y, ue, L);
         }
         if (!fv) return;
-        double* ob = p.out + line_base(fl, rows, p.sz);
+        double* ob = p.out + line_base_t<SZC>(fl, rows, p.sz);
         if (TAB == TAB_EDGES && p.special_first && first_chunk) {
             edge_finish(p.e_first, ob, F, L);
             return;
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         const bool valid = line < p.lines;
         const long long nxt = item + gridDim.x;
         if (nxt < p.items) publish_halo(nxt);          // one item ahead
-        const long long hb = valid ? halo_base(line, p.sz) : 0;
+        const long long hb = valid ? halo_base_t<SZC>(line, p.sz) : 0;
         double* hlo = (valid && first_chunk && A.mail_prev) ? A.mail + par + mb.h_lo() + hb : nullptr;
         double* hhi = (valid && last_chunk && A.mail_next) ? A.mail + par + mb.h_hi() + hb : nullptr;
         unsigned long long a0 = SENTINEL, a1 = SENTINEL, b0 = SENTINEL, b1 = SENTINEL;
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                 sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
             }
             if (valid)
-                chunk_store<M, UNIFORM>(p, tb, p.out + line_base(line, rows, p.sz), sz, r0, d, F,
+                chunk_store<M, UNIFORM>(p, tb, p.out + line_base_t<SZC>(line, rows, p.sz), sz, r0, d, F,
                                         L, true);   // interior warps: never a special chunk
         } else {
             if (!helpers && valid && (first_chunk || last_chunk)) {
@@ -560,7 +560,7 @@ size_t dd_smem(const FastArgs& a, TileCfg c) {
     return tma_smem(a, c) + (size_t)c.tpc * 2 * c.tl * 8;
 }
 
-template <int M, int UNI, int TLT>
+template <int M, int UNI, int TLT, int SZC = 0>
 int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     DDArgs A = A0;
     FastArgs& a = A.t.f;
@@ -575,7 +575,7 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     const size_t smem = dd_smem(a, cfg);
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_dd<M, UNI, TLT>,
+        rc = cuda_check(cudaFuncSetAttribute(k_dd<M, UNI, TLT, SZC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem),
                         "cudaFuncSetAttribute(k_dd)");
@@ -585,13 +585,13 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     int dev = 0, sms = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd<M, UNI, TLT>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd<M, UNI, TLT, SZC>, threads, smem);
     if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
     // exactly the resident capacity: every CTA is co-resident (no waits on
     // unscheduled CTAs); identical on every rank
     long long grid = (long long)nb * sms;
     if (grid > a.items) grid = a.items;
-    k_dd<M, UNI, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_dd<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd launch");
 }
 
@@ -599,7 +599,7 @@ size_t dd2_smem(const FastArgs& a, TileCfg c, int M) {
     return tma_smem(a, c) + (size_t)c.tpc * 2 * (M + 1) * 32 * 8 + (size_t)4 * c.tpc * c.tl * 8;
 }
 
-template <int M, int UNI, int TLT>
+template <int M, int UNI, int TLT, int SZC = 0>
 int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     DDArgs A = A0;
     FastArgs& a = A.t.f;
@@ -615,7 +615,7 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     const size_t smem = dd2_smem(a, cfg, M);
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_dd2<M, UNI, TLT>,
+        rc = cuda_check(cudaFuncSetAttribute(k_dd2<M, UNI, TLT, SZC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem),
                         "cudaFuncSetAttribute(k_dd2)");
@@ -625,11 +625,11 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     int dev = 0, sms = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd2<M, UNI, TLT>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd2<M, UNI, TLT, SZC>, threads, smem);
     if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
     long long grid = (long long)nb * sms;
     if (grid > a.items) grid = a.items;
-    k_dd2<M, UNI, TLT><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_dd2<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd2 launch");
 }
 
@@ -649,6 +649,10 @@ int launch_dd_m(const DDArgs& A, cudaStream_t s) {
                        (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
     if (cfg.tl == 8)
         return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);
+    if constexpr (M == 32)
+        if (A.t.f.sz == 32)
+            return defer ? launch_dd2_t<M, UNI, 16, 32>(A, cfg, s)
+                         : launch_dd_t<M, UNI, 16, 32>(A, cfg, s);
     return defer ? launch_dd2_t<M, UNI, 16>(A, cfg, s) : launch_dd_t<M, UNI, 16>(A, cfg, s);
 }
 

@@ -85,6 +85,19 @@ __device__ __forceinline__ long long line_base(long long line, int rows, int sz)
 __device__ __forceinline__ long long halo_base(long long line, int sz) {
     return (line / sz) * 2LL * sz + (line % sz);
 }
+// compile-time lane width (SZC = 32, the benchmark layout) or runtime (0):
+// with SZC the line decomposition is shifts and every row address of a
+// line is an immediate offset from one base pointer
+template <int SZC>
+__device__ __forceinline__ long long line_base_t(long long line, int rows, int sz) {
+    if (SZC) return (line / SZC) * (long long)rows * SZC + (line % SZC);
+    return line_base(line, rows, sz);
+}
+template <int SZC>
+__device__ __forceinline__ long long halo_base_t(long long line, int sz) {
+    if (SZC) return (line / SZC) * 2LL * SZC + (line % SZC);
+    return halo_base(line, sz);
+}
 
 // Fused width-5 stencil + Alg. 6 (reference distributed.py:257-276) on one
 // chunk of M rows held in registers: v = rows r0-2 .. r0+M+1, d = decoupled.
