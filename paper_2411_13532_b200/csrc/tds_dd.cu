@@ -650,7 +650,7 @@ int launch_dd_m(const DDArgs& A, cudaStream_t s) {
     if (cfg.tl == 8)
         return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);
     if constexpr (M == 32)
-        if (A.t.f.sz == 32)
+        if (A.t.f.sz == 32 && !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0'))
             return defer ? launch_dd2_t<M, UNI, 16, 32>(A, cfg, s)
                          : launch_dd_t<M, UNI, 16, 32>(A, cfg, s);
     return defer ? launch_dd2_t<M, UNI, 16>(A, cfg, s) : launch_dd_t<M, UNI, 16>(A, cfg, s);

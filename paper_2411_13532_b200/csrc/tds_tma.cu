@@ -218,7 +218,8 @@ int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
     // the benchmark layout (sz = 32) gets a compile-time lane width
     if constexpr (M == 32 && MODE == MODE_SOLVE)
-        if (a.sz == 32) return launch_tma_t<M, MODE, UNI, 16, 32>(a, cfg, s);
+        if (a.sz == 32 && !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0'))
+            return launch_tma_t<M, MODE, UNI, 16, 32>(a, cfg, s);
     return launch_tma_t<M, MODE, UNI, 16>(a, cfg, s);
 }
 
