@@ -214,11 +214,15 @@ int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     const bool want32 = e32 ? e32[0] == '1' : UNI != TAB_UNIFORM;
     if (want32 && MODE == MODE_SOLVE && a.sz % 32 == 0 && a.chunks * 32 <= 512 &&
         (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 <= 200 * 1024)
-        return launch_tma_t<M, MODE, UNI, 32, 32>(a, TileCfg{32, 1}, s);
+        return getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '1'
+                   ? launch_tma_t<M, MODE, UNI, 32, 32>(a, TileCfg{32, 1}, s)
+                   : launch_tma_t<M, MODE, UNI, 32>(a, TileCfg{32, 1}, s);
     if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
-    // the benchmark layout (sz = 32) gets a compile-time lane width
+    // compile-time lane width (sz = 32): a win for k_dd / k_dd2 (+9% at
+    // m = 512 in loopback) but measured slower here (5516 vs 5863 GB/s at
+    // 512^3), so k_tma keeps the runtime width unless TDS_SZC_TMA=1
     if constexpr (M == 32 && MODE == MODE_SOLVE)
-        if (a.sz == 32 && !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0'))
+        if (a.sz == 32 && getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '1')
             return launch_tma_t<M, MODE, UNI, 16, 32>(a, cfg, s);
     return launch_tma_t<M, MODE, UNI, 16>(a, cfg, s);
 }
