@@ -214,13 +214,15 @@ int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     const bool want32 = e32 ? e32[0] == '1' : UNI != TAB_UNIFORM;
     if (want32 && MODE == MODE_SOLVE && a.sz % 32 == 0 && a.chunks * 32 <= 512 &&
         (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 <= 200 * 1024)
-        return getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '1'
-                   ? launch_tma_t<M, MODE, UNI, 32, 32>(a, TileCfg{32, 1}, s)
-                   : launch_tma_t<M, MODE, UNI, 32>(a, TileCfg{32, 1}, s);
+        // compile-time lane width: 5147 vs 4980 GB/s for open d/dx at 512^3
+        return getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '0'
+                   ? launch_tma_t<M, MODE, UNI, 32>(a, TileCfg{32, 1}, s)
+                   : launch_tma_t<M, MODE, UNI, 32, 32>(a, TileCfg{32, 1}, s);
     if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
     // compile-time lane width (sz = 32): a win for k_dd / k_dd2 (+9% at
-    // m = 512 in loopback) but measured slower here (5516 vs 5863 GB/s at
-    // 512^3), so k_tma keeps the runtime width unless TDS_SZC_TMA=1
+    // m = 512 in loopback) and 32-line tiles, but measured slower for 16-line
+    // uniform tiles (5516 vs 5863 GB/s at 512^3): runtime width unless
+    // TDS_SZC_TMA=1
     if constexpr (M == 32 && MODE == MODE_SOLVE)
         if (a.sz == 32 && getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '1')
             return launch_tma_t<M, MODE, UNI, 16, 32>(a, cfg, s);
