@@ -279,7 +279,7 @@ __device__ __forceinline__ double subst(const UniformTable& T, int i, int M, dou
 
 }  // namespace
 
-template <int M, int TLT, int GEOM>
+template <int M, int TLT, int GEOM, int SZC>
 __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant__ TransportTmaArgs A) {
     const TransportArgs& p = A.p;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
     const int lane = t % TLT;
     const int chunk = (t / TLT) % C;
     const int tl = t / (TLT * C);
-    const long long sz = p.sz;
+    const long long sz = SZC ? SZC : p.sz;
     const int r0 = chunk * M;
     const size_t tile_elems = (size_t)rows * TLT;
     double* ti = reinterpret_cast<double*>(smem);
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < M; ++i) ob[i * rs] = ob[i * rs] + acc[i];
         } else if (valid) {
-            double* ob = p.out + line_base(line, rows, p.sz) + (long long)r0 * sz;
+            double* ob = p.out + line_base_t<SZC>(line, rows, p.sz) + (long long)r0 * sz;
 #pragma unroll
             for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
         }
@@ -518,7 +518,7 @@ int encode_xy_map(const double* u, int n, int sz, int tl, CUtensorMap* map) {
     return TDS_OK;
 }
 
-template <int M, int TLT, int GEOM>
+template <int M, int TLT, int GEOM, int SZC = 0>
 int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     TransportTmaArgs A;
     A.p = a;
@@ -551,7 +551,7 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
                             sizeof(double) + 2 * sizeof(UniformTable) + 16;
     static size_t smem_set = 0;
     if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_transport_tma<M, TLT, GEOM>,
+        rc = cuda_check(cudaFuncSetAttribute(k_transport_tma<M, TLT, GEOM, SZC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem),
                         "cudaFuncSetAttribute(k_transport_tma)");
@@ -561,12 +561,12 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     int dev = 0, sms = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_transport_tma<M, TLT, GEOM>, threads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_transport_tma<M, TLT, GEOM, SZC>, threads,
                                                   smem);
     if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_tma does not fit on an SM");
     long long grid = (long long)nb * sms;
     if (grid > A.items) grid = A.items;
-    k_transport_tma<M, TLT, GEOM><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_transport_tma<M, TLT, GEOM, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_transport_tma launch");
 }
 
@@ -607,6 +607,8 @@ int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
         if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_XZ>(a, s);
         if (tl == 8) return launch_transport_tma_t<16, 8, GEOM_XZ>(a, s);
     } else {
+        if (tl == 16 && a.sz == 32 && !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0'))
+            return launch_transport_tma_t<16, 16, GEOM_LINES, 32>(a, s);
         if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_LINES>(a, s);
         if (tl == 8) return launch_transport_tma_t<16, 8, GEOM_LINES>(a, s);
     }
