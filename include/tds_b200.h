@@ -202,16 +202,17 @@ int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2,
 int tds_transport_combine(const double* u_j, const double* du, const double* dp,
                           const double* d2u, double nu, double* out, long long count,
                           int accumulate, void* stream);
-/* acc += the (i, dir) contribution, dir = 1 (y) or 2 (z), for a cubic n^3
- * box with everything in the x layout (groups = n^2/sz, n, sz): the y / z
- * lines are read in place through 4-D tensor maps and the result is added
- * into acc. Replaces the reference's reorder(x->dir) + contribution +
- * reorder/accumulate(dir->x) of one term (momentum.py:129-169). Plans:
- * 16-row-chunk P=1 d/dx (d1) and d2/dx2 (d2) operators (TDS_FLAG_CHUNK16);
- * sz | n; y additionally needs sz = 32. TDS_ERR_UNSUPPORTED otherwise. */
+/* acc += the (i, dir) contribution, dir = 1 (y) or 2 (z), for an
+ * (nx, ny, nz) block with everything in the x layout (groups = ny nz/sz, nx,
+ * sz): the y / z lines are read in place through 4-D tensor maps and the
+ * result is added into acc. Replaces the reference's reorder(x->dir) +
+ * contribution + reorder/accumulate(dir->x) of one term (momentum.py:
+ * 129-169); a rank's z-slab uses it for y. Plans: 16-row-chunk P=1 d/dx (d1)
+ * and d2/dx2 (d2) operators of the line length (TDS_FLAG_CHUNK16); sz | ny;
+ * y additionally needs sz = 32, 16 | nx. TDS_ERR_UNSUPPORTED otherwise. */
 int tds_transport_contribution_in_x(const tds_plan* d1, const tds_plan* d2, const double* u_i,
-                                    const double* u_j, double* acc, double nu, int n, int sz,
-                                    int dir, void* stream);
+                                    const double* u_j, double* acc, double nu, int nx, int ny,
+                                    int nz, int sz, int dir, void* stream);
 /* cubic n^3 field: SZ-blocked layout of src_dir -> dst_dir in one pass
  * (reorder, layout.py:144-152); accumulate = 1 adds into dst */
 int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,

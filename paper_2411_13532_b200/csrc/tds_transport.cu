@@ -43,6 +43,7 @@ struct TransportArgs {
     const int* bq2;
     int nb1, nb2;
     int geom;              // GEOM_LINES, GEOM_XZ / GEOM_XY: z / y lines of an x-layout box
+    int nx, ny, nz;        // GEOM_XY / GEOM_XZ: the (nx, ny, nz) block (rows = ny / nz)
 };
 
 // Tile geometry of k_transport_tma: GEOM_LINES reads / writes the field in
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
             if (GEOM == GEOM_XY) {
                 // tile = x-block + (n/TLT) * z; halves of 16 lanes, all y-groups
                 const long long tile = first / TLT;
-                const int nxb = rows / TLT;
+                const int nxb = p.nx / TLT;
                 const int x0 = (int)(tile % nxb) * TLT, z = (int)(tile / nxb);
                 const size_t half = tile_elems / 2;
                 for (int h = 0; h < 2; ++h) {
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
             if (GEOM == GEOM_XZ) {
                 // line = lane-block + sz * (y-group + (n/sz) * x): z line (x, y)
                 const long long tile = first / TLT;
-                const int nlb = p.sz / TLT, ngj = rows / p.sz;
+                const int nlb = p.sz / TLT, ngj = p.ny / p.sz;
                 const int l0 = (int)(tile % nlb) * TLT;
                 const int gj = (int)((tile / nlb) % ngj);
                 const int x = (int)(tile / ((long long)nlb * ngj));
@@ -454,10 +455,10 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         if (valid && GEOM == GEOM_XY) {
             // x-layout address of (x, y, z): ((y/sz + z n/sz) n + x) sz + y % sz
             const long long tile = line / TLT;
-            const int nxb = rows / TLT;
+            const int nxb = p.nx / TLT;
             const long long x = (tile % nxb) * TLT + lane, z = tile / nxb;
             double2* ob = reinterpret_cast<double2*>(
-                p.out + (((long long)(r0 >> 5) + z * (rows / p.sz)) * rows + x) * sz + (r0 & 31));
+                p.out + (((long long)(r0 >> 5) + z * (p.ny / p.sz)) * p.nx + x) * sz + (r0 & 31));
 #pragma unroll
             for (int i = 0; i < M / 2; ++i) {
                 double2 o = ob[i];
@@ -468,11 +469,11 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         } else if (valid && GEOM == GEOM_XZ) {
             // x-layout address of (x, y, z): ((y-group + z n/sz) n + x) sz + lane
             const long long tile = line / TLT;
-            const int nlb = p.sz / TLT, ngj = rows / p.sz;
+            const int nlb = p.sz / TLT, ngj = p.ny / p.sz;
             const long long x = tile / ((long long)nlb * ngj);
             const long long gj = (tile / nlb) % ngj;
-            const long long rs = (long long)rows * rows;        // z stride: n^2
-            double* ob = p.out + (gj * rows + x) * sz + (tile % nlb) * TLT + lane + r0 * rs;
+            const long long rs = (long long)p.nx * p.ny;        // z stride: nx ny
+            double* ob = p.out + (gj * p.nx + x) * sz + (tile % nlb) * TLT + lane + r0 * rs;
 #pragma unroll
             for (int i = 0; i < M; ++i) ob[i * rs] = ob[i * rs] + acc[i];
         } else if (valid) {
@@ -485,13 +486,15 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
 
 namespace {
 
-// 4-D view of a cubic x-layout box (G = n^2/sz, n, sz): (lane, x, y-group, z)
-// with group = y-group + z * n/sz; box TLT lanes x 1 x 1 x boxr z-rows.
-int encode_xz_map(const double* u, int n, int sz, int M, int tl, CUtensorMap* map, int* boxr) {
-    *boxr = box_rows(n, M);
-    cuuint64_t dims[4] = {(cuuint64_t)sz, (cuuint64_t)n, (cuuint64_t)(n / sz), (cuuint64_t)n};
-    cuuint64_t strides[3] = {(cuuint64_t)sz * 8, (cuuint64_t)n * sz * 8,
-                             (cuuint64_t)n * (cuuint64_t)n * 8};
+// 4-D view of an x-layout (nx, ny, nz) block (G = ny nz/sz, nx, sz):
+// (lane, x, y-group, z) with group = y-group + z * ny/sz; box TLT lanes x
+// 1 x 1 x boxr z-rows.
+int encode_xz_map(const double* u, int nx, int ny, int nz, int sz, int M, int tl,
+                  CUtensorMap* map, int* boxr) {
+    *boxr = box_rows(nz, M);
+    cuuint64_t dims[4] = {(cuuint64_t)sz, (cuuint64_t)nx, (cuuint64_t)(ny / sz), (cuuint64_t)nz};
+    cuuint64_t strides[3] = {(cuuint64_t)sz * 8, (cuuint64_t)nx * sz * 8,
+                             (cuuint64_t)nx * (cuuint64_t)ny * 8};
     cuuint32_t box[4] = {(cuuint32_t)tl, 1, 1, (cuuint32_t)*boxr};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(u),
@@ -504,11 +507,11 @@ int encode_xz_map(const double* u, int n, int sz, int M, int tl, CUtensorMap* ma
 
 // The same 4-D view, box 16 lanes x TLT x-positions x all y-groups x 1 z,
 // 128-byte swizzle (GEOM_XY tiles).
-int encode_xy_map(const double* u, int n, int sz, int tl, CUtensorMap* map) {
-    cuuint64_t dims[4] = {(cuuint64_t)sz, (cuuint64_t)n, (cuuint64_t)(n / sz), (cuuint64_t)n};
-    cuuint64_t strides[3] = {(cuuint64_t)sz * 8, (cuuint64_t)n * sz * 8,
-                             (cuuint64_t)n * (cuuint64_t)n * 8};
-    cuuint32_t box[4] = {16, (cuuint32_t)tl, (cuuint32_t)(n / sz), 1};
+int encode_xy_map(const double* u, int nx, int ny, int nz, int sz, int tl, CUtensorMap* map) {
+    cuuint64_t dims[4] = {(cuuint64_t)sz, (cuuint64_t)nx, (cuuint64_t)(ny / sz), (cuuint64_t)nz};
+    cuuint64_t strides[3] = {(cuuint64_t)sz * 8, (cuuint64_t)nx * sz * 8,
+                             (cuuint64_t)nx * (cuuint64_t)ny * 8};
+    cuuint32_t box[4] = {16, (cuuint32_t)tl, (cuuint32_t)(ny / sz), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(u),
                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -535,12 +538,14 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     fi.lines = fj.lines = a.lines;
     int rc;
     if (GEOM == GEOM_XY) {
-        if ((rc = encode_xy_map(a.ui, a.rows, a.sz, TLT, &A.map_i))) return rc;
-        if ((rc = encode_xy_map(a.uj, a.rows, a.sz, TLT, &A.map_j))) return rc;
+        if ((rc = encode_xy_map(a.ui, a.nx, a.ny, a.nz, a.sz, TLT, &A.map_i))) return rc;
+        if ((rc = encode_xy_map(a.uj, a.nx, a.ny, a.nz, a.sz, TLT, &A.map_j))) return rc;
         A.boxr = a.rows;
     } else if (GEOM == GEOM_XZ) {
-        if ((rc = encode_xz_map(a.ui, a.rows, a.sz, M, TLT, &A.map_i, &A.boxr))) return rc;
-        if ((rc = encode_xz_map(a.uj, a.rows, a.sz, M, TLT, &A.map_j, &A.boxr))) return rc;
+        if ((rc = encode_xz_map(a.ui, a.nx, a.ny, a.nz, a.sz, M, TLT, &A.map_i, &A.boxr)))
+            return rc;
+        if ((rc = encode_xz_map(a.uj, a.nx, a.ny, a.nz, a.sz, M, TLT, &A.map_j, &A.boxr)))
+            return rc;
     } else {
         if ((rc = encode_field_map(fi, M, TLT, &A.map_i, &A.boxr))) return rc;
         if ((rc = encode_field_map(fj, M, TLT, &A.map_j, &A.boxr))) return rc;
@@ -598,12 +603,12 @@ static int transport_tma_tl(const TransportArgs& a) {
 int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
     const int tl = transport_tma_tl(a);
     if (a.geom == GEOM_XY) {
-        if (a.sz != 32 || a.rows % 32 || tl != 16)
-            return set_err(TDS_ERR_UNSUPPORTED, "xy transport: sz = 32, 32 | n, 16-line tiles");
+        if (a.sz != 32 || a.ny % 32 || a.nx % 16 || tl != 16)
+            return set_err(TDS_ERR_UNSUPPORTED, "xy transport: sz = 32, 32 | ny, 16 | nx");
         return launch_transport_tma_t<16, 16, GEOM_XY>(a, s);
     }
     if (a.geom == GEOM_XZ) {
-        if (a.rows % a.sz) return set_err(TDS_ERR_UNSUPPORTED, "xz transport: sz must divide n");
+        if (a.ny % a.sz) return set_err(TDS_ERR_UNSUPPORTED, "xz transport: sz must divide ny");
         if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_XZ>(a, s);
         if (tl == 8) return launch_transport_tma_t<16, 8, GEOM_XZ>(a, s);
     } else {
@@ -721,9 +726,13 @@ namespace tds {
 
 int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const double* ui,
                                 const double* uj, double* out, double nu, int accumulate,
-                                long long lines, int sz, cudaStream_t s, int geom) {
+                                long long lines, int sz, cudaStream_t s, int geom, int nx, int ny,
+                                int nz) {
     TransportArgs a;
     a.geom = geom;
+    a.nx = nx;
+    a.ny = ny;
+    a.nz = nz;
     a.ui = ui;
     a.uj = uj;
     a.out = out;

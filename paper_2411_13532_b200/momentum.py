@@ -208,7 +208,7 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
                 rc = N.lib().tds_transport_contribution_in_x(
                     p1.handle, None if p2 is None else p2.handle,
                     _vp(fields.component(i).data), _vp(adv), _vp(acc[i]), float(fields.nu), n,
-                    sz, _DIRECTIONS.index(dj), _stream_handle())
+                    n, n, sz, _DIRECTIONS.index(dj), _stream_handle())
                 if rc == N.TDS_ERR_UNSUPPORTED and i == 0:
                     break                     # shape not tileable: reorder path below
                 N.check(rc)
@@ -324,6 +324,29 @@ class SlabTransport:
                                      int(accumulate), _stream_handle()))
         return res
 
+    def _y_in_place(self, vel, acc):
+        """y terms read in place from the slab's x layout and added into acc
+        (tds_transport_contribution_in_x, GEOM_XY); False if not tileable."""
+        import os
+        if os.environ.get("TDS_TRANSPORT_Y") == "0" or self.sz != 32 or self.n % 32:
+            return False
+        n = self.n
+        part = SubdomainPartition((n,))
+        s1, st1 = _operator(1, self.h, n)
+        p1 = get_plan(s1, st1, part, chunk_rows=16)
+        p2 = None
+        if self.nu != 0.0:
+            s2, st2 = _operator(2, self.h, n)
+            p2 = get_plan(s2, st2, part, chunk_rows=16)
+        for i in range(3):
+            rc = N.lib().tds_transport_contribution_in_x(
+                p1.handle, None if p2 is None else p2.handle, _vp(vel[i]), _vp(vel[1]),
+                _vp(acc[i]), self.nu, n, n, self.m, self.sz, 1, _stream_handle())
+            if rc == N.TDS_ERR_UNSUPPORTED and i == 0:
+                return False
+            N.check(rc)
+        return True
+
     def _z_contribution(self, comp, advect, out):
         torch = _torch()
         if self._rank is None:
@@ -345,11 +368,12 @@ class SlabTransport:
         acc = [torch.empty_like(u) for _ in range(3)]
         for i in range(3):
             _local_contribution(vel[i], vel[0], acc[i], self.n, self.h, self.nu, False)
-        rot = [self._reorder(c, "x", "y") for c in vel]
-        scratch = torch.empty_like(rot[0])
-        for i in range(3):
-            _local_contribution(rot[i], rot[1], scratch, self.n, self.h, self.nu, False)
-            self._reorder(scratch, "y", "x", out=acc[i], accumulate=True)
+        if not self._y_in_place(vel, acc):
+            rot = [self._reorder(c, "x", "y") for c in vel]
+            scratch = torch.empty_like(rot[0])
+            for i in range(3):
+                _local_contribution(rot[i], rot[1], scratch, self.n, self.h, self.nu, False)
+                self._reorder(scratch, "y", "x", out=acc[i], accumulate=True)
         rot = [self._reorder(c, "x", "z") for c in vel]
         scratch = torch.empty_like(rot[0])
         for i in range(3):

@@ -86,8 +86,8 @@ def main():
     case("d1 periodic strict", lo, di, up, True, st, 1024, arith="strict", seed=5)
 
     # config 5: transport RHS on a z-slab decomposition (SlabTransport)
-    for nu in (0.02, 0.0):
-        n, sz = 128, 16
+    for nu, sz in ((0.02, 16), (0.0, 16), (0.01, 32)):
+        n = 128
         rng = np.random.default_rng(77)
         u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
         ctx = RankContext.from_process_group(cyclic=True)
@@ -111,7 +111,7 @@ def main():
                                     rank_counts=(world, world, world))
             errs_p = [O.rel_linf(g, w) for g, w in zip(fulls, ref_p)]
             ok = same and max(errs) <= 1e-12 and max(errs_p) <= 1e-12
-            print(f"[transport slab nu={nu}] P={world} m={tr.m} fused_z={tr._rank[0].fused} "
+            print(f"[transport slab nu={nu} sz={sz}] P={world} m={tr.m} fused_z={tr._rank[0].fused} "
                   f"rel(1,1,P)={max(errs):.3e} rel(P,P,P)={max(errs_p):.3e} repeat_same={same} "
                   f"{'OK' if ok else 'FAIL'}", flush=True)
             if not ok:
