@@ -603,9 +603,11 @@ static int transport_tma_tl(const TransportArgs& a) {
 int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
     const int tl = transport_tma_tl(a);
     if (a.geom == GEOM_XY) {
-        if (a.sz != 32 || a.ny % 32 || a.nx % 16 || tl != 16)
-            return set_err(TDS_ERR_UNSUPPORTED, "xy transport: sz = 32, 32 | ny, 16 | nx");
-        return launch_transport_tma_t<16, 16, GEOM_XY>(a, s);
+        // 8- or 16-line tiles: the swizzle row of (y-group, line) is line & 7
+        if (a.sz != 32 || a.ny % 32 || (tl != 16 && tl != 8) || a.nx % tl)
+            return set_err(TDS_ERR_UNSUPPORTED, "xy transport: sz = 32, 32 | ny, tile | nx");
+        if (tl == 16) return launch_transport_tma_t<16, 16, GEOM_XY>(a, s);
+        return launch_transport_tma_t<16, 8, GEOM_XY>(a, s);
     }
     if (a.geom == GEOM_XZ) {
         if (a.ny % a.sz) return set_err(TDS_ERR_UNSUPPORTED, "xz transport: sz must divide ny");

@@ -120,13 +120,15 @@ def test_slab_transport_single_rank(nu):
         assert torch.equal(rhs[i], ev[i].data)
 
 
-@pytest.mark.parametrize("n,sz,nu", [(64, 32, 0.05), (64, 8, 0.0), (128, 16, 0.02),
-                                     (128, 32, 0.0), (96, 32, 0.01)])
-def test_in_place_y_z_bitwise_equals_reorder_pipeline(monkeypatch, n, sz, nu):
+@pytest.mark.parametrize("n,sz,nu,tl", [(64, 32, 0.05, 16), (64, 8, 0.0, 16), (128, 16, 0.02, 16),
+                                        (128, 32, 0.0, 16), (96, 32, 0.01, 16),
+                                        (64, 32, 0.02, 8), (128, 32, 0.0, 8)])
+def test_in_place_y_z_bitwise_equals_reorder_pipeline(monkeypatch, n, sz, nu, tl):
     """y / z contributions read in place from the x layout and added into the
     accumulators (tds_transport_contribution_in_x; y needs sz = 32) give the
     same bits as the reference-shaped reorder -> contribution ->
     reorder/accumulate pipeline, and match the oracle."""
+    monkeypatch.setenv("TDS_TRANSPORT_TL", str(tl))     # 8: the n = 1024 tile width
     rng = np.random.default_rng(n + sz)
     u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
     f = T.VelocityField.from_arrays(u3, v3, w3, nu, 2 * np.pi / n, sz=sz)
