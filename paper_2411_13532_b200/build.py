@@ -10,6 +10,7 @@ The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -39,9 +40,9 @@ def build(force=False, verbose_ptxas=False):
     os.makedirs(LIBDIR, exist_ok=True)
     objdir = os.path.join(LIBDIR, "obj")
     os.makedirs(objdir, exist_ok=True)
-    headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".h")]
+    headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "tds_b200.h"))
-    objs = []
+    objs, jobs = [], []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(objdir, src + ".o")
@@ -51,15 +52,19 @@ def build(force=False, verbose_ptxas=False):
                    "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
-            _run(cmd)
+            jobs.append(cmd)
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            _run([NVCC, "-x", "c++", "-O2", "-std=c++17", "-Wno-deprecated-gpu-targets",
-                  "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
-                  "-c", s, "-o", o])
+            jobs.append([NVCC, "-x", "c++", "-O2", "-std=c++17", "-Wno-deprecated-gpu-targets",
+                         "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
+                         "-c", s, "-o", o])
+    # translation units compile independently: run them in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, j) for j in jobs]:
+            f.result()
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
     return LIB
