@@ -25,6 +25,9 @@ tds::FastArgs fast_args(const tds_plan* p, long long lines, int sz) {
     std::memset(&a, 0, sizeof(a));
     a.tab = p->d_tab;
     a.Hp = p->d_Hp;
+    a.Hb = p->d_Hb;
+    a.bq0 = p->d_bq0;
+    a.nb = p->band_n;
     a.g = p->d_g;
     a.lines = lines;
     a.rows = p->block_rows;

@@ -54,6 +54,9 @@ struct FastArgs {
     double* d_last_out;
     const double* tab;     // rows x NCOEF (GLOBAL table)
     const double2* Hp;     // C x K pairs: Hp[k*K+q] = (H[2k][q], H[2k+1][q])
+    const double2* Hb;     // banded Hp: C x nb pairs, columns bq0[k] + j (mod K)
+    const int* bq0;
+    int nb;
     const double* g;       // 2 x K pass-A functionals
     long long lines;
     long long items;       // work items of tiles_per_cta tiles (persistent kernels)

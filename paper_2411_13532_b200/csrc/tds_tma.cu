@@ -155,7 +155,13 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         }
 
         double F, L;
-        chunk_bounds<TLT>(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
+        // banded reduced map (plan.cpp upload_H: every entry above 2^-70 of the
+        // chunk's largest); TDS_BAND=0 -> the full K-term row
+        if (A.band)
+            band_bounds<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb, Y, K, lane,
+                             F, L);
+        else
+            chunk_bounds<TLT>(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
         if (valid)
             chunk_store_any<M, TAB>(p, tb, p.out + line_base_t<SZC>(line, p.rows, p.sz), sz, r0, d, F,
                                         L, A.store_cs != 0, chunk);
@@ -175,6 +181,7 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     int rc = encode_field_map(a, M, TLT, &A.map, &A.boxr);
     if (rc) return rc;
     A.store_cs = store_policy();
+    A.band = a.Hb && a.nb > 0 && !(getenv("TDS_BAND") && getenv("TDS_BAND")[0] == '0');
     const int threads = cfg.tpc * a.chunks * TLT;
     size_t smem = tma_smem(a, cfg);
     const size_t tab_bytes = (size_t)a.rows * NCOEF * sizeof(double);

@@ -14,6 +14,7 @@ struct TmaArgs {
     int boxr;          // rows per TMA box (divides rows)
     int store_cs;      // streaming stores (A/B knob TDS_STCS)
     int tab_smem;      // TAB_GLOBAL: per-row table staged in shared memory
+    int band;          // banded reduced map (FastArgs::Hb)
 };
 
 // lines per tile (8 or 16; 0 = not TMA-eligible) and tiles per CTA

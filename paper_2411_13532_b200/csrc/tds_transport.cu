@@ -245,34 +245,6 @@ __device__ __forceinline__ void sweeps_src(const UniformTable& T, Src v, double 
     d[0] = fma(-T.w[0], d[1], d[0]) * T.f[0];
 }
 
-// (F, L) of a chunk from the banded reduced map: nb columns starting at q0
-// (cyclic), Y in shared memory with stride TLT
-template <int TLT>
-__device__ __forceinline__ void band_bounds(const double2* __restrict__ hb, int q0, int nb,
-                                            const double* Y, int K, int lane, double& F,
-                                            double& L) {
-    double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
-    int q = q0, j = 0;
-    for (; j + 1 < nb; j += 2) {
-        const double2 h0 = __ldg(hb + j), h1 = __ldg(hb + j + 1);
-        const int qb = q + 1 == K ? 0 : q + 1;
-        const double ya = Y[q * TLT + lane], yb = Y[qb * TLT + lane];
-        F0 = fma(h0.x, ya, F0);
-        L0 = fma(h0.y, ya, L0);
-        F1 = fma(h1.x, yb, F1);
-        L1 = fma(h1.y, yb, L1);
-        q = qb + 1 == K ? 0 : qb + 1;
-    }
-    if (j < nb) {
-        const double2 h0 = __ldg(hb + j);
-        const double ya = Y[q * TLT + lane];
-        F0 = fma(h0.x, ya, F0);
-        L0 = fma(h0.y, ya, L0);
-    }
-    F = F0 + F1;
-    L = L0 + L1;
-}
-
 __device__ __forceinline__ double subst(const UniformTable& T, int i, int M, double F, double L,
                                         double di) {
     return i == 0 ? F : (i == M - 1 ? L : fma(-T.sc[i], L, fma(-T.sa[i], F, di)));
