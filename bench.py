@@ -216,7 +216,7 @@ def run_single(args, torch):
         "ms_per_solve": {d: round(v, 5) for d, v in per_dir.items()},
         "direction_spread_pct": round(100 * (max(per_dir.values()) - min(per_dir.values()))
                                       / min(per_dir.values()), 2),
-        "roofline": {"bound": "hbm", "kernel": "k_tma<32,SOLVE,TAB_UNIFORM,16> (TMA-staged fused solve)",
+        "roofline": {"bound": "hbm", "kernel": "k_tma<32,SOLVE,TAB_UNIFORM,32,sz=32> (TMA-staged fused solve, 32-line tiles)",
                      "achieved": round(achieved, 2), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": ncu_traffic(),

@@ -211,14 +211,13 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
 template <int M, int MODE, int UNI>
 int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     const TileCfg cfg = tile_cfg(a);
-    // 32-line tiles: one chunk per warp, so a special edge chunk (TAB_EDGES)
-    // or a per-row table chunk (TAB_GLOBAL) never diverges from its warp
-    // neighbour; 1 CTA of 512 threads per SM. Uniform plans keep 16-line
-    // tiles (2 CTAs/SM): at 512^3 under the sustained-load power cap (~1700
-    // MHz) 16-line tiles measured 5827 vs 5750 GB/s, at full clock 32-line
-    // tiles 5977 vs 5631. A/B knob TDS_TMA_TL32 = 0 (never) / 1 (always).
+    // 32-line tiles (1 CTA of 512 threads per SM): one chunk per warp, so a
+    // special edge chunk never diverges from a uniform neighbour, 256-byte row
+    // segments, and (with the compile-time lane width and the banded map)
+    // fewer instructions. Measured at 512^3, 1000 steps under the power cap:
+    // 5812 / 5823 GB/s vs 5523 / 5532 for 16-line tiles. Knob TDS_TMA_TL32=0.
     const char* e32 = getenv("TDS_TMA_TL32");
-    const bool want32 = e32 ? e32[0] == '1' : UNI != TAB_UNIFORM;
+    const bool want32 = e32 ? e32[0] == '1' : true;
     if (want32 && MODE == MODE_SOLVE && a.sz % 32 == 0 && a.chunks * 32 <= 512 &&
         (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 <= 200 * 1024)
         // compile-time lane width: 5147 vs 4980 GB/s for open d/dx at 512^3
