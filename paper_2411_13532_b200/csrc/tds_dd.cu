@@ -241,8 +241,12 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         // pin-independent part of the reduced map first (overlaps the
         // edge warps' ROUND 2 below)
         double F, L;
-        chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr, nullptr,
-                          F, L);
+        if (A.t.band)   // banded reduced map, pin columns excluded (TDS_BAND=0: full row)
+            band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb, Y,
+                                    K, lane, F, L);
+        else
+            chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr,
+                              nullptr, F, L);
         // ROUND 2: the rank's decoupled boundary rows, 2x2 pairs, pins
         double* P = sP + (size_t)tl * 2 * TLT;
         if (valid && (first_chunk || last_chunk)) {
@@ -505,8 +509,12 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
 
         // chunk boundary values without the rank pins
         double F, L;
-        chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr, nullptr,
-                          F, L);
+        if (A.t.band)   // banded reduced map, pin columns excluded (TDS_BAND=0: full row)
+            band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb, Y,
+                                    K, lane, F, L);
+        else
+            chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr,
+                              nullptr, F, L);
         if (!edge_warp) {
             // ROUND 2 posts of this item (helper warp): the rank's d[0] / d[m-1]
             if (wt == 1 && role < 2 && valid) {
@@ -676,6 +684,7 @@ int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail
     A.mail_next = mail_next;
     A.epoch = epoch;
     A.timeout_ns = 10ULL * 1000 * 1000 * 1000;   // 10 s: a stall records an error
+    A.t.band = a.Hb && a.nb > 0 && !(getenv("TDS_BAND") && getenv("TDS_BAND")[0] == '0');
     if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
         A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
     const int tab = !uniform ? TAB_GLOBAL

@@ -216,6 +216,35 @@ __device__ __forceinline__ void band_bounds(const double2* __restrict__ hb, int 
     L = L0 + L1;
 }
 
+// The same with the rank pins' columns (q = 0 and q = K-1 of a per-rank map)
+// left out: they are applied separately once u_start / u_end are known.
+template <int TLT>
+__device__ __forceinline__ void band_bounds_nopins(const double2* __restrict__ hb, int q0, int nb,
+                                                   const double* Y, int K, int lane, double& F,
+                                                   double& L) {
+    double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
+    int q = q0, j = 0;
+    for (; j + 1 < nb; j += 2) {
+        const double2 h0 = __ldg(hb + j), h1 = __ldg(hb + j + 1);
+        const int qb = q + 1 == K ? 0 : q + 1;
+        const double ya = (q == 0 || q == K - 1) ? 0.0 : Y[q * TLT + lane];
+        const double yb = (qb == 0 || qb == K - 1) ? 0.0 : Y[qb * TLT + lane];
+        F0 = fma(h0.x, ya, F0);
+        L0 = fma(h0.y, ya, L0);
+        F1 = fma(h1.x, yb, F1);
+        L1 = fma(h1.y, yb, L1);
+        q = qb + 1 == K ? 0 : qb + 1;
+    }
+    if (j < nb) {
+        const double2 h0 = __ldg(hb + j);
+        const double ya = (q == 0 || q == K - 1) ? 0.0 : Y[q * TLT + lane];
+        F0 = fma(h0.x, ya, F0);
+        L0 = fma(h0.y, ya, L0);
+    }
+    F = F0 + F1;
+    L = L0 + L1;
+}
+
 // Alg. 7 at chunk level + one streaming store per row.
 template <int M, bool UNIFORM>
 __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __restrict__ tb,
