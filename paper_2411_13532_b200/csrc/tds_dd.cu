@@ -657,6 +657,19 @@ int launch_dd_m(const DDArgs& A, cudaStream_t s) {
                        (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
     if (cfg.tl == 8)
         return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);
+    if constexpr (M == 32) {
+        // k_dd with 32-line tiles (one chunk per warp) when no deferral
+        // applies (m = 128: every chunk is an edge chunk). Same choice on
+        // every rank: it depends on the plan and sz only. Knob TDS_DD_TL32=0.
+        const bool tl32 = !defer && A.t.f.sz == 32 && A.t.f.chunks * 32 <= 512 &&
+                          !(getenv("TDS_DD_TL32") && getenv("TDS_DD_TL32")[0] == '0') &&
+                          !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0');
+        if (tl32) {
+            const int per_tile = A.t.f.chunks * 32;
+            const TileCfg c32{32, per_tile >= 256 ? 1 : 256 / per_tile};
+            if (dd_smem(A.t.f, c32) <= 200 * 1024) return launch_dd_t<M, UNI, 32, 32>(A, c32, s);
+        }
+    }
     if constexpr (M == 32)
         if (A.t.f.sz == 32 && !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0'))
             return defer ? launch_dd2_t<M, UNI, 16, 32>(A, cfg, s)
