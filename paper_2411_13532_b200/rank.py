@@ -25,8 +25,8 @@ import os
 import ctypes
 
 from . import _native as N
-from .distributed import (DistCoeffs, Plan, _flags, _stream_handle, decouple_fused,
-                          solve_boundary_pair, substitute, BoundaryPair, local_slice)
+from .distributed import (Plan, _flags, _stream_handle, decouple_fused, solve_boundary_pair,
+                          substitute, BoundaryPair)
 from .transport import (BOUNDARY_HIGH, BOUNDARY_LOW, HALO_HIGH, HALO_LOW, exchange_boundary,
                         exchange_halo)
 
