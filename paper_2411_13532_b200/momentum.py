@@ -299,6 +299,7 @@ class SlabTransport:
         self.off = self.part.offsets()[r]
         self.lay = {d: LayoutDescriptor(n, n, self.m, sz, d) for d in _DIRECTIONS}
         self._rank = None
+        self._marks = None
         if p > 1:
             if not ctx.cyclic:
                 raise ValueError("the transport box is periodic: the rank chain must be a ring")
@@ -366,20 +367,40 @@ class SlabTransport:
         torch = _torch()
         vel = (u, v, w)
         acc = [torch.empty_like(u) for _ in range(3)]
+        marks = self._marks
+        if marks is not None:
+            marks[0].record()
         for i in range(3):
             _local_contribution(vel[i], vel[0], acc[i], self.n, self.h, self.nu, False)
+        if marks is not None:
+            marks[1].record()
         if not self._y_in_place(vel, acc):
             rot = [self._reorder(c, "x", "y") for c in vel]
             scratch = torch.empty_like(rot[0])
             for i in range(3):
                 _local_contribution(rot[i], rot[1], scratch, self.n, self.h, self.nu, False)
                 self._reorder(scratch, "y", "x", out=acc[i], accumulate=True)
+        if marks is not None:
+            marks[2].record()
         rot = [self._reorder(c, "x", "z") for c in vel]
         scratch = torch.empty_like(rot[0])
         for i in range(3):
             self._z_contribution(rot[i], rot[2], scratch)
             self._reorder(scratch, "z", "x", out=acc[i], accumulate=True)
+        if marks is not None:
+            marks[3].record()
         return tuple(acc)
+
+    def phase_ms(self):
+        """Per-direction device time (x, y, z terms) of the last rhs() call
+        when timing was enabled with `timed(True)`."""
+        m = self._marks
+        return {d: m[k].elapsed_time(m[k + 1]) for k, d in enumerate("xyz")}
+
+    def timed(self, on=True):
+        torch = _torch()
+        self._marks = ([torch.cuda.Event(enable_timing=True) for _ in range(4)] if on
+                       else None)
 
     def euler_step(self, u, v, w, dt):
         """u <- u + dt * RHS(u) on this rank's slab (momentum.py:216-222)."""

@@ -94,6 +94,13 @@ def main():
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             t = float(tt.item())
         best = min(best, t)
+    phases = None
+    if world > 1 or args.slab:
+        tr.timed(True)
+        step()
+        torch.cuda.synchronize()
+        phases = {k: round(v, 3) for k, v in tr.phase_ms().items()}
+        tr.timed(False)
     if world > 1:
         tr.check()
         tr.close()
@@ -104,7 +111,8 @@ def main():
                           "ms_per_rhs": round(best, 3),
                           "gdof_per_s": round(pts / (best * 1e-3) / 1e9, 2),
                           "gdof_per_s_per_gpu": round(pts_local / (best * 1e-3) / 1e9, 2),
-                          "logical_gbs_432B": round(BYTES_PER_POINT * pts / (best * 1e-3) / 1e9, 1)}),
+                          "logical_gbs_432B": round(BYTES_PER_POINT * pts / (best * 1e-3) / 1e9, 1),
+                          "rank0_phase_ms": phases}),
               flush=True)
     if world > 1:
         torch.distributed.barrier()
