@@ -202,6 +202,22 @@ int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2,
 int tds_transport_combine(const double* u_j, const double* du, const double* dp,
                           const double* d2u, double nu, double* out, long long count,
                           int accumulate, void* stream);
+/* One (i, j) transport term along a direction split over the ranks
+ * (one rank per GPU; SlabTransport's z terms): out = -1/2 (u_j d(u_i) +
+ * d(u_j u_i)) + nu d2(u_i) on this rank's (groups, m, sz) block, the three
+ * DistD2 solves fused in one kernel with their neighbour rounds done over
+ * IPC-mapped mailboxes (tds_transport_mailbox_words words each, sentinel
+ * filled by tds_ipc_alloc). d1 / d2: this rank's d/dx and d2/dx2 plans with
+ * 16-row chunks (TDS_FLAG_CHUNK16). Replaces directional_contribution
+ * (momentum.py:102-126) with run_distd2 over the rank chain.
+ * TDS_ERR_UNSUPPORTED when the plans / field do not allow it. */
+long long tds_transport_mailbox_words(long long groups, int sz);
+int tds_transport_mailbox_error(const double* mail, long long groups, int sz, int* err);
+int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const double* u_i,
+                        const double* u_j, double* out, double nu, long long groups, int sz,
+                        double* mail, double* mail_prev, double* mail_next,
+                        unsigned long long epoch, void* stream);
+
 /* acc += the (i, dir) contribution, dir = 1 (y) or 2 (z), for an
  * (nx, ny, nz) block with everything in the x layout (groups = ny nz/sz, nx,
  * sz): the y / z lines are read in place through 4-D tensor maps and the

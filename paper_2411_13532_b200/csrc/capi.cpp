@@ -7,6 +7,7 @@
 #include <string>
 
 #include "tds_internal.h"
+#include "tds_tma.h"
 
 using tds::set_err;
 
@@ -333,6 +334,56 @@ extern "C" int tds_mailbox_error(const double* mail, long long groups, int sz, i
                              "read mailbox error word");
     *err = (v == 1ULL) ? 1 : 0;   // ERR_TIMEOUT (sentinel fill = no error)
     return rc;
+}
+
+namespace tds {
+long long dd_transport_mail_words(long long lines);
+int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui,
+                        const double* uj, double* out, double nu, long long lines, int sz,
+                        double* mail, double* mail_prev, double* mail_next,
+                        unsigned long long epoch, cudaStream_t s);
+}  // namespace tds
+
+extern "C" long long tds_transport_mailbox_words(long long groups, int sz) {
+    return tds::dd_transport_mail_words(groups * sz);
+}
+
+extern "C" int tds_transport_mailbox_error(const double* mail, long long groups, int sz,
+                                           int* err) {
+    long long words = tds::dd_transport_mail_words(groups * sz);
+    unsigned long long v = 0;
+    int rc = tds::cuda_check(cudaMemcpy(&v, mail + (words - 1), 8, cudaMemcpyDeviceToHost),
+                             "read transport mailbox error word");
+    *err = (v == 1ULL) ? 1 : 0;
+    return rc;
+}
+
+extern "C" int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const double* u_i,
+                                   const double* u_j, double* out, double nu, long long groups,
+                                   int sz, double* mail, double* mail_prev, double* mail_next,
+                                   unsigned long long epoch, void* stream) {
+    int rc = check_field(d1, groups, sz);
+    if (rc) return rc;
+    if (!u_i || !u_j || !out || !mail) return set_err(TDS_ERR_INVALID, "null argument");
+    auto ok = [&](const tds_plan* p) {
+        return p->rank >= 0 && p->P >= 2 && p->path == TDS_PATH_FAST && p->M == 16 &&
+               p->uniform && !p->special_first && !p->special_last;
+    };
+    if (!ok(d1) || (nu != 0.0 && (!d2 || !ok(d2) || d2->C != d1->C || d2->rank != d1->rank ||
+                                  d2->block_rows != d1->block_rows)))
+        return set_err(TDS_ERR_UNSUPPORTED,
+                       "fused distributed transport needs uniform per-rank 16-row-chunk plans");
+    if ((d1->has_prev && !mail_prev) || (d1->has_next && !mail_next))
+        return set_err(TDS_ERR_INVALID, "missing mailbox");
+    if (reinterpret_cast<uintptr_t>(u_i) % 16 || reinterpret_cast<uintptr_t>(u_j) % 16 ||
+        tds::box_rows(d1->block_rows, 16) == 0 || !tds::encode_fn())
+        return set_err(TDS_ERR_UNSUPPORTED, "fused distributed transport: not TMA-eligible");
+    const long long lines = groups * sz;
+    tds::FastArgs f1 = fast_args(d1, lines, sz);
+    tds::FastArgs f2 = nu != 0.0 ? fast_args(d2, lines, sz) : f1;
+    return tds::launch_dd_transport(f1, f2, u_i, u_j, out, nu, lines, sz, mail,
+                                    d1->has_prev ? mail_prev : nullptr,
+                                    d1->has_next ? mail_next : nullptr, epoch, S(stream));
 }
 
 extern "C" int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle) {

@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "tds_device.cuh"
 #include "tds_tma.h"
@@ -79,7 +80,8 @@ __device__ __forceinline__ unsigned long long ld_sys_u64(const double* p) {
 }
 // wait for a neighbour's value in my mailbox slot, consume it, re-arm the slot
 // (v: the slot's value if already loaded, else SENTINEL)
-__device__ double take_v(double* slot, unsigned long long v, const DDArgs& A,
+template <class Args>
+__device__ double take_v(double* slot, unsigned long long v, const Args& A,
                          unsigned long long* err) {
     if (v == SENTINEL) v = ld_sys_u64(slot);
     if (v == SENTINEL) {
@@ -100,7 +102,8 @@ __device__ double take_v(double* slot, unsigned long long v, const DDArgs& A,
     *reinterpret_cast<unsigned long long*>(slot) = SENTINEL;
     return __longlong_as_double((long long)v);
 }
-__device__ __forceinline__ double take(double* slot, const DDArgs& A, unsigned long long* err) {
+template <class Args>
+__device__ __forceinline__ double take(double* slot, const Args& A, unsigned long long* err) {
     return take_v(slot, SENTINEL, A, err);
 }
 
@@ -710,6 +713,384 @@ int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail
     if (M == 16) { DISPATCH_TAB(16) }
 #undef DISPATCH_TAB
     return set_err(TDS_ERR_UNSUPPORTED, "unsupported chunk size");
+}
+
+// ===========================================================================
+// k_dd_transport: one (i, j) term of the transport RHS along a direction
+// that is split over the ranks (SlabTransport's z terms), as ONE kernel per
+// rank: -1/2 (u_j d(u_i) + d(u_j u_i)) + nu d2(u_i) with the three compact
+// solves of every chunk fused as in k_transport_tma (16-row chunks, running
+// contribution in registers, u_i / u_j tiles by TMA read from shared memory)
+// and each solve's two neighbour rounds done in-kernel as in k_dd: ROUND 1
+// posts the first / last two rows of u_i and u_j one item ahead, ROUND 2
+// posts each solve's g.Y and takes the neighbour's (2x2 pair -> pins). The
+// reference's per-term pipeline (momentum.py:102-126 with run_distd2 over
+// rank_count ranks) is three DistD2 solves + products; here the HBM traffic
+// is u_i, u_j read once and the term written once (24 B/point).
+//
+// Mailbox (TrMail, 8-byte sentinel slots, two parity halves of 14 L):
+//   DP(s) [L], s = 0..2   prev's d[m-1] of solve s
+//   DN(s) [L]             next's d[0] of solve s
+//   HLO_I, HLO_J [2L]     prev's last two rows of u_i, u_j
+//   HHI_I, HHI_J [2L]     next's first two rows of u_i, u_j
+// Deadlock freedom as k_dd: identical persistent schedule on every rank,
+// posts before waits, waits only on the same CTA index of a neighbour.
+struct TrMail {
+    long long L;
+    __host__ __device__ long long half(unsigned long long epoch) const {
+        return (long long)(epoch & 1ULL) * 14 * L;
+    }
+    __host__ __device__ long long dp(int s) const { return s * L; }
+    __host__ __device__ long long dn(int s) const { return (3 + s) * L; }
+    __host__ __device__ long long hlo_i() const { return 6 * L; }
+    __host__ __device__ long long hlo_j() const { return 8 * L; }
+    __host__ __device__ long long hhi_i() const { return 10 * L; }
+    __host__ __device__ long long hhi_j() const { return 12 * L; }
+    __host__ __device__ long long err() const { return 28 * L; }
+    __host__ __device__ long long words() const { return 28 * L + 1; }
+};
+
+struct TrDDArgs {
+    FastArgs f1, f2;           // rank plans: d/dx (f1), d2/dx2 (f2); Hp = pinned map
+    CUtensorMap map_i, map_j;
+    int boxr;
+    const double* ui;
+    const double* uj;
+    double* out;
+    double nu;
+    int has_nu;
+    long long lines;
+    int rows, sz, chunks, tpc;
+    long long items;
+    int band;
+    double* mail;
+    double* mail_prev;
+    double* mail_next;
+    unsigned long long epoch;
+    unsigned long long timeout_ns;
+};
+
+namespace {
+
+template <int M, typename Src>
+__device__ __forceinline__ void tr_sweeps(const UniformTable& T, Src v, double (&d)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double rhs = T.st[0] * v(i);
+        rhs = fma(T.st[1], v(i + 1), rhs);
+        rhs = fma(T.st[2], v(i + 2), rhs);
+        rhs = fma(T.st[3], v(i + 3), rhs);
+        rhs = fma(T.st[4], v(i + 4), rhs);
+        if (i < 2) d[i] = rhs * T.r[i];
+        else d[i] = fma(-T.r[i], d[i - 1], rhs) * T.f[i];
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) d[i] = fma(-T.w[i], d[i + 1], d[i]);
+    d[0] = fma(-T.w[0], d[1], d[0]) * T.f[0];
+}
+
+__device__ __forceinline__ double tr_subst(const UniformTable& T, int i, int M, double F,
+                                           double L, double di) {
+    return i == 0 ? F : (i == M - 1 ? L : fma(-T.sc[i], L, fma(-T.sa[i], F, di)));
+}
+
+}  // namespace
+
+template <int TLT, int SZC>
+__global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__ TrDDArgs A) {
+    constexpr int M = 16;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int C = A.chunks, K = 2 * C, rows = A.rows, tpc = A.tpc;
+    const int t = threadIdx.x;
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
+    const long long sz = SZC ? SZC : A.sz;
+    const int r0 = chunk * M;
+    const TrMail mb{A.lines};
+    const long long par = mb.half(A.epoch);
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(A.mail + mb.err());
+    const size_t tile_elems = (size_t)rows * TLT;
+    double* ti = reinterpret_cast<double*>(smem);
+    double* tj = ti + (size_t)tpc * tile_elems;
+    double* sY = tj + (size_t)tpc * tile_elems;           // [3][tpc][K][TLT]
+    const size_t ybuf = (size_t)tpc * K * TLT;
+    double* sP = sY + 3 * ybuf;                           // [3][tpc][2][TLT]
+    UniformTable* sT = reinterpret_cast<UniformTable*>(sP + (size_t)3 * tpc * 2 * TLT);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sT + 2);
+    const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
+    {
+        const double* s1 = reinterpret_cast<const double*>(&A.f1.ut);
+        const double* s2 = reinterpret_cast<const double*>(&A.f2.ut);
+        double* dst = reinterpret_cast<double*>(sT);
+        constexpr int W = sizeof(UniformTable) / sizeof(double);
+        for (int k = t; k < 2 * W; k += blockDim.x) dst[k] = k < W ? s1[k] : s2[k - W];
+    }
+    const UniformTable& T1 = sT[0];
+    const UniformTable& T2 = sT[1];
+
+    auto issue = [&](long long item) {
+        uint32_t bytes = 0;
+        for (int j = 0; j < tpc; ++j)
+            if ((item * tpc + j) * TLT < A.lines)
+                bytes += (uint32_t)(2 * tile_elems * sizeof(double));
+        mbar_expect_tx(bar, bytes);
+        for (int j = 0; j < tpc; ++j) {
+            const long long first = (item * tpc + j) * TLT;
+            if (first >= A.lines) break;
+            const int g = (int)(first / A.sz), l0 = (int)(first % A.sz);
+            for (int b = 0; b * A.boxr < rows; ++b) {
+                tma_load_3d(ti + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_i, bar, l0,
+                            b * A.boxr, g);
+                tma_load_3d(tj + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_j, bar, l0,
+                            b * A.boxr, g);
+            }
+        }
+    };
+    // ROUND 1 of `item`: first two rows of u_i, u_j -> prev, last two -> next
+    auto publish_halo = [&](long long item) {
+        if (!first_chunk && !last_chunk) return;
+        const long long ln = (item * tpc + tl) * TLT + lane;
+        if (ln >= A.lines) return;
+        const long long lb = line_base_t<SZC>(ln, rows, A.sz);
+        const double* bi = A.ui + lb;
+        const double* bj = A.uj + lb;
+        const long long hb = halo_base_t<SZC>(ln, A.sz);
+        if (first_chunk && A.mail_prev) {
+            double* m = A.mail_prev + par;
+            post(m + mb.hhi_i() + hb, __ldg(bi));
+            post(m + mb.hhi_i() + hb + sz, __ldg(bi + sz));
+            post(m + mb.hhi_j() + hb, __ldg(bj));
+            post(m + mb.hhi_j() + hb + sz, __ldg(bj + sz));
+        }
+        if (last_chunk && A.mail_next) {
+            double* m = A.mail_next + par;
+            const long long a = (long long)(rows - 2) * sz, b = (long long)(rows - 1) * sz;
+            post(m + mb.hlo_i() + hb, __ldg(bi + a));
+            post(m + mb.hlo_i() + hb + sz, __ldg(bi + b));
+            post(m + mb.hlo_j() + hb, __ldg(bj + a));
+            post(m + mb.hlo_j() + hb + sz, __ldg(bj + b));
+        }
+    };
+    auto release = [&](long long nxt) {
+        __syncthreads();
+        if (t == 0 && nxt < A.items) {
+            fence_proxy_async();
+            issue(nxt);
+        }
+    };
+
+    if (t == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    long long item = blockIdx.x;
+    if (item < A.items) {
+        if (t == 0) issue(item);
+        publish_halo(item);
+    }
+    uint32_t phase = 0;
+    const double* Ti = ti + tl * tile_elems;
+    const double* Tj = tj + tl * tile_elems;
+    const int base = (r0 - 2) * TLT + lane;
+
+    for (; item < A.items; item += gridDim.x) {
+        const long long line = (item * tpc + tl) * TLT + lane;
+        const bool valid = line < A.lines;
+        const long long nxt = item + gridDim.x;
+        if (nxt < A.items) publish_halo(nxt);            // one item ahead
+        const long long hb = valid ? halo_base_t<SZC>(line, A.sz) : 0;
+        const bool hlo = valid && first_chunk && A.mail_prev;
+        const bool hhi = valid && last_chunk && A.mail_next;
+        while (!mbar_try_wait(bar, phase)) {
+        }
+        phase ^= 1u;
+        // rank-edge halos of u_i and u_j (ROUND 1 of this item)
+        double hi0 = 0.0, hi1 = 0.0, hi2 = 0.0, hi3 = 0.0;
+        double hj0 = 0.0, hj1 = 0.0, hj2 = 0.0, hj3 = 0.0;
+        if (hlo) {
+            double* m = A.mail + par;
+            hi0 = take(m + mb.hlo_i() + hb, A, err);
+            hi1 = take(m + mb.hlo_i() + hb + sz, A, err);
+            hj0 = take(m + mb.hlo_j() + hb, A, err);
+            hj1 = take(m + mb.hlo_j() + hb + sz, A, err);
+        }
+        if (hhi) {
+            double* m = A.mail + par;
+            hi2 = take(m + mb.hhi_i() + hb, A, err);
+            hi3 = take(m + mb.hhi_i() + hb + sz, A, err);
+            hj2 = take(m + mb.hhi_j() + hb, A, err);
+            hj3 = take(m + mb.hhi_j() + hb + sz, A, err);
+        }
+        // window row i (= block row r0 - 2 + i) of u_i / u_j
+        auto wi = [&](int i) {
+            if (i < 2 && first_chunk) return i == 0 ? hi0 : hi1;
+            if (i >= M + 2 && last_chunk) return i == M + 2 ? hi2 : hi3;
+            return Ti[base + i * TLT];
+        };
+        auto wj = [&](int i) {
+            if (i < 2 && first_chunk) return i == 0 ? hj0 : hj1;
+            if (i >= M + 2 && last_chunk) return i == M + 2 ? hj2 : hj3;
+            return Tj[base + i * TLT];
+        };
+        double acc[M], d[M];
+        double F, L;
+        // one solve's chunk boundary values with the rank pins (ROUND 2)
+        auto bounds = [&](int s, const FastArgs& p) {
+            double* Y = sY + (size_t)s * ybuf + (size_t)tl * K * TLT;
+            Y[(2 * chunk) * TLT + lane] = d[0];
+            Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            __syncthreads();
+            if (A.band)
+                band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb,
+                                        Y, K, lane, F, L);
+            else
+                chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr,
+                                  nullptr, F, L);
+            double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
+            if (valid && (first_chunk || last_chunk)) {
+                double g0y = 0.0, g1y = 0.0;
+                for (int q = 0; q < K; ++q) {
+                    const double y = Y[q * TLT + lane];
+                    if (first_chunk) g0y = fma(__ldg(p.g + q), y, g0y);
+                    if (last_chunk) g1y = fma(__ldg(p.g + K + q), y, g1y);
+                }
+                if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
+                if (last_chunk && A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
+                if (first_chunk) {
+                    double us = g0y;
+                    if (p.has_prev) {
+                        const double prev_last = take(A.mail + par + mb.dp(s) + line, A, err);
+                        us = (g0y - p.sa_first * prev_last) / p.det_prev;
+                    }
+                    P[lane] = us;
+                }
+                if (last_chunk) {
+                    double ue = g1y;
+                    if (p.has_next) {
+                        const double next_first = take(A.mail + par + mb.dn(s) + line, A, err);
+                        ue = (g1y - p.sc_last * next_first) / p.det_next;
+                    }
+                    P[TLT + lane] = ue;
+                }
+            }
+            __syncthreads();
+            const double2 h0 = __ldg(p.Hp + (size_t)chunk * K);
+            const double2 hl = __ldg(p.Hp + (size_t)chunk * K + K - 1);
+            const double us = P[lane], ue = P[TLT + lane];
+            F = fma(h0.x, us, fma(hl.x, ue, F));
+            L = fma(h0.y, us, fma(hl.y, ue, L));
+        };
+
+        // (A) d(u_i) -> acc = u_j * du_i
+        tr_sweeps<M>(T1, wi, d);
+        bounds(0, A.f1);
+#pragma unroll
+        for (int i = 0; i < M; ++i) acc[i] = Tj[base + (i + 2) * TLT] * tr_subst(T1, i, M, F, L, d[i]);
+        // (B) d(u_j u_i) -> acc = -1/2 (acc + dprod)
+        tr_sweeps<M>(T1, [&](int i) { return wj(i) * wi(i); }, d);
+        if (!A.has_nu) release(nxt);
+        bounds(1, A.f1);
+#pragma unroll
+        for (int i = 0; i < M; ++i) acc[i] = -0.5 * (acc[i] + tr_subst(T1, i, M, F, L, d[i]));
+        // (C) acc += nu d2(u_i)
+        if (A.has_nu) {
+            tr_sweeps<M>(T2, wi, d);
+            release(nxt);
+            bounds(2, A.f2);
+#pragma unroll
+            for (int i = 0; i < M; ++i) acc[i] = fma(A.nu, tr_subst(T2, i, M, F, L, d[i]), acc[i]);
+        }
+        if (valid) {
+            double* ob = A.out + line_base_t<SZC>(line, rows, A.sz) + (long long)r0 * sz;
+#pragma unroll
+            for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
+        }
+    }
+}
+
+namespace {
+
+template <int TLT, int SZC>
+int launch_dd_transport_t(const TrDDArgs& A0, cudaStream_t s) {
+    TrDDArgs A = A0;
+    const int per_tile = A.chunks * TLT;
+    A.tpc = per_tile >= 256 ? 1 : 256 / per_tile;
+    const long long tiles = (A.lines + TLT - 1) / TLT;
+    A.items = (tiles + A.tpc - 1) / A.tpc;
+    if (A.items <= 0) return TDS_OK;
+    FastArgs fi{}, fj{};
+    fi.u = A.ui;
+    fj.u = A.uj;
+    fi.rows = fj.rows = A.rows;
+    fi.sz = fj.sz = A.sz;
+    fi.lines = fj.lines = A.lines;
+    int rc = encode_field_map(fi, 16, TLT, &A.map_i, &A.boxr);
+    if (rc) return rc;
+    rc = encode_field_map(fj, 16, TLT, &A.map_j, &A.boxr);
+    if (rc) return rc;
+    const int threads = A.tpc * per_tile;
+    const size_t smem = (size_t)A.tpc *
+                            (2 * (size_t)A.rows * TLT + 3 * (size_t)2 * A.chunks * TLT +
+                             3 * 2 * TLT) * sizeof(double) +
+                        2 * sizeof(UniformTable) + 16;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        rc = cuda_check(cudaFuncSetAttribute(k_dd_transport<TLT, SZC>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem),
+                        "cudaFuncSetAttribute(k_dd_transport)");
+        if (rc) return rc;
+        smem_set = smem;
+    }
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd_transport<TLT, SZC>, threads, smem);
+    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport does not fit on an SM");
+    long long grid = (long long)nb * sms;   // co-resident, identical on every rank
+    if (grid > A.items) grid = A.items;
+    k_dd_transport<TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_dd_transport launch");
+}
+
+}  // namespace
+
+long long dd_transport_mail_words(long long lines) { return TrMail{lines}.words(); }
+long long dd_transport_err_word(long long lines) { return TrMail{lines}.err(); }
+
+int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui,
+                        const double* uj, double* out, double nu, long long lines, int sz,
+                        double* mail, double* mail_prev, double* mail_next,
+                        unsigned long long epoch, cudaStream_t s) {
+    TrDDArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.f1 = f1;
+    A.f2 = f2;
+    A.ui = ui;
+    A.uj = uj;
+    A.out = out;
+    A.nu = nu;
+    A.has_nu = nu != 0.0;
+    A.lines = lines;
+    A.rows = f1.rows;
+    A.sz = sz;
+    A.chunks = f1.chunks;
+    A.band = f1.Hb && f1.nb > 0 && (!A.has_nu || (f2.Hb && f2.nb > 0)) &&
+             !(getenv("TDS_BAND") && getenv("TDS_BAND")[0] == '0');
+    A.mail = mail;
+    A.mail_prev = mail_prev;
+    A.mail_next = mail_next;
+    A.epoch = epoch;
+    A.timeout_ns = 10ULL * 1000 * 1000 * 1000;
+    if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
+        A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
+    if (sz % 16 == 0 && A.chunks * 16 <= 512) {
+        if (sz == 32) return launch_dd_transport_t<16, 32>(A, s);
+        return launch_dd_transport_t<16, 0>(A, s);
+    }
+    return set_err(TDS_ERR_UNSUPPORTED, "fused distributed transport: sz % 16 and <= 32 chunks");
 }
 
 }  // namespace tds

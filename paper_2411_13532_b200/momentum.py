@@ -307,6 +307,19 @@ class SlabTransport:
             s2, st2 = _operator(2, self.h, n)
             self._rank = (DistD2Rank(s1, st1, self.part, ctx),
                           DistD2Rank(s2, st2, self.part, ctx) if self.nu != 0.0 else None)
+            # fused z terms (k_dd_transport): per-rank 16-row-chunk plans of
+            # both operators + one IPC mailbox set per field shape
+            from .distributed import Plan
+            import os
+            self._zfused = None
+            if os.environ.get("TDS_FUSED_TRANSPORT", "1") != "0":
+                r = ctx.rank_id
+                self._zfused = (
+                    Plan.create(s1, st1.c, self.part.local_sizes, r, N.TDS_FLAG_CHUNK16),
+                    Plan.create(s2, st2.c, self.part.local_sizes, r, N.TDS_FLAG_CHUNK16)
+                    if self.nu != 0.0 else None)
+            self._zmail = {}
+            self._zepoch = 0
 
     def local_slab(self, u3):
         """Pack this rank's slab of a global Cartesian (n, n, n) array for x."""
@@ -348,10 +361,37 @@ class SlabTransport:
             N.check(rc)
         return True
 
+    def _z_fused(self, comp, advect, out):
+        """The z term as one k_dd_transport launch per rank; False when the
+        plans / shape do not allow it (then three DistD2Rank solves)."""
+        from .rank import open_mailboxes
+        if not self._zfused:
+            return False
+        p1, p2 = self._zfused
+        groups, m, sz = comp.shape
+        key = (groups, sz)
+        mb = self._zmail.get(key)
+        if mb is None:
+            mb = open_mailboxes(self.ctx, N.lib().tds_transport_mailbox_words(groups, sz))
+            self._zmail[key] = mb
+        own, prev, nxt, _ = mb
+        self._zepoch += 1
+        rc = N.lib().tds_fused_transport(
+            p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
+            self.nu, groups, sz, own, prev, nxt, self._zepoch, _stream_handle())
+        if rc == N.TDS_ERR_UNSUPPORTED and self._zepoch == 1:
+            self._zfused = None        # same decision on every rank: plans / shape only
+            return False
+        N.check(rc)
+        self.ctx.exchange_rounds += 6
+        return True
+
     def _z_contribution(self, comp, advect, out):
         torch = _torch()
         if self._rank is None:
             _local_contribution(comp, advect, out, self.m, self.h, self.nu, False)
+            return
+        if self._z_fused(comp, advect, out):
             return
         r1, r2 = self._rank
         d_comp = r1.solve(comp)
@@ -411,11 +451,25 @@ class SlabTransport:
         for r in self._rank or ():
             if r is not None:
                 r.check()
+        for (groups, sz), (own, _, _, _) in getattr(self, "_zmail", {}).items():
+            err = ctypes.c_int(0)
+            N.check(N.lib().tds_transport_mailbox_error(own, groups, sz, ctypes.byref(err)))
+            if err.value:
+                raise TimeoutError(f"rank {self.ctx.rank_id}: fused transport timed out "
+                                   "waiting for a neighbour")
+
+    @property
+    def fused_z(self):
+        return bool(getattr(self, "_zfused", None))
 
     def close(self):
+        from .rank import close_mailboxes
         for r in self._rank or ():
             if r is not None:
                 r.close()
+        for mb in getattr(self, "_zmail", {}).values():
+            close_mailboxes(mb)
+        self._zmail = {}
 
 
 def euler_step(fields, dt, rank_count=1):

@@ -35,6 +35,40 @@ def _vp(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
+def open_mailboxes(ctx, words):
+    """Allocate this rank's sentinel-filled mailbox of `words` 8-byte slots,
+    exchange CUDA IPC handles over the rank group, and map prev's / next's
+    mailboxes: returns (own, prev, next, [mapped pointers])."""
+    import torch.distributed as dist
+    lib = N.lib()
+    own = ctypes.c_void_p()
+    handle = ctypes.create_string_buffer(64)
+    N.check(lib.tds_ipc_alloc(words * 8, ctypes.byref(own), handle))
+    handles = [None] * ctx.rank_count
+    dist.all_gather_object(handles, handle.raw, group=ctx.group)
+    opened = {}
+
+    def open_rank(pos):
+        pos %= ctx.rank_count
+        if pos not in opened:
+            ptr = ctypes.c_void_p()
+            N.check(lib.tds_ipc_open(handles[pos], ctypes.byref(ptr)))
+            opened[pos] = ptr
+        return opened[pos]
+
+    prev = open_rank(ctx.rank_id - 1) if ctx.has_prev else ctypes.c_void_p(0)
+    nxt = open_rank(ctx.rank_id + 1) if ctx.has_next else ctypes.c_void_p(0)
+    return own, prev, nxt, list(opened.values())
+
+
+def close_mailboxes(mb):
+    lib = N.lib()
+    own, _, _, opened = mb
+    for ptr in opened:
+        lib.tds_ipc_close(ptr)
+    lib.tds_ipc_free(own)
+
+
 class DistD2Rank:
     """Per-rank solver object: plan (coefficient tables on this GPU) and the
     neighbour buffers, reused across solves."""
@@ -80,32 +114,11 @@ class DistD2Rank:
     def _mailbox(self, groups, sz):
         """Own mailbox + the neighbours' mailboxes mapped through CUDA IPC
         (one collective handle exchange per field shape)."""
-        import torch.distributed as dist
         key = (groups, sz)
         mb = self._mail.get(key)
-        if mb is not None:
-            return mb
-        lib, ctx = N.lib(), self.ctx
-        words = lib.tds_mailbox_words(groups, sz)
-        own = ctypes.c_void_p()
-        handle = ctypes.create_string_buffer(64)
-        N.check(lib.tds_ipc_alloc(words * 8, ctypes.byref(own), handle))
-        handles = [None] * ctx.rank_count
-        dist.all_gather_object(handles, handle.raw, group=ctx.group)
-        opened = {}
-
-        def open_rank(pos):
-            pos %= ctx.rank_count
-            if pos not in opened:
-                ptr = ctypes.c_void_p()
-                N.check(lib.tds_ipc_open(handles[pos], ctypes.byref(ptr)))
-                opened[pos] = ptr
-            return opened[pos]
-
-        prev = open_rank(ctx.rank_id - 1) if ctx.has_prev else ctypes.c_void_p(0)
-        nxt = open_rank(ctx.rank_id + 1) if ctx.has_next else ctypes.c_void_p(0)
-        mb = (own, prev, nxt, list(opened.values()))
-        self._mail[key] = mb
+        if mb is None:
+            mb = open_mailboxes(self.ctx, N.lib().tds_mailbox_words(groups, sz))
+            self._mail[key] = mb
         return mb
 
     def check(self):
@@ -119,11 +132,8 @@ class DistD2Rank:
                                    "waiting for a neighbour")
 
     def close(self):
-        lib = N.lib()
-        for own, _, _, opened in self._mail.values():
-            for ptr in opened:
-                lib.tds_ipc_close(ptr)
-            lib.tds_ipc_free(own)
+        for mb in self._mail.values():
+            close_mailboxes(mb)
         self._mail = {}
 
     def solve(self, u, out=None):

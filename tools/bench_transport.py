@@ -65,7 +65,7 @@ def main():
         def step():
             return tr.rhs(*vel)
         pts_local = n * n * tr.m
-        what = f"SlabTransport z-slabs m={tr.m}, fused_z={bool(tr._rank and tr._rank[0].fused)}"
+        what = f"SlabTransport z-slabs m={tr.m}, fused_z_kernel={tr.fused_z}"
     else:
         u3, v3, w3 = (torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
                       for _ in range(3))
