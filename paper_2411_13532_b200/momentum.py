@@ -312,7 +312,14 @@ class SlabTransport:
             from .distributed import Plan
             import os
             self._zfused = None
-            if os.environ.get("TDS_FUSED_TRANSPORT", "1") != "0":
+            # equal blocks on every rank (identical persistent schedules), and
+            # m <= 256: measured faster than three k_dd2 solves + combine at
+            # m = 128 / 256 (2.99 -> 2.54, 5.55 -> 5.06 ms per z phase), slower
+            # at m = 512 (41.7 -> 45.2 ms: one CTA per SM cannot hide the three
+            # in-item neighbour waits). TDS_FUSED_TRANSPORT=0 / 2: never / always.
+            knob = os.environ.get("TDS_FUSED_TRANSPORT", "1")
+            if (knob != "0" and len(set(self.part.local_sizes)) == 1
+                    and (knob == "2" or self.m <= 256)):
                 r = ctx.rank_id
                 self._zfused = (
                     Plan.create(s1, st1.c, self.part.local_sizes, r, N.TDS_FLAG_CHUNK16),
