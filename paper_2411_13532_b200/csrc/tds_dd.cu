@@ -1086,11 +1086,17 @@ int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui
     A.timeout_ns = 10ULL * 1000 * 1000 * 1000;
     if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
         A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
-    if (sz % 16 == 0 && A.chunks * 16 <= 512) {
+    int tl = 16;
+    if (const char* e = getenv("TDS_TRANSPORT_TL")) tl = atoi(e) == 8 ? 8 : 16;
+    if (tl == 16 && sz % 16 == 0 && A.chunks * 16 <= 512) {
         if (sz == 32) return launch_dd_transport_t<16, 32>(A, s);
         return launch_dd_transport_t<16, 0>(A, s);
     }
-    return set_err(TDS_ERR_UNSUPPORTED, "fused distributed transport: sz % 16 and <= 32 chunks");
+    if (sz % 8 == 0 && A.chunks * 8 <= 512) {
+        if (sz == 32) return launch_dd_transport_t<8, 32>(A, s);
+        return launch_dd_transport_t<8, 0>(A, s);
+    }
+    return set_err(TDS_ERR_UNSUPPORTED, "fused distributed transport: sz % 8, tile <= 512 threads");
 }
 
 }  // namespace tds
