@@ -29,6 +29,8 @@ tds::FastArgs fast_args(const tds_plan* p, long long lines, int sz) {
     a.Hb = p->d_Hb;
     a.bq0 = p->d_bq0;
     a.nb = p->band_n;
+    a.g_n0 = p->g_n0 ? p->g_n0 : 2 * p->C;
+    a.g_n1 = p->g_n1 ? p->g_n1 : 2 * p->C;
     a.g = p->d_g;
     a.lines = lines;
     a.rows = p->block_rows;

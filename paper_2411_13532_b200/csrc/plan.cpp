@@ -432,6 +432,24 @@ int upload_H(tds_plan* p, const vector<double>& H, const vector<double>& gv) {
         if ((rc = upload(p, &p->d_Hb, Hb.data(), Hb.size()))) return rc;
         if ((rc = upload(p, &p->d_bq0, q0.data(), q0.size()))) return rc;
     }
+    // g0 / g1 (the rank's Alg. 6 rows d[0], d[m-1] as functionals of the
+    // chunk reduced rhs) decay away from their own end: keep the leading /
+    // trailing entries above 2^-70 of the largest (g_n0 / g_n1 terms)
+    if (!gv.empty()) {
+        const double rel = std::ldexp(1.0, -70);
+        double m0 = 0.0, m1 = 0.0;
+        for (int q = 0; q < K; ++q) {
+            m0 = std::max(m0, std::fabs(gv[q]));
+            m1 = std::max(m1, std::fabs(gv[K + q]));
+        }
+        int n0 = 0, n1 = 0;
+        for (int q = 0; q < K; ++q)
+            if (std::fabs(gv[q]) > rel * m0) n0 = q + 1;
+        for (int q = K - 1; q >= 0; --q)
+            if (std::fabs(gv[K + q]) > rel * m1) n1 = K - q;
+        p->g_n0 = n0;
+        p->g_n1 = n1;
+    }
     return upload(p, &p->d_g, gv.data(), gv.size());
 }
 

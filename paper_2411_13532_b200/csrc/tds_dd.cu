@@ -253,12 +253,8 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         // ROUND 2: the rank's decoupled boundary rows, 2x2 pairs, pins
         double* P = sP + (size_t)tl * 2 * TLT;
         if (valid && (first_chunk || last_chunk)) {
-            double g0y = 0.0, g1y = 0.0;
-            for (int q = 0; q < K; ++q) {
-                const double y = Y[q * TLT + lane];
-                if (first_chunk) g0y = fma(__ldg(p.g + q), y, g0y);
-                if (last_chunk) g1y = fma(__ldg(p.g + K + q), y, g1y);
-            }
+            const double g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
+            const double g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
             if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, g0y);
             if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, g1y);
             if (first_chunk) {
@@ -521,15 +517,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         if (!edge_warp) {
             // ROUND 2 posts of this item (helper warp): the rank's d[0] / d[m-1]
             if (wt == 1 && role < 2 && valid) {
-                const double* g = p.g + role * K;
-                double gy0 = 0.0, gy1 = 0.0;
-                int q = 0;
-                for (; q + 1 < K; q += 2) {
-                    gy0 = fma(__ldg(g + q), Y[q * TLT + lane], gy0);
-                    gy1 = fma(__ldg(g + q + 1), Y[(q + 1) * TLT + lane], gy1);
-                }
-                if (q < K) gy0 = fma(__ldg(g + q), Y[q * TLT + lane], gy0);
-                const double gy = gy0 + gy1;
+                const double gy = gdot<TLT>(p, role, Y, K, lane);
                 if (role == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
                 if (role == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
                 sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
@@ -541,9 +529,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             if (!helpers && valid && (first_chunk || last_chunk)) {
                 for (int r = 0; r < 2; ++r) {
                     if ((r == 0 && !first_chunk) || (r == 1 && !last_chunk)) continue;
-                    const double* g = p.g + r * K;
-                    double gy = 0.0;
-                    for (int q = 0; q < K; ++q) gy = fma(__ldg(g + q), Y[q * TLT + lane], gy);
+                    const double gy = gdot<TLT>(p, r, Y, K, lane);
                     if (r == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
                     if (r == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
                     sGY[(((size_t)(it & 1) * tpc + tl) * 2 + r) * TLT + lane] = gy;
@@ -950,12 +936,8 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
                                   nullptr, F, L);
             double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
             if (valid && (first_chunk || last_chunk)) {
-                double g0y = 0.0, g1y = 0.0;
-                for (int q = 0; q < K; ++q) {
-                    const double y = Y[q * TLT + lane];
-                    if (first_chunk) g0y = fma(__ldg(p.g + q), y, g0y);
-                    if (last_chunk) g1y = fma(__ldg(p.g + K + q), y, g1y);
-                }
+                const double g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
+                const double g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
                 if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
                 if (last_chunk && A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
                 if (first_chunk) {

@@ -245,6 +245,24 @@ __device__ __forceinline__ void band_bounds_nopins(const double2* __restrict__ h
     L = L0 + L1;
 }
 
+// The rank's Alg. 6 boundary row r (0: d[0] = g0 . Y, 1: d[m-1] = g1 . Y)
+// over its significant terms only (plan.cpp upload_H: g_n0 leading / g_n1
+// trailing entries above 2^-70 of the largest).
+template <int TLT>
+__device__ __forceinline__ double gdot(const FastArgs& p, int r, const double* Y, int K,
+                                       int lane) {
+    const double* g = p.g + r * K;
+    const int q0 = r == 0 ? 0 : K - p.g_n1, q1 = r == 0 ? p.g_n0 : K;
+    double a = 0.0, b = 0.0;
+    int q = q0;
+    for (; q + 1 < q1; q += 2) {
+        a = fma(__ldg(g + q), Y[q * TLT + lane], a);
+        b = fma(__ldg(g + q + 1), Y[(q + 1) * TLT + lane], b);
+    }
+    if (q < q1) a = fma(__ldg(g + q), Y[q * TLT + lane], a);
+    return a + b;
+}
+
 // Alg. 7 at chunk level + one streaming store per row.
 template <int M, bool UNIFORM>
 __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __restrict__ tb,

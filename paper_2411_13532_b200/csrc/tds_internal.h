@@ -57,6 +57,7 @@ struct FastArgs {
     const double2* Hb;     // banded Hp: C x nb pairs, columns bq0[k] + j (mod K)
     const int* bq0;
     int nb;
+    int g_n0, g_n1;        // g0 . Y over q < g_n0, g1 . Y over q >= K - g_n1
     const double* g;       // 2 x K pass-A functionals
     long long lines;
     long long items;       // work items of tiles_per_cta tiles (persistent kernels)
@@ -160,6 +161,7 @@ struct tds_plan {
     double2* d_Hb = nullptr;   // banded H: C x band_n, columns d_bq0[k] + j (mod K)
     int* d_bq0 = nullptr;
     int band_n = 0;
+    int g_n0 = 0, g_n1 = 0;   // significant leading / trailing terms of g0 / g1
     double* d_g = nullptr;
     double sa_first = 0, sc_last = 0, prev_sc_last = 0, next_sa_first = 0;
     double det_prev = 1, det_next = 1;

@@ -141,16 +141,8 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         __syncthreads();
 
         if (MODE == MODE_PASS_A) {
-            if (valid && chunk == 0) {
-                double s = 0.0;
-                for (int q = 0; q < K; ++q) s = fma(__ldg(p.g + q), Y[q * TLT + lane], s);
-                p.d_first_out[line] = s;
-            }
-            if (valid && chunk == C - 1) {
-                double s = 0.0;
-                for (int q = 0; q < K; ++q) s = fma(__ldg(p.g + K + q), Y[q * TLT + lane], s);
-                p.d_last_out[line] = s;
-            }
+            if (valid && chunk == 0) p.d_first_out[line] = gdot<TLT>(p, 0, Y, K, lane);
+            if (valid && chunk == C - 1) p.d_last_out[line] = gdot<TLT>(p, 1, Y, K, lane);
             continue;
         }
 
