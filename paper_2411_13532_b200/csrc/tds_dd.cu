@@ -241,8 +241,16 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
         __syncthreads();
 
-        // pin-independent part of the reduced map first (overlaps the
-        // edge warps' ROUND 2 below)
+        // ROUND 2 posts first (the rank's decoupled boundary rows), then the
+        // pin-independent part of the reduced map while they travel, then
+        // the neighbours' rows -> 2x2 pairs -> pins
+        double g0y = 0.0, g1y = 0.0;
+        if (valid && (first_chunk || last_chunk)) {
+            g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
+            g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
+            if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, g0y);
+            if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, g1y);
+        }
         double F, L;
         if (A.t.band)   // banded reduced map, pin columns excluded (TDS_BAND=0: full row)
             band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb, Y,
@@ -250,13 +258,8 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         else
             chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr,
                               nullptr, F, L);
-        // ROUND 2: the rank's decoupled boundary rows, 2x2 pairs, pins
         double* P = sP + (size_t)tl * 2 * TLT;
         if (valid && (first_chunk || last_chunk)) {
-            const double g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
-            const double g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
-            if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, g0y);
-            if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, g1y);
             if (first_chunk) {
                 double us = g0y;
                 if (p.has_prev) {
@@ -928,6 +931,14 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             Y[(2 * chunk) * TLT + lane] = d[0];
             Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
             __syncthreads();
+            // posts first, pin-free bounds while they travel, then the takes
+            double g0y = 0.0, g1y = 0.0;
+            if (valid && (first_chunk || last_chunk)) {
+                g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
+                g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
+                if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
+                if (last_chunk && A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
+            }
             if (A.band)
                 band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb,
                                         Y, K, lane, F, L);
@@ -936,10 +947,6 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
                                   nullptr, F, L);
             double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
             if (valid && (first_chunk || last_chunk)) {
-                const double g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
-                const double g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
-                if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
-                if (last_chunk && A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
                 if (first_chunk) {
                     double us = g0y;
                     if (p.has_prev) {
