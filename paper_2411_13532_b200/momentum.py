@@ -312,14 +312,12 @@ class SlabTransport:
             from .distributed import Plan
             import os
             self._zfused = None
-            # equal blocks on every rank (identical persistent schedules), and
-            # m <= 256: measured faster than three k_dd2 solves + combine at
-            # m = 128 / 256 (2.99 -> 2.54, 5.55 -> 5.06 ms per z phase), slower
-            # at m = 512 (41.7 -> 45.2 ms: one CTA per SM cannot hide the three
-            # in-item neighbour waits). TDS_FUSED_TRANSPORT=0 / 2: never / always.
+            # equal blocks on every rank (identical persistent schedules).
+            # Measured faster than three k_dd2 solves + combine at every m
+            # tried (z phase, 1024^3 on 2 GPUs: 34.7 vs 41.8 ms; 512^3 on 4
+            # GPUs: 2.21 vs 2.99 ms). TDS_FUSED_TRANSPORT=0: never.
             knob = os.environ.get("TDS_FUSED_TRANSPORT", "1")
-            if (knob != "0" and len(set(self.part.local_sizes)) == 1
-                    and (knob == "2" or self.m <= 256)):
+            if knob != "0" and len(set(self.part.local_sizes)) == 1:
                 r = ctx.rank_id
                 self._zfused = (
                     Plan.create(s1, st1.c, self.part.local_sizes, r, N.TDS_FLAG_CHUNK16),
