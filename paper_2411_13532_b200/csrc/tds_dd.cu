@@ -509,6 +509,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
         __syncthreads();
 
+        // ROUND 2 posts of this item first (helper warp): the rank's d[0] /
+        // d[m-1], on their way while the chunk boundary values are formed
+        if (!edge_warp && wt == 1 && role < 2 && valid) {
+            const double gy = gdot<TLT>(p, role, Y, K, lane);
+            if (role == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
+            if (role == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
+            sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
+        }
         // chunk boundary values without the rank pins
         double F, L;
         if (A.t.band)   // banded reduced map, pin columns excluded (TDS_BAND=0: full row)
@@ -518,13 +526,6 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr,
                               nullptr, F, L);
         if (!edge_warp) {
-            // ROUND 2 posts of this item (helper warp): the rank's d[0] / d[m-1]
-            if (wt == 1 && role < 2 && valid) {
-                const double gy = gdot<TLT>(p, role, Y, K, lane);
-                if (role == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
-                if (role == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
-                sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
-            }
             if (valid)
                 chunk_store<M, UNIFORM>(p, tb, p.out + line_base_t<SZC>(line, rows, p.sz), sz, r0, d, F,
                                         L, true);   // interior warps: never a special chunk
