@@ -86,7 +86,7 @@ def main():
     case("d1 periodic strict", lo, di, up, True, st, 1024, arith="strict", seed=5)
 
     # config 5: transport RHS on a z-slab decomposition (SlabTransport)
-    for nu, sz in ((0.02, 16), (0.0, 16), (0.01, 32)):
+    for nu, sz in ((0.02, 16), (0.0, 16), (0.01, 32), (0.01, 8)):
         n = 128
         rng = np.random.default_rng(77)
         u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
