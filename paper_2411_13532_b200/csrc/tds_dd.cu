@@ -926,19 +926,29 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
         };
         double acc[M], d[M];
         double F, L;
-        // one solve's chunk boundary values with the rank pins (ROUND 2)
-        auto bounds = [&](int s, const FastArgs& p) {
+        // Each solve: Y, ROUND 2 posts, and the pin-free chunk boundary values
+        // (F, L); the pins of all three solves are taken once at the end of
+        // the item and applied as a correction (x is affine in the pins:
+        // x_i += dx_i(dF, dL) with dF = h0.x us + hl.x ue, dL = h0.y us +
+        // hl.y ue), so the three neighbour round trips overlap the item.
+        auto post_bounds = [&](int s, const FastArgs& p) {
             double* Y = sY + (size_t)s * ybuf + (size_t)tl * K * TLT;
             Y[(2 * chunk) * TLT + lane] = d[0];
             Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
             __syncthreads();
-            // posts first, pin-free bounds while they travel, then the takes
-            double g0y = 0.0, g1y = 0.0;
+            double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
             if (valid && (first_chunk || last_chunk)) {
-                g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
-                g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
-                if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
-                if (last_chunk && A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
+                // own rows now (g0.Y / g1.Y); the pair solve comes at the end
+                if (first_chunk) {
+                    const double g0y = gdot<TLT>(p, 0, Y, K, lane);
+                    if (A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
+                    P[lane] = g0y;
+                }
+                if (last_chunk) {
+                    const double g1y = gdot<TLT>(p, 1, Y, K, lane);
+                    if (A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
+                    P[TLT + lane] = g1y;
+                }
             }
             if (A.band)
                 band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb,
@@ -946,52 +956,61 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             else
                 chunk_bounds<TLT>(p.Hp + (size_t)chunk * K + 1, Y + TLT, K - 2, lane, nullptr,
                                   nullptr, F, L);
+        };
+        // the neighbours' rows of solve s -> 2x2 pairs -> pins in P (edge threads)
+        auto take_pins = [&](int s, const FastArgs& p) {
             double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
-            if (valid && (first_chunk || last_chunk)) {
-                if (first_chunk) {
-                    double us = g0y;
-                    if (p.has_prev) {
-                        const double prev_last = take(A.mail + par + mb.dp(s) + line, A, err);
-                        us = (g0y - p.sa_first * prev_last) / p.det_prev;
-                    }
-                    P[lane] = us;
-                }
-                if (last_chunk) {
-                    double ue = g1y;
-                    if (p.has_next) {
-                        const double next_first = take(A.mail + par + mb.dn(s) + line, A, err);
-                        ue = (g1y - p.sc_last * next_first) / p.det_next;
-                    }
-                    P[TLT + lane] = ue;
-                }
+            if (!valid) return;
+            if (first_chunk && p.has_prev) {
+                const double prev_last = take(A.mail + par + mb.dp(s) + line, A, err);
+                P[lane] = (P[lane] - p.sa_first * prev_last) / p.det_prev;
             }
-            __syncthreads();
+            if (last_chunk && p.has_next) {
+                const double next_first = take(A.mail + par + mb.dn(s) + line, A, err);
+                P[TLT + lane] = (P[TLT + lane] - p.sc_last * next_first) / p.det_next;
+            }
+        };
+        // pin correction of solve s, scaled by w (and by u_j for solve A)
+        auto correct = [&](int s, const FastArgs& p, const UniformTable& T, double w, bool by_uj) {
+            const double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
             const double2 h0 = __ldg(p.Hp + (size_t)chunk * K);
             const double2 hl = __ldg(p.Hp + (size_t)chunk * K + K - 1);
             const double us = P[lane], ue = P[TLT + lane];
-            F = fma(h0.x, us, fma(hl.x, ue, F));
-            L = fma(h0.y, us, fma(hl.y, ue, L));
+            const double dF = fma(h0.x, us, hl.x * ue), dL = fma(h0.y, us, hl.y * ue);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double dx = i == 0 ? dF : (i == M - 1 ? dL : -fma(T.sc[i], dL, T.sa[i] * dF));
+                if (by_uj) dx *= Tj[base + (i + 2) * TLT];
+                acc[i] = fma(w, dx, acc[i]);
+            }
         };
 
-        // (A) d(u_i) -> acc = u_j * du_i
+        // (A) d(u_i) -> acc = u_j * du_i   (pin-free part)
         tr_sweeps<M>(T1, wi, d);
-        bounds(0, A.f1);
+        post_bounds(0, A.f1);
 #pragma unroll
         for (int i = 0; i < M; ++i) acc[i] = Tj[base + (i + 2) * TLT] * tr_subst(T1, i, M, F, L, d[i]);
         // (B) d(u_j u_i) -> acc = -1/2 (acc + dprod)
         tr_sweeps<M>(T1, [&](int i) { return wj(i) * wi(i); }, d);
-        if (!A.has_nu) release(nxt);
-        bounds(1, A.f1);
+        post_bounds(1, A.f1);
 #pragma unroll
         for (int i = 0; i < M; ++i) acc[i] = -0.5 * (acc[i] + tr_subst(T1, i, M, F, L, d[i]));
         // (C) acc += nu d2(u_i)
         if (A.has_nu) {
             tr_sweeps<M>(T2, wi, d);
-            release(nxt);
-            bounds(2, A.f2);
+            post_bounds(2, A.f2);
 #pragma unroll
             for (int i = 0; i < M; ++i) acc[i] = fma(A.nu, tr_subst(T2, i, M, F, L, d[i]), acc[i]);
         }
+        // the three solves' pins (one wait point) and their corrections
+        take_pins(0, A.f1);
+        take_pins(1, A.f1);
+        if (A.has_nu) take_pins(2, A.f2);
+        __syncthreads();
+        correct(0, A.f1, T1, -0.5, true);
+        correct(1, A.f1, T1, -0.5, false);
+        if (A.has_nu) correct(2, A.f2, T2, A.nu, false);
+        release(nxt);             // tiles consumed (u_j rows of the A correction)
         if (valid) {
             double* ob = A.out + line_base_t<SZC>(line, rows, A.sz) + (long long)r0 * sz;
 #pragma unroll
