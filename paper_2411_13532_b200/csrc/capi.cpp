@@ -367,9 +367,11 @@ extern "C" int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const
     int rc = check_field(d1, groups, sz);
     if (rc) return rc;
     if (!u_i || !u_j || !out || !mail) return set_err(TDS_ERR_INVALID, "null argument");
+    // C >= 2: the kernel's edge threads hold either the first or the last
+    // chunk of a block, never both
     auto ok = [&](const tds_plan* p) {
         return p->rank >= 0 && p->P >= 2 && p->path == TDS_PATH_FAST && p->M == 16 &&
-               p->uniform && !p->special_first && !p->special_last;
+               p->C >= 2 && p->uniform && !p->special_first && !p->special_last;
     };
     if (!ok(d1) || (nu != 0.0 && (!d2 || !ok(d2) || d2->C != d1->C || d2->rank != d1->rank ||
                                   d2->block_rows != d1->block_rows)))

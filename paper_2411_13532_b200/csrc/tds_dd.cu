@@ -893,25 +893,29 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
         const long long hb = valid ? halo_base_t<SZC>(line, A.sz) : 0;
         const bool hlo = valid && first_chunk && A.mail_prev;
         const bool hhi = valid && last_chunk && A.mail_next;
+        // halo slots of this item: the four loads in flight together, across
+        // the TMA wait (a serial take() each would put four L2 round trips
+        // on the edge threads' critical path)
+        double* hs = A.mail + par + (hlo ? mb.hlo_i() : mb.hhi_i()) + hb;
+        double* hsj = A.mail + par + (hlo ? mb.hlo_j() : mb.hhi_j()) + hb;
+        unsigned long long s0 = SENTINEL, s1 = SENTINEL, s2 = SENTINEL, s3 = SENTINEL;
+        if (hlo || hhi) {
+            s0 = ld_sys_u64(hs);
+            s1 = ld_sys_u64(hs + sz);
+            s2 = ld_sys_u64(hsj);
+            s3 = ld_sys_u64(hsj + sz);
+        }
         while (!mbar_try_wait(bar, phase)) {
         }
         phase ^= 1u;
         // rank-edge halos of u_i and u_j (ROUND 1 of this item)
         double hi0 = 0.0, hi1 = 0.0, hi2 = 0.0, hi3 = 0.0;
         double hj0 = 0.0, hj1 = 0.0, hj2 = 0.0, hj3 = 0.0;
-        if (hlo) {
-            double* m = A.mail + par;
-            hi0 = take(m + mb.hlo_i() + hb, A, err);
-            hi1 = take(m + mb.hlo_i() + hb + sz, A, err);
-            hj0 = take(m + mb.hlo_j() + hb, A, err);
-            hj1 = take(m + mb.hlo_j() + hb + sz, A, err);
-        }
-        if (hhi) {
-            double* m = A.mail + par;
-            hi2 = take(m + mb.hhi_i() + hb, A, err);
-            hi3 = take(m + mb.hhi_i() + hb + sz, A, err);
-            hj2 = take(m + mb.hhi_j() + hb, A, err);
-            hj3 = take(m + mb.hhi_j() + hb + sz, A, err);
+        if (hlo || hhi) {
+            const double a0 = take_v(hs, s0, A, err), a1 = take_v(hs + sz, s1, A, err);
+            const double b0 = take_v(hsj, s2, A, err), b1 = take_v(hsj + sz, s3, A, err);
+            if (hlo) { hi0 = a0; hi1 = a1; hj0 = b0; hj1 = b1; }
+            else { hi2 = a0; hi3 = a1; hj2 = b0; hj3 = b1; }
         }
         // window row i (= block row r0 - 2 + i) of u_i / u_j
         auto wi = [&](int i) {
@@ -958,17 +962,21 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
                                   nullptr, F, L);
         };
         // the neighbours' rows of solve s -> 2x2 pairs -> pins in P (edge threads)
-        auto take_pins = [&](int s, const FastArgs& p) {
+        auto take_pins = [&](int s, const FastArgs& p, unsigned long long v) {
             double* P = sP + ((size_t)s * tpc + tl) * 2 * TLT;
             if (!valid) return;
             if (first_chunk && p.has_prev) {
-                const double prev_last = take(A.mail + par + mb.dp(s) + line, A, err);
+                const double prev_last = take_v(A.mail + par + mb.dp(s) + line, v, A, err);
                 P[lane] = (P[lane] - p.sa_first * prev_last) / p.det_prev;
             }
             if (last_chunk && p.has_next) {
-                const double next_first = take(A.mail + par + mb.dn(s) + line, A, err);
+                const double next_first = take_v(A.mail + par + mb.dn(s) + line, v, A, err);
                 P[TLT + lane] = (P[TLT + lane] - p.sc_last * next_first) / p.det_next;
             }
+        };
+        // the pin slot this thread reads for solve s (edge threads), loaded early
+        auto pin_slot = [&](int s) -> double* {
+            return A.mail + par + (first_chunk ? mb.dp(s) : mb.dn(s)) + line;
         };
         // pin correction of solve s, scaled by w (and by u_j for solve A)
         auto correct = [&](int s, const FastArgs& p, const UniformTable& T, double w, bool by_uj) {
@@ -1002,10 +1010,17 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
 #pragma unroll
             for (int i = 0; i < M; ++i) acc[i] = fma(A.nu, tr_subst(T2, i, M, F, L, d[i]), acc[i]);
         }
-        // the three solves' pins (one wait point) and their corrections
-        take_pins(0, A.f1);
-        take_pins(1, A.f1);
-        if (A.has_nu) take_pins(2, A.f2);
+        // the three solves' pins (one wait point: the slot loads in flight
+        // together) and their corrections
+        unsigned long long v0 = SENTINEL, v1 = SENTINEL, v2 = SENTINEL;
+        if (valid && ((first_chunk && A.f1.has_prev) || (last_chunk && A.f1.has_next))) {
+            v0 = ld_sys_u64(pin_slot(0));
+            v1 = ld_sys_u64(pin_slot(1));
+            if (A.has_nu) v2 = ld_sys_u64(pin_slot(2));
+        }
+        take_pins(0, A.f1, v0);
+        take_pins(1, A.f1, v1);
+        if (A.has_nu) take_pins(2, A.f2, v2);
         __syncthreads();
         correct(0, A.f1, T1, -0.5, true);
         correct(1, A.f1, T1, -0.5, false);
