@@ -7,7 +7,9 @@
  * would bind (ctypes stub in INTEGRATION.md). Every function:
  *   - takes plain pointers and sizes (no torch types);
  *   - takes DEVICE pointers for field data, owned by the caller;
- *   - takes an explicit cudaStream_t (passed as void*), never synchronises;
+ *   - takes an explicit cudaStream_t (passed as void*) and never synchronises
+ *     the host with the device, except the functions marked SYNCHRONOUS
+ *     (plan creation / destruction, IPC setup, tds_mailbox_error);
  *   - returns 0 (TDS_OK) or a TDS_ERR_* code; tds_last_error() gives text.
  * All error conditions the reference raises (SingularPivot, SingularPair,
  * SingularCorrection, ValueError) are coefficient-only and are raised by
@@ -25,7 +27,7 @@
 extern "C" {
 #endif
 
-#define TDS_ABI_VERSION 1
+#define TDS_ABI_VERSION 2
 
 #define TDS_OK 0
 #define TDS_ERR_INVALID 1             /* ValueError (shape/partition/size)  */
@@ -108,9 +110,11 @@ int tds_plan_rank_coeffs(const tds_plan* plan, int k, double* s_a, double* s_c,
  * a[0] couples to the row before the block, c[m-1] to the row after it.
  * Outputs host arrays of length m, bit-identical to the reference; s_c[0]
  * and s_a[m-1] are zeroed and their signed values returned in dropped[2]. */
+/* pivot_floor: |pivot| <= pivot_floor raises SingularPivot (reference
+ * default 1e-300, distributed.py:144). */
 int tds_preprocess(const double* a, const double* b, const double* c, int m,
-                   double* s_a, double* s_c, double* w, double* f, double* r,
-                   double* dropped);
+                   double pivot_floor, double* s_a, double* s_c, double* w, double* f,
+                   double* r, double* dropped);
 
 /*
  * Whole-operator solve (rank == -1 plans): out = A^{-1} stencil(u) with the
@@ -150,26 +154,48 @@ int tds_finish(const tds_plan* plan, const double* u, const double* halo_lo,
  * One kernel per rank does the whole distd2_solve (distributed.py:327-366):
  * both neighbour rounds are peer stores into the neighbours' MAILBOXES,
  * fence-free (sentinel-armed slots). A mailbox is tds_mailbox_words(groups,
- * sz) 8-byte words filled with 0xFF bytes (tds_ipc_alloc does this);
- * neighbours map it with CUDA IPC.
+ * sz) 8-byte words prepared by tds_mailbox_init (tds_ipc_alloc does this);
+ * neighbours map it with CUDA IPC (one process per GPU) or use the pointer
+ * directly (several ranks in one process: same device, or peer access
+ * enabled with tds_peer_access).
  * `epoch` must increase by one per solve (same value on every rank). All
- * ranks must have the same block size. Waits time out after 10 s and set
- * the mailbox error word (tds_mailbox_error) instead of hanging. */
+ * ranks must have the same block size and the same `max_ctas`: the kernel is
+ * persistent and every rank must run the same schedule. max_ctas == 0 uses
+ * the device's resident capacity, max_ctas > 0 caps it, max_ctas = -k uses
+ * capacity / k: ranks SHARING a device (k of them at most on any device)
+ * must split it so that all of them are co-resident. A wait that exceeds 10 s (TDS_FUSED_TIMEOUT_MS) sets the
+ * mailbox error word and yields NaN instead of hanging.
+ * The last three words of every mailbox are STATUS words: [0] error
+ * (1 = timeout), [1] / [2] cumulative halo / boundary-row words this rank
+ * posted to its neighbours (measured message accounting). */
 long long tds_mailbox_words(long long groups, int sz);
+int tds_mailbox_init(double* mail, long long words, void* stream);
+/* async copy of the three status words into host memory (pinned for true
+ * asynchrony); `words` is the mailbox length */
+int tds_mailbox_status(const double* mail, long long words, unsigned long long* host_status,
+                       void* stream);
 int tds_fused_eligible(const tds_plan* plan, long long groups, int sz);
 int tds_fused_solve(const tds_plan* plan, const double* u, double* out,
                     long long groups, int sz, double* mail, double* mail_prev,
-                    double* mail_next, unsigned long long epoch, void* stream);
+                    double* mail_next, unsigned long long epoch, int max_ctas, void* stream);
+/* SYNCHRONOUS convenience: *err = 1 if the mailbox recorded a timeout */
 int tds_mailbox_error(const double* mail, long long groups, int sz, int* err);
-/* CUDA IPC plumbing for mailboxes: handle is 64 bytes (cudaIpcMemHandle_t) */
+/* CUDA IPC plumbing for mailboxes: handle is 64 bytes (cudaIpcMemHandle_t).
+ * tds_ipc_alloc prepares the mailbox (tds_mailbox_init) and synchronises
+ * before returning the handle. */
 int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle);
 int tds_ipc_open(const unsigned char* handle, void** ptr);
 int tds_ipc_close(void* ptr);
 int tds_ipc_free(void* ptr);
+/* enable access from the current device to peer_device (no-op if equal or
+ * already enabled); TDS_ERR_UNSUPPORTED if the pair has no P2P path */
+int tds_peer_access(int peer_device);
 
 /* ---- phase-level kernels, reference arithmetic (bit-identical) ----------
  * Position-major (rows, lanes) device arrays, as the reference phase
- * functions take them. Coefficients are host arrays (copied per call). */
+ * functions take them. Coefficient arrays (stencil m x 5, w, f, r, s_a, s_c
+ * of length m) are DEVICE arrays too: no allocation, copy or host
+ * synchronisation per call. */
 /* decouple_fused: u_ext (m+4, lanes) -> d (m, lanes); distributed.py:257-276 */
 int tds_decouple_fused(const double* u_ext, const double* stencil, const double* w,
                        const double* f, const double* r, double* d, int m,
@@ -183,10 +209,12 @@ int tds_boundary_pair(const double* d_last, const double* d_first, double s_c_la
                       double s_a_first, double* u_last, double* u_first,
                       long long lanes, void* stream);
 /* thomas_solve / periodic_thomas_solve (serial.py:26-90) on a (groups, n, sz)
- * field; an RhsBatch (m, n) is groups = m, sz = 1. */
+ * field; an RhsBatch (m, n) is groups = m, sz = 1. Bands are host arrays;
+ * the multipliers are built once per (operator, pivot_floor, device) and
+ * cached, so repeated calls allocate and copy nothing. */
 int tds_thomas(const double* lower, const double* diag, const double* upper,
                int periodic, const double* rhs, double* out, int n,
-               long long groups, int sz, void* stream);
+               long long groups, int sz, double pivot_floor, void* stream);
 
 /* ---- momentum-transport RHS (momentum.py:102-169) ------------------------
  * One (component i, direction j) contribution of the skew-symmetric
@@ -206,8 +234,8 @@ int tds_transport_combine(const double* u_j, const double* du, const double* dp,
  * (one rank per GPU; SlabTransport's z terms): out = -1/2 (u_j d(u_i) +
  * d(u_j u_i)) + nu d2(u_i) on this rank's (groups, m, sz) block, the three
  * DistD2 solves fused in one kernel with their neighbour rounds done over
- * IPC-mapped mailboxes (tds_transport_mailbox_words words each, sentinel
- * filled by tds_ipc_alloc). d1 / d2: this rank's d/dx and d2/dx2 plans with
+ * IPC-mapped mailboxes (tds_transport_mailbox_words words each, prepared by
+ * tds_mailbox_init; same status words and max_ctas rule as tds_fused_solve). d1 / d2: this rank's d/dx and d2/dx2 plans with
  * 16-row chunks (TDS_FLAG_CHUNK16). Replaces directional_contribution
  * (momentum.py:102-126) with run_distd2 over the rank chain.
  * TDS_ERR_UNSUPPORTED when the plans / field do not allow it. */
@@ -216,7 +244,7 @@ int tds_transport_mailbox_error(const double* mail, long long groups, int sz, in
 int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const double* u_i,
                         const double* u_j, double* out, double nu, long long groups, int sz,
                         double* mail, double* mail_prev, double* mail_next,
-                        unsigned long long epoch, void* stream);
+                        unsigned long long epoch, int max_ctas, void* stream);
 
 /* acc += the (i, dir) contribution, dir = 1 (y) or 2 (z), for an
  * (nx, ny, nz) block with everything in the x layout (groups = ny nz/sz, nx,

@@ -17,6 +17,7 @@ _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "li
 _lib = None
 _lock = threading.Lock()
 
+ABI_VERSION = 2
 TDS_OK = 0
 TDS_ERR_INVALID = 1
 TDS_ERR_SINGULAR_PIVOT = 2
@@ -59,18 +60,21 @@ SIGNATURES = {
     "tds_plan_destroy": (_I, [_P]),
     "tds_plan_query": (_I, [_P, ctypes.POINTER(PlanInfo)]),
     "tds_plan_rank_coeffs": (_I, [_P, _I, _DP, _DP, _DP, _DP, _DP, _DP]),
-    "tds_preprocess": (_I, [_DP, _DP, _DP, _I, _DP, _DP, _DP, _DP, _DP, _DP]),
+    "tds_preprocess": (_I, [_DP, _DP, _DP, _I, _D, _DP, _DP, _DP, _DP, _DP, _DP]),
     "tds_solve": (_I, [_P, _P, _P, _LL, _I, _P]),
     "tds_halo_rows": (_I, [_P, _P, _P, _P, _LL, _I, _P]),
     "tds_boundary_rows": (_I, [_P, _P, _P, _P, _P, _P, _P, _LL, _I, _P]),
     "tds_finish": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _LL, _I, _P]),
-    "tds_decouple_fused": (_I, [_P, _DP, _DP, _DP, _DP, _P, _I, _LL, _P]),
-    "tds_substitute": (_I, [_P, _DP, _DP, _P, _P, _P, _I, _LL, _P]),
+    "tds_decouple_fused": (_I, [_P, _P, _P, _P, _P, _P, _I, _LL, _P]),
+    "tds_substitute": (_I, [_P, _P, _P, _P, _P, _P, _I, _LL, _P]),
     "tds_boundary_pair": (_I, [_P, _P, _D, _D, _P, _P, _LL, _P]),
-    "tds_thomas": (_I, [_DP, _DP, _DP, _I, _P, _P, _I, _LL, _I, _P]),
+    "tds_thomas": (_I, [_DP, _DP, _DP, _I, _P, _P, _I, _LL, _I, _D, _P]),
     "tds_mailbox_words": (_LL, [_LL, _I]),
     "tds_fused_eligible": (_I, [_P, _LL, _I]),
-    "tds_fused_solve": (_I, [_P, _P, _P, _LL, _I, _P, _P, _P, ctypes.c_ulonglong, _P]),
+    "tds_mailbox_init": (_I, [_P, _LL, _P]),
+    "tds_mailbox_status": (_I, [_P, _LL, _P, _P]),
+    "tds_peer_access": (_I, [_I]),
+    "tds_fused_solve": (_I, [_P, _P, _P, _LL, _I, _P, _P, _P, ctypes.c_ulonglong, _I, _P]),
     "tds_mailbox_error": (_I, [_P, _LL, _I, _IP]),
     "tds_ipc_alloc": (_I, [_LL, ctypes.POINTER(_P), ctypes.c_char_p]),
     "tds_ipc_open": (_I, [ctypes.c_char_p, ctypes.POINTER(_P)]),
@@ -83,7 +87,7 @@ SIGNATURES = {
     "tds_transport_mailbox_words": (_LL, [_LL, _I]),
     "tds_transport_mailbox_error": (_I, [_P, _LL, _I, ctypes.POINTER(_I)]),
     "tds_fused_transport": (_I, [_P, _P, _P, _P, _P, _D, _LL, _I, _P, _P, _P,
-                                 ctypes.c_ulonglong, _P]),
+                                 ctypes.c_ulonglong, _I, _P]),
     "tds_reorder3": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "tds_pack": (_I, [_P, _P, _I, _I, _I, _I, _I, _LL, _P]),
     "tds_unpack": (_I, [_P, _P, _I, _I, _I, _I, _I, _LL, _P]),
@@ -111,7 +115,7 @@ def lib():
                 fn = getattr(h, name)
                 fn.restype = res
                 fn.argtypes = args
-            if h.tds_abi_version() != 1:
+            if h.tds_abi_version() != ABI_VERSION:
                 raise RuntimeError("libtds_b200.so ABI version mismatch")
             _lib = h
     return _lib

@@ -139,7 +139,7 @@ def _solver_fn(a, sys, n):
             N.check(N.lib().tds_thomas(N.dptr(lo), N.dptr(di), N.dptr(up), int(sys.periodic),
                                        ctypes.c_void_p(f.data_ptr()),
                                        ctypes.c_void_p(out.data_ptr()), n, f.shape[0],
-                                       f.shape[2], _stream_handle()))
+                                       f.shape[2], T.distributed.PIVOT_FLOOR, _stream_handle()))
             return out
         return thomas
     part = T.SubdomainPartition.balanced(n, a.ranks)

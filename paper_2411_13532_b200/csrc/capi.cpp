@@ -199,40 +199,18 @@ extern "C" int tds_decouple_fused(const double* u_ext, const double* stencil, co
                                   const double* f, const double* r, double* d, int m,
                                   long long lanes, void* stream) {
     if (m < 4) return set_err(TDS_ERR_INVALID, "local block needs at least 4 rows");
-    cudaStream_t s = S(stream);
-    double* buf = nullptr;
-    size_t mm = size_t(m);
-    int rc = scratch_alloc(&buf, mm * 8, s);
-    if (rc) return rc;
-    double *dst = buf, *dw = buf + 5 * mm, *df = buf + 6 * mm, *dr = buf + 7 * mm;
-    rc = tds::cuda_check(cudaMemcpyAsync(dst, stencil, 5 * mm * sizeof(double),
-                                         cudaMemcpyHostToDevice, s), "copy stencil");
-    if (!rc) rc = tds::cuda_check(cudaMemcpyAsync(dw, w, mm * 8, cudaMemcpyHostToDevice, s), "copy w");
-    if (!rc) rc = tds::cuda_check(cudaMemcpyAsync(df, f, mm * 8, cudaMemcpyHostToDevice, s), "copy f");
-    if (!rc) rc = tds::cuda_check(cudaMemcpyAsync(dr, r, mm * 8, cudaMemcpyHostToDevice, s), "copy r");
-    if (!rc) rc = tds::launch_decouple_pm(u_ext, dst, dw, df, dr, d, m, lanes, s);
-    // host arrays may be released once the copies are done
-    cudaStreamSynchronize(s);
-    cudaFreeAsync(buf, s);
-    return rc;
+    if (lanes > 0 && (!u_ext || !stencil || !w || !f || !r || !d))
+        return set_err(TDS_ERR_INVALID, "null argument");
+    return tds::launch_decouple_pm(u_ext, stencil, w, f, r, d, m, lanes, S(stream));
 }
 
 extern "C" int tds_substitute(const double* d, const double* s_a, const double* s_c,
                               const double* u_start, const double* u_end, double* out, int m,
                               long long lanes, void* stream) {
     if (m < 4) return set_err(TDS_ERR_INVALID, "local block needs at least 4 rows");
-    cudaStream_t s = S(stream);
-    double* buf = nullptr;
-    int rc = scratch_alloc(&buf, size_t(2) * m, s);
-    if (rc) return rc;
-    rc = tds::cuda_check(cudaMemcpyAsync(buf, s_a, size_t(m) * 8, cudaMemcpyHostToDevice, s), "copy s_a");
-    if (!rc)
-        rc = tds::cuda_check(cudaMemcpyAsync(buf + m, s_c, size_t(m) * 8, cudaMemcpyHostToDevice, s),
-                             "copy s_c");
-    if (!rc) rc = tds::launch_substitute_pm(d, buf, buf + m, u_start, u_end, out, m, lanes, s);
-    cudaStreamSynchronize(s);
-    cudaFreeAsync(buf, s);
-    return rc;
+    if (lanes > 0 && (!d || !s_a || !s_c || !u_start || !u_end || !out))
+        return set_err(TDS_ERR_INVALID, "null argument");
+    return tds::launch_substitute_pm(d, s_a, s_c, u_start, u_end, out, m, lanes, S(stream));
 }
 
 extern "C" int tds_boundary_pair(const double* d_last, const double* d_first, double s_c_last,
@@ -248,25 +226,27 @@ extern "C" int tds_boundary_pair(const double* d_last, const double* d_first, do
                             S(stream));
 }
 
+namespace tds {
+int thomas_plan(const double* lower, const double* diag, const double* upper, int periodic, int n,
+                double pivot_floor, const tds_plan** out);
+}
+
 extern "C" int tds_thomas(const double* lower, const double* diag, const double* upper,
                           int periodic, const double* rhs, double* out, int n, long long groups,
-                          int sz, void* stream) {
+                          int sz, double pivot_floor, void* stream) {
     // A P=1 staged plan over a (groups, n, sz) field with the identity
-    // stencil (its zero weights never see the halo). RhsBatch (m, n) is the
-    // case groups=m, sz=1.
-    int one = n;
-    tds_plan* p = nullptr;
-    int rc = tds_plan_create(lower, diag, upper, periodic, nullptr, n, &one, 1, -1,
-                             TDS_FLAG_STAGED, &p);
+    // stencil (its zero weights never see the halo), cached per operator and
+    // device (plan.cpp thomas_plan): no allocation or copy per call. RhsBatch
+    // (m, n) is the case groups=m, sz=1.
+    if (groups < 0 || sz < 1) return set_err(TDS_ERR_INVALID, "bad field shape");
+    const tds_plan* p = nullptr;
+    int rc = tds::thomas_plan(lower, diag, upper, periodic, n, pivot_floor, &p);
     if (rc) return rc;
     tds::StagedArgs a = staged_args(p, groups * sz, sz);
     a.u = rhs;
     a.out = out;
     a.edge_mode = tds::EDGE_ZERO;
-    rc = tds::launch_thomas(a, S(stream));
-    cudaStreamSynchronize(S(stream));
-    tds_plan_destroy(p);
-    return rc;
+    return tds::launch_thomas(a, S(stream));
 }
 
 static int pack_common(const double* src, double* dst, int nx, int ny, int nz, int sz,
@@ -295,7 +275,7 @@ namespace tds {
 long long dd_mail_words(long long lines);
 bool dd_eligible(int M, const FastArgs& a);
 int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
-              double* mail_next, unsigned long long epoch, long long tiles, cudaStream_t s);
+              double* mail_next, unsigned long long epoch, int max_ctas, cudaStream_t s);
 }  // namespace tds
 
 extern "C" long long tds_mailbox_words(long long groups, int sz) {
@@ -311,7 +291,7 @@ extern "C" int tds_fused_eligible(const tds_plan* p, long long groups, int sz) {
 
 extern "C" int tds_fused_solve(const tds_plan* p, const double* u, double* out, long long groups,
                                int sz, double* mail, double* mail_prev, double* mail_next,
-                               unsigned long long epoch, void* stream) {
+                               unsigned long long epoch, int max_ctas, void* stream) {
     int rc = check_field(p, groups, sz);
     if (rc) return rc;
     if (p->rank < 0 || p->P < 2 || p->path != TDS_PATH_FAST)
@@ -326,16 +306,55 @@ extern "C" int tds_fused_solve(const tds_plan* p, const double* u, double* out, 
     if (!tds::dd_eligible(p->M, a))
         return set_err(TDS_ERR_UNSUPPORTED, "field not eligible for the fused kernel");
     return tds::launch_dd(p->M, p->uniform, a, mail, p->has_prev ? mail_prev : nullptr,
-                          p->has_next ? mail_next : nullptr, epoch, tiles_of(lines), S(stream));
+                          p->has_next ? mail_next : nullptr, epoch, max_ctas, S(stream));
+}
+
+static int read_status(const double* mail, long long words, int* err) {
+    if (!mail || words < 3 || !err) return set_err(TDS_ERR_INVALID, "null argument");
+    unsigned long long v = 0;
+    int rc = tds::cuda_check(cudaMemcpy(&v, mail + (words - 3), 8, cudaMemcpyDeviceToHost),
+                             "read mailbox error word");
+    *err = (v == 1ULL) ? 1 : 0;   // ERR_TIMEOUT
+    return rc;
 }
 
 extern "C" int tds_mailbox_error(const double* mail, long long groups, int sz, int* err) {
-    long long words = tds::dd_mail_words(groups * sz);
-    unsigned long long v = 0;
-    int rc = tds::cuda_check(cudaMemcpy(&v, mail + (words - 1), 8, cudaMemcpyDeviceToHost),
-                             "read mailbox error word");
-    *err = (v == 1ULL) ? 1 : 0;   // ERR_TIMEOUT (sentinel fill = no error)
+    return read_status(mail, tds::dd_mail_words(groups * sz), err);
+}
+
+extern "C" int tds_mailbox_init(double* mail, long long words, void* stream) {
+    if (!mail || words < 3) return set_err(TDS_ERR_INVALID, "bad mailbox");
+    cudaStream_t s = S(stream);
+    int rc = tds::cuda_check(cudaMemsetAsync(mail, 0xFF, size_t(words) * 8, s),
+                             "cudaMemsetAsync(mailbox)");   // sentinel fill
+    if (!rc)
+        rc = tds::cuda_check(cudaMemsetAsync(mail + (words - 3), 0, 3 * 8, s),
+                             "cudaMemsetAsync(mailbox status)");
     return rc;
+}
+
+extern "C" int tds_mailbox_status(const double* mail, long long words,
+                                  unsigned long long* host_status, void* stream) {
+    if (!mail || words < 3 || !host_status) return set_err(TDS_ERR_INVALID, "null argument");
+    return tds::cuda_check(cudaMemcpyAsync(host_status, mail + (words - 3), 3 * 8,
+                                           cudaMemcpyDeviceToHost, S(stream)),
+                           "copy mailbox status");
+}
+
+extern "C" int tds_peer_access(int peer_device) {
+    int dev = 0;
+    int rc = tds::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc || peer_device == dev) return rc;
+    int can = 0;
+    rc = tds::cuda_check(cudaDeviceCanAccessPeer(&can, dev, peer_device), "cudaDeviceCanAccessPeer");
+    if (rc) return rc;
+    if (!can) return set_err(TDS_ERR_UNSUPPORTED, "no peer access between the devices");
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return TDS_OK;
+    }
+    return tds::cuda_check(e, "cudaDeviceEnablePeerAccess");
 }
 
 namespace tds {
@@ -343,7 +362,7 @@ long long dd_transport_mail_words(long long lines);
 int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui,
                         const double* uj, double* out, double nu, long long lines, int sz,
                         double* mail, double* mail_prev, double* mail_next,
-                        unsigned long long epoch, cudaStream_t s);
+                        unsigned long long epoch, int max_ctas, cudaStream_t s);
 }  // namespace tds
 
 extern "C" long long tds_transport_mailbox_words(long long groups, int sz) {
@@ -352,18 +371,13 @@ extern "C" long long tds_transport_mailbox_words(long long groups, int sz) {
 
 extern "C" int tds_transport_mailbox_error(const double* mail, long long groups, int sz,
                                            int* err) {
-    long long words = tds::dd_transport_mail_words(groups * sz);
-    unsigned long long v = 0;
-    int rc = tds::cuda_check(cudaMemcpy(&v, mail + (words - 1), 8, cudaMemcpyDeviceToHost),
-                             "read transport mailbox error word");
-    *err = (v == 1ULL) ? 1 : 0;
-    return rc;
+    return read_status(mail, tds::dd_transport_mail_words(groups * sz), err);
 }
 
 extern "C" int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const double* u_i,
                                    const double* u_j, double* out, double nu, long long groups,
                                    int sz, double* mail, double* mail_prev, double* mail_next,
-                                   unsigned long long epoch, void* stream) {
+                                   unsigned long long epoch, int max_ctas, void* stream) {
     int rc = check_field(d1, groups, sz);
     if (rc) return rc;
     if (!u_i || !u_j || !out || !mail) return set_err(TDS_ERR_INVALID, "null argument");
@@ -387,13 +401,17 @@ extern "C" int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const
     tds::FastArgs f2 = nu != 0.0 ? fast_args(d2, lines, sz) : f1;
     return tds::launch_dd_transport(f1, f2, u_i, u_j, out, nu, lines, sz, mail,
                                     d1->has_prev ? mail_prev : nullptr,
-                                    d1->has_next ? mail_next : nullptr, epoch, S(stream));
+                                    d1->has_next ? mail_next : nullptr, epoch, max_ctas,
+                                    S(stream));
 }
 
 extern "C" int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle) {
     int rc = tds::cuda_check(cudaMalloc(ptr, size_t(bytes)), "cudaMalloc(mailbox)");
     if (rc) return rc;
-    rc = tds::cuda_check(cudaMemset(*ptr, 0xFF, size_t(bytes)), "cudaMemset(mailbox)");   // sentinel fill
+    // sentinel fill + zeroed status words, complete BEFORE the handle is
+    // shared: a neighbour may post as soon as it can map the mailbox
+    rc = tds_mailbox_init(static_cast<double*>(*ptr), bytes / 8, nullptr);
+    if (!rc) rc = tds::cuda_check(cudaDeviceSynchronize(), "mailbox fill");
     if (rc) return rc;
     cudaIpcMemHandle_t h;
     rc = tds::cuda_check(cudaIpcGetMemHandle(&h, *ptr), "cudaIpcGetMemHandle");

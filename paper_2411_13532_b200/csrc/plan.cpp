@@ -62,7 +62,7 @@ std::string fmt(const char* f, double v) {
 // row before the block, c[m-1] to the row after it. Same operation order as
 // the reference; the two couplings it discards are returned in drop_*.
 int preprocess_block(const double* a, const double* b, const double* c, int m,
-                     tds_rank_coeffs& co, int rank) {
+                     tds_rank_coeffs& co, int rank, double pivot_floor = tds::PIVOT_FLOOR) {
     if (m < 4)
         return set_err(TDS_ERR_INVALID,
                        "local block needs at least 4 rows, got " + std::to_string(m), rank);
@@ -85,7 +85,7 @@ int preprocess_block(const double* a, const double* b, const double* c, int m,
     }
     for (int j = 2; j < m; ++j) {
         double den = b[j] - a[j] * sc[j - 1];
-        if (std::fabs(den) <= tds::PIVOT_FLOOR)
+        if (std::fabs(den) <= pivot_floor)
             return set_err(TDS_ERR_SINGULAR_PIVOT,
                            fmt("pivot %.3e at local row ", den) + std::to_string(j + 1), rank);
         f[j] = 1.0 / den;
@@ -99,7 +99,7 @@ int preprocess_block(const double* a, const double* b, const double* c, int m,
         sc[j] = -sc[j] * sc[j + 1];
     }
     double clo = 1.0 - sc[0] * sa[1];
-    if (std::fabs(clo) <= tds::PIVOT_FLOOR)
+    if (std::fabs(clo) <= pivot_floor)
         return set_err(TDS_ERR_SINGULAR_PIVOT, fmt("closure pivot %.3e", clo), rank);
     f[0] = 1.0 / clo;
     sa[0] = f[0] * sa[0];
@@ -620,6 +620,14 @@ extern "C" int tds_plan_create_local(const double* a, const double* b, const dou
 extern "C" int tds_plan_create(const double* lower, const double* diag, const double* upper,
                                int periodic, const double* stencil, int n, const int* sizes_in,
                                int P, int rank, int flags, tds_plan** out) {
+    return tds::plan_create_impl(lower, diag, upper, periodic, stencil, n, sizes_in, P, rank,
+                                 flags, tds::PIVOT_FLOOR, out);
+}
+
+namespace tds {
+int plan_create_impl(const double* lower, const double* diag, const double* upper, int periodic,
+                     const double* stencil, int n, const int* sizes_in, int P, int rank,
+                     int flags, double pivot_floor, tds_plan** out) {
     if (!out) return set_err(TDS_ERR_INVALID, "null plan output");
     *out = nullptr;
     if (!lower || !diag || !upper) return set_err(TDS_ERR_INVALID, "null band pointer");
@@ -642,6 +650,7 @@ extern "C" int tds_plan_create(const double* lower, const double* diag, const do
 
     const Global g = make_global(lower, diag, upper, periodic != 0, stencil, n);
     tds_plan* p = new_plan(n, g.periodic, P, rank, flags);
+    p->pivot_floor = pivot_floor;
     p->sizes = sizes;
     p->offs = offs;
     p->margin = margin_of(g);
@@ -794,7 +803,7 @@ extern "C" int tds_plan_create(const double* lower, const double* diag, const do
     cp[0] = lc[0] / lb[0];
     for (int i = 1; i < n; ++i) {
         double den = lb[i] - la[i] * cp[i - 1];
-        if (std::fabs(den) <= tds::PIVOT_FLOOR)
+        if (std::fabs(den) <= p->pivot_floor)
             return fail(set_err(TDS_ERR_SINGULAR_PIVOT,
                                 fmt("pivot %.3e at row ", den) + std::to_string(i + 1)));
         w[i] = 1.0 / den;
@@ -813,7 +822,7 @@ extern "C" int tds_plan_create(const double* lower, const double* diag, const do
         for (int i = n - 2; i >= 0; --i) z[i] -= cp[i] * z[i + 1];
         double ql = la[0] / gamma;
         double den = 1.0 + 1.0 * z[0] + ql * z[n - 1];
-        if (std::fabs(den) <= tds::PIVOT_FLOOR)
+        if (std::fabs(den) <= p->pivot_floor)
             return fail(set_err(TDS_ERR_SINGULAR_CORRECTION, fmt("correction denominator %.3e", den)));
         p->th_qlast = ql;
         p->th_den = den;
@@ -825,6 +834,8 @@ extern "C" int tds_plan_create(const double* lower, const double* diag, const do
     *out = p;
     return TDS_OK;
 }
+
+}  // namespace tds
 
 extern "C" int tds_plan_query(const tds_plan* p, tds_plan_info* info) {
     if (!p || !info) return set_err(TDS_ERR_INVALID, "null argument");
@@ -860,12 +871,12 @@ extern "C" int tds_plan_rank_coeffs(const tds_plan* p, int k, double* sa, double
 }
 
 extern "C" int tds_preprocess(const double* a, const double* b, const double* c, int m,
-                              double* sa, double* sc, double* w, double* f, double* r,
-                              double* dropped) {
+                              double pivot_floor, double* sa, double* sc, double* w, double* f,
+                              double* r, double* dropped) {
     if (!a || !b || !c || !sa || !sc || !w || !f || !r || !dropped)
         return set_err(TDS_ERR_INVALID, "null argument");
     tds_rank_coeffs co;
-    int rc = preprocess_block(a, b, c, m, co, -1);
+    int rc = preprocess_block(a, b, c, m, co, -1, pivot_floor);
     if (rc) return rc;
     co.sc[0] = 0.0;
     co.sa[m - 1] = 0.0;
@@ -878,3 +889,69 @@ extern "C" int tds_preprocess(const double* a, const double* b, const double* c,
     dropped[1] = co.drop_last;
     return TDS_OK;
 }
+
+// ---------------------------------------------------------------- Thomas plans
+// tds_thomas's P=1 staged plans, cached per (device, operator, pivot floor):
+// the ABI call then allocates and copies nothing (reference serial.py:26-90).
+#include <deque>
+#include <mutex>
+
+namespace {
+struct ThomasKey {
+    int dev, n, periodic;
+    double floor;
+    vector<double> bands;   // lower | diag | upper
+    bool operator==(const ThomasKey& o) const {
+        return dev == o.dev && n == o.n && periodic == o.periodic && floor == o.floor &&
+               std::memcmp(bands.data(), o.bands.data(), bands.size() * sizeof(double)) == 0;
+    }
+};
+std::mutex g_thomas_mu;
+std::deque<std::pair<ThomasKey, tds_plan*>> g_thomas;   // most recent first
+constexpr size_t THOMAS_CACHE = 16;
+}  // namespace
+
+namespace tds {
+int plan_create_impl(const double* lower, const double* diag, const double* upper, int periodic,
+                     const double* stencil, int n, const int* sizes_in, int P, int rank,
+                     int flags, double pivot_floor, tds_plan** out);
+
+int thomas_plan(const double* lower, const double* diag, const double* upper, int periodic, int n,
+                double pivot_floor, const tds_plan** out) {
+    if (!lower || !diag || !upper || !out) return set_err(TDS_ERR_INVALID, "null argument");
+    if (n < 3) return set_err(TDS_ERR_INVALID, "system size must be at least 3");
+    ThomasKey key;
+    if (cudaGetDevice(&key.dev) != cudaSuccess) return cuda_check(cudaGetLastError(), "cudaGetDevice");
+    key.n = n;
+    key.periodic = periodic != 0;
+    key.floor = pivot_floor;
+    key.bands.reserve(size_t(3) * n);
+    key.bands.insert(key.bands.end(), lower, lower + n);
+    key.bands.insert(key.bands.end(), diag, diag + n);
+    key.bands.insert(key.bands.end(), upper, upper + n);
+    std::lock_guard<std::mutex> lock(g_thomas_mu);
+    for (size_t i = 0; i < g_thomas.size(); ++i)
+        if (g_thomas[i].first.bands.size() == key.bands.size() && g_thomas[i].first == key) {
+            auto hit = g_thomas[i];
+            g_thomas.erase(g_thomas.begin() + i);
+            g_thomas.push_front(hit);
+            *out = hit.second;
+            return TDS_OK;
+        }
+    int one = n;
+    tds_plan* p = nullptr;
+    int rc = plan_create_impl(lower, diag, upper, periodic, nullptr, n, &one, 1, -1,
+                              TDS_FLAG_STAGED, pivot_floor, &p);
+    if (rc) return rc;
+    if (g_thomas.size() >= THOMAS_CACHE) {
+        // evicted plans may still be in use by queued kernels: synchronise
+        // their device before freeing (cache misses only)
+        cudaDeviceSynchronize();
+        tds_plan_destroy(g_thomas.back().second);
+        g_thomas.pop_back();
+    }
+    g_thomas.emplace_front(std::move(key), p);
+    *out = p;
+    return TDS_OK;
+}
+}  // namespace tds

@@ -37,10 +37,14 @@ struct DDArgs {
     double* mail_next;     // next rank's mailbox
     unsigned long long epoch;
     unsigned long long timeout_ns;
+    int max_ctas;          // host-side grid cap (0: resident capacity)
 };
 
 // Mailbox layout (8-byte words), L = lines. Two parity halves (epoch & 1)
-// of 6L value slots each, then one error word:
+// of 6L value slots each, then three STATUS words (not sentinel slots;
+// tds_mailbox_init zeroes them): the error word and the cumulative counts of
+// halo / boundary words this rank has posted to its neighbours (the measured
+// message accounting of transport.py:45-48,71-80):
 //   D_FROM_PREV [L]  prev's d[m-1] per line      D_FROM_NEXT [L]  next's d[0]
 //   H_LO [2L]  prev's last two rows (G,2,sz)     H_HI [2L]  next's first two rows
 // A slot holds either the SENTINEL bit pattern (all ones: the byte-uniform
@@ -58,11 +62,12 @@ struct Mail {
     __host__ __device__ long long h_lo() const { return 2 * L; }
     __host__ __device__ long long h_hi() const { return 4 * L; }
     __host__ __device__ long long err() const { return 12 * L; }
-    __host__ __device__ long long words() const { return 12 * L + 1; }
+    __host__ __device__ long long words() const { return 12 * L + 3; }
 };
 
 constexpr unsigned long long SENTINEL = ~0ULL;
 constexpr unsigned long long ERR_TIMEOUT = 1ULL;
+constexpr int STATUS_WORDS = 3;   // error, halo words posted, boundary words posted
 
 namespace {
 
@@ -95,7 +100,8 @@ __device__ double take_v(double* slot, unsigned long long v, const Args& A,
             if (*reinterpret_cast<volatile unsigned long long*>(err) == ERR_TIMEOUT ||
                 globaltimer() - t0 > A.timeout_ns) {
                 atomicExch(err, ERR_TIMEOUT);
-                return 0.0;
+                // poison: a timed-out solve must not look like a result
+                return __longlong_as_double(0x7FF8000000000000LL);
             }
         }
     }
@@ -105,6 +111,16 @@ __device__ double take_v(double* slot, unsigned long long v, const Args& A,
 template <class Args>
 __device__ __forceinline__ double take(double* slot, const Args& A, unsigned long long* err) {
     return take_v(slot, SENTINEL, A, err);
+}
+// add this warp's posted-word counts to the rank's own status words
+// (err + 1: halo words, err + 2: boundary words); one atomic per warp
+__device__ __forceinline__ void flush_counts(unsigned long long* err, unsigned nh, unsigned nb) {
+    const unsigned mask = __activemask();
+    const unsigned a = __reduce_add_sync(mask, nh), b = __reduce_add_sync(mask, nb);
+    if ((threadIdx.x & 31) == __ffs(mask) - 1) {
+        if (a) atomicAdd(err + 1, (unsigned long long)a);
+        if (b) atomicAdd(err + 2, (unsigned long long)b);
+    }
 }
 
 }  // namespace
@@ -150,6 +166,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
                             l0, b * A.t.boxr, g);
         }
     };
+    unsigned nh = 0, nbw = 0;   // words posted (halo / boundary rows)
     // ROUND 1 for `item`: my first two rows -> prev's high halo, my last two
     // rows -> next's low halo (read straight from my block in HBM)
     auto publish_halo = [&](long long item) {
@@ -161,12 +178,14 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
             post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
+            nh += 2;
         }
         if (last_chunk && A.mail_next) {
             const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
             const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
             post(A.mail_next + par + mb.h_lo() + hb, a0);
             post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
+            nh += 2;
         }
     };
 
@@ -248,8 +267,14 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         if (valid && (first_chunk || last_chunk)) {
             g0y = first_chunk ? gdot<TLT>(p, 0, Y, K, lane) : 0.0;
             g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
-            if (first_chunk && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, g0y);
-            if (last_chunk && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, g1y);
+            if (first_chunk && A.mail_prev) {
+                post(A.mail_prev + par + mb.d_from_next() + line, g0y);
+                ++nbw;
+            }
+            if (last_chunk && A.mail_next) {
+                post(A.mail_next + par + mb.d_from_prev() + line, g1y);
+                ++nbw;
+            }
         }
         double F, L;
         if (A.t.band)   // banded reduced map, pin columns excluded (TDS_BAND=0: full row)
@@ -290,6 +315,7 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             chunk_store_any<M, TAB>(p, tb, p.out + line_base_t<SZC>(line, rows, p.sz), sz, r0, d, F, L,
                                         A.t.store_cs != 0, chunk);
     }
+    flush_counts(err, nh, nbw);
 }
 
 // ---------------------------------------------------------------------------
@@ -358,6 +384,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                             l0, b * A.t.boxr, g);
         }
     };
+    unsigned nh = 0, nbw = 0;   // words posted (halo / boundary rows)
     auto publish_halo = [&](long long item) {
         if (!halo_lo_poster && !halo_hi_poster) return;
         const long long ln = (item * tpc + tl) * TLT + lane;
@@ -368,12 +395,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
             post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
+            nh += 2;
         }
         if (halo_hi_poster && A.mail_next) {
             const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
             const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
             post(A.mail_next + par + mb.h_lo() + hb, a0);
             post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
+            nh += 2;
         }
     };
     auto edge_finish = [&](const EdgeTable& T, double* ob, double F, double L) {
@@ -513,8 +542,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         // d[m-1], on their way while the chunk boundary values are formed
         if (!edge_warp && wt == 1 && role < 2 && valid) {
             const double gy = gdot<TLT>(p, role, Y, K, lane);
-            if (role == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
-            if (role == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
+            if (role == 0 && A.mail_prev) {
+                post(A.mail_prev + par + mb.d_from_next() + line, gy);
+                ++nbw;
+            }
+            if (role == 1 && A.mail_next) {
+                post(A.mail_next + par + mb.d_from_prev() + line, gy);
+                ++nbw;
+            }
             sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
         }
         // chunk boundary values without the rank pins
@@ -534,8 +569,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                 for (int r = 0; r < 2; ++r) {
                     if ((r == 0 && !first_chunk) || (r == 1 && !last_chunk)) continue;
                     const double gy = gdot<TLT>(p, r, Y, K, lane);
-                    if (r == 0 && A.mail_prev) post(A.mail_prev + par + mb.d_from_next() + line, gy);
-                    if (r == 1 && A.mail_next) post(A.mail_next + par + mb.d_from_prev() + line, gy);
+                    if (r == 0 && A.mail_prev) {
+                        post(A.mail_prev + par + mb.d_from_next() + line, gy);
+                        ++nbw;
+                    }
+                    if (r == 1 && A.mail_next) {
+                        post(A.mail_next + par + mb.d_from_prev() + line, gy);
+                        ++nbw;
+                    }
                     sGY[(((size_t)(it & 1) * tpc + tl) * 2 + r) * TLT + lane] = gy;
                 }
             }
@@ -553,6 +594,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         __syncthreads();   // the helper warp's g.Y of the last item
         if (edge_warp) finish(prev_item, (it - 1) & 1);
     }
+    flush_counts(err, nh, nbw);
 }
 
 namespace {
@@ -574,24 +616,13 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     A.t.store_cs = store_policy();
     const int threads = cfg.tpc * a.chunks * TLT;
     const size_t smem = dd_smem(a, cfg);
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_dd<M, UNI, TLT, SZC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        "cudaFuncSetAttribute(k_dd)");
-        if (rc) return rc;
-        smem_set = smem;
-    }
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd<M, UNI, TLT, SZC>, threads, smem);
-    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
-    // exactly the resident capacity: every CTA is co-resident (no waits on
-    // unscheduled CTAs); identical on every rank
-    long long grid = (long long)nb * sms;
-    if (grid > a.items) grid = a.items;
+    const void* fn = reinterpret_cast<const void*>(k_dd<M, UNI, TLT, SZC>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd)"))) return rc;
+    // at most the resident capacity (every CTA co-resident: no wait on an
+    // unscheduled CTA), capped by max_ctas when several ranks share a device;
+    // identical on every rank
+    const long long grid = persistent_grid(fn, threads, smem, a.items, A.max_ctas);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
     k_dd<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd launch");
 }
@@ -614,22 +645,10 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     if (rc) return rc;
     const int threads = cfg.tpc * a.chunks * TLT;
     const size_t smem = dd2_smem(a, cfg, M);
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_dd2<M, UNI, TLT, SZC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        "cudaFuncSetAttribute(k_dd2)");
-        if (rc) return rc;
-        smem_set = smem;
-    }
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd2<M, UNI, TLT, SZC>, threads, smem);
-    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
-    long long grid = (long long)nb * sms;
-    if (grid > a.items) grid = a.items;
+    const void* fn = reinterpret_cast<const void*>(k_dd2<M, UNI, TLT, SZC>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd2)"))) return rc;
+    const long long grid = persistent_grid(fn, threads, smem, a.items, A.max_ctas);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
     k_dd2<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd2 launch");
 }
@@ -682,8 +701,10 @@ bool dd_eligible(int M, const FastArgs& a) {
 }
 
 int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
-              double* mail_next, unsigned long long epoch, long long /*tiles*/, cudaStream_t s) {
+              double* mail_next, unsigned long long epoch, int max_ctas, cudaStream_t s) {
     DDArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.max_ctas = max_ctas;
     A.t.f = a;
     A.mail = mail;
     A.mail_prev = mail_prev;
@@ -737,7 +758,7 @@ struct TrMail {
     __host__ __device__ long long hhi_i() const { return 10 * L; }
     __host__ __device__ long long hhi_j() const { return 12 * L; }
     __host__ __device__ long long err() const { return 28 * L; }
-    __host__ __device__ long long words() const { return 28 * L + 1; }
+    __host__ __device__ long long words() const { return 28 * L + 3; }   // + status words
 };
 
 struct TrDDArgs {
@@ -758,6 +779,7 @@ struct TrDDArgs {
     double* mail_next;
     unsigned long long epoch;
     unsigned long long timeout_ns;
+    int max_ctas;
 };
 
 namespace {
@@ -837,6 +859,7 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             }
         }
     };
+    unsigned nh = 0, nbw = 0;   // words posted (halo / boundary rows)
     // ROUND 1 of `item`: first two rows of u_i, u_j -> prev, last two -> next
     auto publish_halo = [&](long long item) {
         if (!first_chunk && !last_chunk) return;
@@ -852,6 +875,7 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             post(m + mb.hhi_i() + hb + sz, __ldg(bi + sz));
             post(m + mb.hhi_j() + hb, __ldg(bj));
             post(m + mb.hhi_j() + hb + sz, __ldg(bj + sz));
+            nh += 4;
         }
         if (last_chunk && A.mail_next) {
             double* m = A.mail_next + par;
@@ -860,6 +884,7 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             post(m + mb.hlo_i() + hb + sz, __ldg(bi + b));
             post(m + mb.hlo_j() + hb, __ldg(bj + a));
             post(m + mb.hlo_j() + hb + sz, __ldg(bj + b));
+            nh += 4;
         }
     };
     auto release = [&](long long nxt) {
@@ -945,12 +970,18 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
                 // own rows now (g0.Y / g1.Y); the pair solve comes at the end
                 if (first_chunk) {
                     const double g0y = gdot<TLT>(p, 0, Y, K, lane);
-                    if (A.mail_prev) post(A.mail_prev + par + mb.dn(s) + line, g0y);
+                    if (A.mail_prev) {
+                        post(A.mail_prev + par + mb.dn(s) + line, g0y);
+                        ++nbw;
+                    }
                     P[lane] = g0y;
                 }
                 if (last_chunk) {
                     const double g1y = gdot<TLT>(p, 1, Y, K, lane);
-                    if (A.mail_next) post(A.mail_next + par + mb.dp(s) + line, g1y);
+                    if (A.mail_next) {
+                        post(A.mail_next + par + mb.dp(s) + line, g1y);
+                        ++nbw;
+                    }
                     P[TLT + lane] = g1y;
                 }
             }
@@ -1032,6 +1063,7 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
         }
     }
+    flush_counts(err, nh, nbw);
 }
 
 namespace {
@@ -1059,22 +1091,11 @@ int launch_dd_transport_t(const TrDDArgs& A0, cudaStream_t s) {
                             (2 * (size_t)A.rows * TLT + 3 * (size_t)2 * A.chunks * TLT +
                              3 * 2 * TLT) * sizeof(double) +
                         2 * sizeof(UniformTable) + 16;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_dd_transport<TLT, SZC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        "cudaFuncSetAttribute(k_dd_transport)");
-        if (rc) return rc;
-        smem_set = smem;
-    }
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dd_transport<TLT, SZC>, threads, smem);
-    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport does not fit on an SM");
-    long long grid = (long long)nb * sms;   // co-resident, identical on every rank
-    if (grid > A.items) grid = A.items;
+    const void* fn = reinterpret_cast<const void*>(k_dd_transport<TLT, SZC>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd_transport)"))) return rc;
+    // co-resident, identical on every rank (max_ctas: ranks sharing a device)
+    const long long grid = persistent_grid(fn, threads, smem, A.items, A.max_ctas);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport does not fit on an SM");
     k_dd_transport<TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd_transport launch");
 }
@@ -1087,9 +1108,10 @@ long long dd_transport_err_word(long long lines) { return TrMail{lines}.err(); }
 int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui,
                         const double* uj, double* out, double nu, long long lines, int sz,
                         double* mail, double* mail_prev, double* mail_next,
-                        unsigned long long epoch, cudaStream_t s) {
+                        unsigned long long epoch, int max_ctas, cudaStream_t s) {
     TrDDArgs A;
     std::memset(&A, 0, sizeof(A));
+    A.max_ctas = max_ctas;
     A.f1 = f1;
     A.f2 = f2;
     A.ui = ui;

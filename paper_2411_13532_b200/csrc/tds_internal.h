@@ -132,6 +132,14 @@ int cuda_check(cudaError_t e, const char* what);
 
 }  // namespace tds
 
+struct tds_plan;
+namespace tds {
+// tds_plan_create with an explicit pivot floor (plan.cpp)
+int plan_create_impl(const double* lower, const double* diag, const double* upper, int periodic,
+                     const double* stencil, int n, const int* sizes_in, int P, int rank,
+                     int flags, double pivot_floor, tds_plan** out);
+}  // namespace tds
+
 // Rank-level DistD2 coefficients (distributed.py:43-68), dropped couplings kept.
 struct tds_rank_coeffs {
     std::vector<double> sa, sc, w, f, r;   // sc[0], sa[m-1] zeroed as the reference
@@ -144,6 +152,7 @@ struct tds_plan {
     int P = 1;
     int rank = -1;
     int flags = 0;
+    double pivot_floor = tds::PIVOT_FLOOR;   // P=1 Thomas tables (serial.py:26-90)
     int path = TDS_PATH_STAGED;
     int block_off = 0, block_rows = 0;   // rows of the global line held here
     std::vector<int> sizes, offs;

@@ -19,6 +19,9 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "tds_device.cuh"
 #include "tds_tma.h"
@@ -180,22 +183,10 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     A.tab_smem = UNI == TAB_GLOBAL && smem + tab_bytes <= 227 * 1024 &&
                  !(getenv("TDS_TAB_SMEM") && getenv("TDS_TAB_SMEM")[0] == '0');
     if (A.tab_smem) smem += tab_bytes;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_tma<M, MODE, UNI, TLT, SZC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        "cudaFuncSetAttribute(k_tma)");
-        if (rc) return rc;
-        smem_set = smem;
-    }
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tma<M, MODE, UNI, TLT, SZC>, threads, smem);
-    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_tma does not fit on an SM");
-    long long grid = (long long)nb * sms;
-    if (grid > A.f.items) grid = A.f.items;
+    const void* fn = reinterpret_cast<const void*>(k_tma<M, MODE, UNI, TLT, SZC>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_tma)"))) return rc;
+    const long long grid = persistent_grid(fn, threads, smem, A.f.items, 0);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_tma does not fit on an SM");
     k_tma<M, MODE, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_tma launch");
 }
@@ -228,6 +219,34 @@ int launch_tma_m(const FastArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+int ensure_smem(const void* fn, size_t smem, const char* what) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check(cudaGetLastError(), what);
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = done[{fn, dev}];
+    if (smem <= cur) return TDS_OK;
+    int rc = cuda_check(
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), what);
+    if (!rc) cur = smem;
+    return rc;
+}
+
+long long persistent_grid(const void* fn, int threads, size_t smem, long long items,
+                          int max_ctas) {
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem);
+    if (nb < 1) return 0;
+    long long grid = (long long)nb * sms;
+    if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+    if (max_ctas < 0) grid = grid / -(long long)max_ctas > 0 ? grid / -(long long)max_ctas : 1;
+    if (grid > items) grid = items;
+    return grid;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

@@ -30,5 +30,13 @@ int box_rows(int rows, int M);
 int store_policy();
 // 3-D tensor map (lanes, rows, groups) over the field a.u; box tl x boxr x 1
 int encode_field_map(const FastArgs& a, int M, int tl, CUtensorMap* map, int* boxr);
+// cudaFuncAttributeMaxDynamicSharedMemorySize of `fn` raised to >= smem on
+// the CURRENT device (the attribute is per device context; cached per
+// (function, device), thread-safe)
+int ensure_smem(const void* fn, size_t smem, const char* what);
+// persistent grid: resident CTAs x SMs of the current device, capped by
+// `items` and (if > 0) by max_ctas; 0 if the kernel does not fit an SM
+long long persistent_grid(const void* fn, int threads, size_t smem, long long items,
+                          int max_ctas);
 
 }  // namespace tds

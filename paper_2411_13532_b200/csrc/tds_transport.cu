@@ -526,23 +526,10 @@ int launch_transport_tma_t(const TransportArgs& a, cudaStream_t s) {
     const size_t smem = (size_t)A.p.tiles_per_cta *
                             (2 * (size_t)a.rows * TLT + 3 * (size_t)2 * a.chunks * TLT) *
                             sizeof(double) + 2 * sizeof(UniformTable) + 16;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        rc = cuda_check(cudaFuncSetAttribute(k_transport_tma<M, TLT, GEOM, SZC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        "cudaFuncSetAttribute(k_transport_tma)");
-        if (rc) return rc;
-        smem_set = smem;
-    }
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_transport_tma<M, TLT, GEOM, SZC>, threads,
-                                                  smem);
-    if (nb < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_tma does not fit on an SM");
-    long long grid = (long long)nb * sms;
-    if (grid > A.items) grid = A.items;
+    const void* fn = reinterpret_cast<const void*>(k_transport_tma<M, TLT, GEOM, SZC>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_transport_tma)"))) return rc;
+    const long long grid = persistent_grid(fn, threads, smem, A.items, 0);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_tma does not fit on an SM");
     k_transport_tma<M, TLT, GEOM, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_transport_tma launch");
 }

@@ -121,15 +121,13 @@ def preprocess(local_sys, position, cyclic, pivot_floor=PIVOT_FLOOR, warn_not_do
     m = local_sys.n
     if m < 4:
         raise ValueError(f"local block needs at least 4 rows, got {m}")
-    if pivot_floor != PIVOT_FLOOR:
-        raise ValueError("the native plan builder uses the reference pivot floor 1e-300")
     if warn_not_dominant and not is_diagonally_dominant(local_sys):
         warnings.warn("local block is not strictly diagonally dominant",
                       NotDominantWarning, stacklevel=2)
     a, b, c = (N.f64(x) for x in (local_sys.lower, local_sys.diag, local_sys.upper))
     out = [np.empty(m) for _ in range(5)]
     dropped = np.empty(2)
-    N.check(N.lib().tds_preprocess(N.dptr(a), N.dptr(b), N.dptr(c), m,
+    N.check(N.lib().tds_preprocess(N.dptr(a), N.dptr(b), N.dptr(c), m, float(pivot_floor),
                                    *[N.dptr(o) for o in out], N.dptr(dropped)))
     sa, sc, w, f, r = out
     return DistCoeffs(sa, sc, w, f, r, m, bool(cyclic), position,
@@ -291,15 +289,114 @@ def get_plan(sys, stencil, part, rank=-1, arithmetic="fast", chunk_rows=None):
 
 # ------------------------------------------------------------- operator
 
-def _audit_counts(part, periodic, groups, sz):
-    """Message accounting of the reference protocol (transport.py:66-80,
-    distributed.py:308-366): per directed edge one scalar share, one halo
-    (groups, 2, sz) and one boundary row (groups, sz) message."""
-    p = part.rank_count
-    edges = 2 * p if periodic else 2 * (p - 1)
-    msgs = 3 * edges
-    nbytes = edges * (8 + groups * HALO_DEPTH * sz * 8 + groups * sz * 8)
-    return msgs, nbytes
+class _RankGroup:
+    """P DistD2 ranks of one operator inside this process: one
+    LocalRankContext + DistD2Rank per rank, each on its device with its own
+    stream (several ranks may share a device; transport.spawn_ranks). The
+    per-rank kernels and neighbour rounds are the ones a torchrun rank runs
+    (rank.py): the fused k_dd / k_dd2 exchange through device mailboxes
+    (NVLink peer stores between B200s), the two-pass path through the
+    contexts' device-to-device messages. Replaces the reference's threaded
+    run_distd2 body (distributed.py:417-441)."""
+
+    def __init__(self, sys, stencil, part, devices, arithmetic, warn_not_dominant):
+        from .rank import DistD2Rank
+        from .transport import make_contexts, run_on
+        self.part = part
+        self.contexts = make_contexts(part.rank_count, sys.periodic, devices)
+        self.ranks = run_on(self.contexts, lambda ctx: DistD2Rank(
+            sys, stencil, part, ctx, arithmetic=arithmetic, warn_not_dominant=warn_not_dominant))
+        self._streams = None
+        self._bufs = {}
+
+    def _rank_streams(self):
+        torch = _torch()
+        if self._streams is None:
+            self._streams = [torch.cuda.Stream(c.device) for c in self.contexts]
+        return self._streams
+
+    def solve(self, field, out):
+        """field, out: (groups, n, sz) CUDA tensors (any device)."""
+        from .transport import run_on
+        torch = _torch()
+        groups, n, sz = field.shape
+        offs, sizes = self.part.offsets(), self.part.local_sizes
+        if all(r.fused_eligible(groups, sz) for r in self.ranks):
+            run_on(self.contexts, lambda ctx: self.ranks[ctx.rank_id].mailbox(groups, sz))
+            caller = torch.cuda.current_stream(field.device)
+            streams = self._rank_streams()
+            key = (groups, sz)
+            bufs = self._bufs.get(key)
+            if bufs is None:
+                bufs = [(torch.empty((groups, m, sz), dtype=torch.float64, device=c.device),
+                         torch.empty((groups, m, sz), dtype=torch.float64, device=c.device))
+                        for c, m in zip(self.contexts, sizes)]
+                self._bufs[key] = bufs
+            for k, (rank, s) in enumerate(zip(self.ranks, streams)):
+                s.wait_stream(caller)
+                with torch.cuda.stream(s):
+                    bufs[k][0].copy_(field[:, offs[k]:offs[k] + sizes[k], :], non_blocking=True)
+            # every rank's kernel is enqueued before any is waited for: the
+            # persistent grids are co-resident (max_ctas splits shared devices)
+            for k, (rank, s) in enumerate(zip(self.ranks, streams)):
+                with torch.cuda.device(self.contexts[k].device):
+                    rank.launch_fused(bufs[k][0], bufs[k][1], s)
+            for k, s in enumerate(streams):
+                with torch.cuda.stream(s):
+                    out[:, offs[k]:offs[k] + sizes[k], :].copy_(bufs[k][1], non_blocking=True)
+                caller.wait_stream(s)
+            return out
+        torch.cuda.current_stream(field.device).synchronize()
+
+        def body(ctx):
+            k = ctx.rank_id
+            u = field[:, offs[k]:offs[k] + sizes[k], :].to(ctx.device).contiguous()
+            res = self.ranks[k].solve(u)
+            out[:, offs[k]:offs[k] + sizes[k], :].copy_(res)
+            return None
+
+        run_on(self.contexts, body)
+        return out
+
+    def check(self):
+        """Wait for every rank's last fused solve; TimeoutError if one timed out."""
+        from .transport import run_on
+        run_on(self.contexts, lambda ctx: self.ranks[ctx.rank_id].check())
+
+    def audit(self, audit, rounds_before):
+        self.check()
+        audit["rounds_per_rank"] = [c.exchange_rounds - r0
+                                    for c, r0 in zip(self.contexts, rounds_before)]
+        audit["messages_sent"] = sum(c.messages_sent for c in self.contexts)
+        audit["bytes_sent"] = sum(c.bytes_sent for c in self.contexts)
+        audit["max_dropped"] = max(r.coeffs.max_dropped for r in self.ranks)
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+
+
+_GROUPS = {}
+_GROUPS_MAX = 8
+
+
+def _rank_group(sys, stencil, part, devices, arithmetic, warn_not_dominant, fresh=False):
+    torch = _torch()
+    devs = tuple(torch.device("cuda", d) if isinstance(d, int) else torch.device(d)
+                 for d in devices)
+    if len(devs) != part.rank_count:
+        raise ValueError(f"{len(devs)} devices given for {part.rank_count} ranks")
+    if fresh:
+        return _RankGroup(sys, stencil, part, devs, arithmetic, warn_not_dominant)
+    st = None if stencil is None else stencil.c
+    key = (sys.lower.tobytes(), sys.diag.tobytes(), sys.upper.tobytes(), bool(sys.periodic),
+           None if st is None else st.tobytes(), part.local_sizes, devs, arithmetic)
+    g = _GROUPS.get(key)
+    if g is None:
+        if len(_GROUPS) >= _GROUPS_MAX:
+            _GROUPS.pop(next(iter(_GROUPS))).close()
+        g = _GROUPS[key] = _RankGroup(sys, stencil, part, devs, arithmetic, warn_not_dominant)
+    return g
 
 
 class _HostPipe:
@@ -377,15 +474,28 @@ def _pipelined_host_solve(plan, u_host, out_host, groups, sz):
 
 def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
                warn_not_dominant=True, audit=None, *, arithmetic="fast", stream=None,
-               out=None):
+               out=None, devices=None):
     """Solve A u = stencil(field) over P subdomains (distributed.py:399-449).
 
     field_values: (n_groups, n, sz) NumPy array or CUDA tensor. P=1 gives the
     serial (periodic) Thomas result; P>1 the reference's DistD2 truncation at
-    the same subdomain boundaries (all ranks emulated on this GPU; for one
-    rank per GPU see `DistD2Rank`). Keyword extensions: `arithmetic`
-    ("fast" | "strict"), `stream` (torch.cuda.Stream), `out` (result buffer:
-    a CUDA tensor, or a pinned CPU tensor for host-resident pipelines)."""
+    the same subdomain boundaries.
+
+    How P>1 runs:
+      * default: one whole-operator kernel on the current GPU, the rank
+        boundaries folded into its reduced map (fastest; no messages);
+      * `devices=[d_0, ..., d_{P-1}]` (CUDA device per rank, repeats allowed):
+        P real ranks in this process (the reference's spawn_ranks shape),
+        per-rank kernels with in-kernel neighbour rounds over NVLink peer
+        memory (k_dd / k_dd2), or the two-pass path through device messages;
+      * `audit=dict`: the real ranks as above (on `devices`, default all on
+        the current GPU) with fresh contexts, so rounds / messages / bytes are
+        the ones actually exchanged (messages of the fused kernels are counted
+        on the device from the words they post).
+    One rank per PROCESS (torchrun) is `DistD2Rank`. Keyword extensions:
+    `arithmetic` ("fast" | "strict"), `stream` (torch.cuda.Stream), `out`
+    (result buffer: a CUDA tensor, or a pinned CPU tensor for host-resident
+    pipelines), `devices`."""
     shape = tuple(field_values.shape)
     if len(shape) != 3:
         raise ValueError(f"field must be (n_groups, n, sz), got {shape}")
@@ -403,18 +513,17 @@ def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
             if not is_diagonally_dominant(local_slice(sys, part, k)):
                 warnings.warn("local block is not strictly diagonally dominant",
                               NotDominantWarning, stacklevel=2)
-    plan = get_plan(sys, stencil, part, -1, arithmetic)
     torch = _torch()
+    if part.rank_count > 1 and (devices is not None or audit is not None):
+        return _run_ranks(sys, field_values, part, stencil, warn_not_dominant, audit,
+                          arithmetic, stream, out, devices)
+    plan = get_plan(sys, stencil, part, -1, arithmetic)
     if (isinstance(field_values, torch.Tensor) and not field_values.is_cuda
             and field_values.is_pinned() and field_values.dtype == torch.float64
             and field_values.is_contiguous() and groups >= 2):
         res = out if out is not None else torch.empty(shape, dtype=torch.float64,
                                                       pin_memory=True)
         _pipelined_host_solve(plan, field_values, res, groups, sz)
-        if audit is not None and part.rank_count > 1:
-            msgs, nbytes = _audit_counts(part, sys.periodic, groups, sz)
-            audit.update(rounds_per_rank=[2] * part.rank_count, messages_sent=msgs,
-                         bytes_sent=nbytes, max_dropped=float(plan.info.max_dropped))
         return res
     fld = _Field(field_values)
     if groups * sz == 0:
@@ -422,18 +531,64 @@ def run_distd2(sys, field_values, part=None, stencil=None, rank_count=None,
     res = out if (out is not None and not fld.host) else fld.empty_like()
     N.check(N.lib().tds_solve(plan.handle, fld.ptr, ctypes.c_void_p(res.data_ptr()),
                               groups, sz, _stream_handle(stream)), part.rank_count)
-    if audit is not None and part.rank_count > 1:
-        msgs, nbytes = _audit_counts(part, sys.periodic, groups, sz)
-        audit["rounds_per_rank"] = [2] * part.rank_count
-        audit["messages_sent"] = msgs
-        audit["bytes_sent"] = nbytes
-        audit["max_dropped"] = float(plan.info.max_dropped)
     if out is not None and not fld.host:
         return res
     return fld.give(res, out)
 
 
+def _run_ranks(sys, field_values, part, stencil, warn_not_dominant, audit, arithmetic, stream,
+               out, devices):
+    """run_distd2 over P real in-process ranks (see run_distd2)."""
+    torch = _torch()
+    if devices is None:
+        _need_cuda()
+        devices = [torch.cuda.current_device()] * part.rank_count
+    fresh = audit is not None
+    group = _rank_group(sys, stencil, part, devices, arithmetic, warn_not_dominant, fresh)
+    try:
+        rounds_before = [c.exchange_rounds for c in group.contexts]
+        fld = _Field(field_values)
+        ctx_stream = torch.cuda.stream(stream) if stream is not None else None
+        if ctx_stream is not None:
+            ctx_stream.__enter__()
+        try:
+            res = out if (out is not None and not fld.host) else fld.empty_like()
+            if fld.t.numel():
+                group.solve(fld.t, res)
+        finally:
+            if ctx_stream is not None:
+                ctx_stream.__exit__(None, None, None)
+        if audit is not None:
+            group.audit(audit, rounds_before)
+        if out is not None and not fld.host:
+            return res
+        return fld.give(res, out)
+    finally:
+        if fresh:
+            group.close()
+
+
 # ------------------------------------------------------ phase functions
+
+_DEV_COEFFS = {}
+_DEV_COEFFS_MAX = 64
+
+
+def _dev(arr, device):
+    """Device copy of a host coefficient array, cached per (array, device):
+    the phase kernels take device coefficients (no per-call allocation or
+    host synchronisation inside the ABI)."""
+    torch = _torch()
+    key = (id(arr), str(device))
+    hit = _DEV_COEFFS.get(key)
+    if hit is not None and hit[0] is arr:
+        return hit[1]
+    if len(_DEV_COEFFS) >= _DEV_COEFFS_MAX:
+        _DEV_COEFFS.pop(next(iter(_DEV_COEFFS)))
+    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+    _DEV_COEFFS[key] = (arr, t)
+    return t
+
 
 def _lanes_of(shape):
     lanes = 1
@@ -450,9 +605,11 @@ def decouple_fused(u_ext, coeffs, stencil):
         raise ValueError(f"expected {m + 4} positions incl. halo, got {u_ext.shape[0]}")
     fld = _Field(u_ext)
     d = fld.empty_like((m,) + tuple(u_ext.shape[1:]))
-    st = N.f64(stencil.c[:m])
-    w, f, r = N.f64(coeffs.w), N.f64(coeffs.f), N.f64(coeffs.r)
-    N.check(N.lib().tds_decouple_fused(fld.ptr, N.dptr(st), N.dptr(w), N.dptr(f), N.dptr(r),
+    dev = fld.t.device
+    st = _dev(stencil.c, dev)[:m].contiguous()
+    w, f, r = (_dev(x, dev) for x in (coeffs.w, coeffs.f, coeffs.r))
+    N.check(N.lib().tds_decouple_fused(fld.ptr, *(ctypes.c_void_p(x.data_ptr())
+                                                  for x in (st, w, f, r)),
                                        ctypes.c_void_p(d.data_ptr()), m,
                                        _lanes_of(u_ext.shape), _stream_handle()))
     return fld.give(d)
@@ -493,8 +650,8 @@ def substitute(d, coeffs, u_start, u_end):
     fd = _Field(d)
     us, ue = _Field(u_start), _Field(u_end)
     out = fd.empty_like()
-    sa, sc = N.f64(coeffs.s_a), N.f64(coeffs.s_c)
-    N.check(N.lib().tds_substitute(fd.ptr, N.dptr(sa), N.dptr(sc), us.ptr, ue.ptr,
+    sa, sc = (ctypes.c_void_p(_dev(x, fd.t.device).data_ptr()) for x in (coeffs.s_a, coeffs.s_c))
+    N.check(N.lib().tds_substitute(fd.ptr, sa, sc, us.ptr, ue.ptr,
                                    ctypes.c_void_p(out.data_ptr()), m, _lanes_of(d.shape),
                                    _stream_handle()))
     return fd.give(out)

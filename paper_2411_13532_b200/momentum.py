@@ -325,6 +325,7 @@ class SlabTransport:
                     if self.nu != 0.0 else None)
             self._zmail = {}
             self._zepoch = 0
+            self._zbroken = None
 
     def local_slab(self, u3):
         """Pack this rank's slab of a global Cartesian (n, n, n) array for x."""
@@ -369,27 +370,44 @@ class SlabTransport:
     def _z_fused(self, comp, advect, out):
         """The z term as one k_dd_transport launch per rank; False when the
         plans / shape do not allow it (then three DistD2Rank solves)."""
-        from .rank import open_mailboxes
         if not self._zfused:
             return False
+        if self._zbroken is not None:
+            raise TimeoutError(str(self._zbroken))
         p1, p2 = self._zfused
         groups, m, sz = comp.shape
         key = (groups, sz)
         mb = self._zmail.get(key)
         if mb is None:
-            mb = open_mailboxes(self.ctx, N.lib().tds_transport_mailbox_words(groups, sz))
+            mb = self.ctx.open_mailboxes(N.lib().tds_transport_mailbox_words(groups, sz))
             self._zmail[key] = mb
-        own, prev, nxt, _ = mb
+        self._poll_z()
         self._zepoch += 1
+        stream = _torch().cuda.current_stream()
         rc = N.lib().tds_fused_transport(
             p1.handle, None if p2 is None else p2.handle, _vp(comp), _vp(advect), _vp(out),
-            self.nu, groups, sz, own, prev, nxt, self._zepoch, _stream_handle())
+            self.nu, groups, sz, mb.own, mb.prev, mb.next, self._zepoch,
+            self.ctx.fused_grid_cap, ctypes.c_void_p(stream.cuda_stream))
         if rc == N.TDS_ERR_UNSUPPORTED and self._zepoch == 1:
             self._zfused = None        # same decision on every rank: plans / shape only
             return False
         N.check(rc)
+        mb.post_status(stream)
         self.ctx.exchange_rounds += 6
         return True
+
+    def _poll_z(self, block=False):
+        """Fold the fused z kernels' status words into the context (posted
+        halo words of u_i and u_j: 4 L per directed edge per term, boundary
+        rows: one L per solve); TimeoutError if a wait timed out."""
+        from .rank import account_status
+        for (groups, sz), mb in self._zmail.items():
+            lines = groups * sz
+            try:
+                account_status(self.ctx, mb, 4 * lines, lines, block)
+            except TimeoutError as exc:
+                self._zbroken = exc
+                raise
 
     def _z_contribution(self, comp, advect, out):
         torch = _torch()
@@ -453,27 +471,26 @@ class SlabTransport:
         return tuple(c + dt * r for c, r in zip((u, v, w), rhs))
 
     def check(self):
+        """Wait for the last fused kernels' status; TimeoutError if a rank's
+        neighbour never arrived (synchronous)."""
         for r in self._rank or ():
             if r is not None:
                 r.check()
-        for (groups, sz), (own, _, _, _) in getattr(self, "_zmail", {}).items():
-            err = ctypes.c_int(0)
-            N.check(N.lib().tds_transport_mailbox_error(own, groups, sz, ctypes.byref(err)))
-            if err.value:
-                raise TimeoutError(f"rank {self.ctx.rank_id}: fused transport timed out "
-                                   "waiting for a neighbour")
+        if getattr(self, "_zbroken", None) is not None:
+            raise TimeoutError(str(self._zbroken))
+        if getattr(self, "_zmail", None):
+            self._poll_z(block=True)
 
     @property
     def fused_z(self):
         return bool(getattr(self, "_zfused", None))
 
     def close(self):
-        from .rank import close_mailboxes
         for r in self._rank or ():
             if r is not None:
                 r.close()
         for mb in getattr(self, "_zmail", {}).values():
-            close_mailboxes(mb)
+            mb.close()
         self._zmail = {}
 
 

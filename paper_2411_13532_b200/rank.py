@@ -1,34 +1,42 @@
-"""One rank per B200: the per-rank DistD2 solve (reference distributed.py:
-327-366 run by transport.spawn_ranks, transport.py:105-139), with the two
-neighbour rounds on NCCL (torch.distributed) and the arithmetic in
-libtds_b200.so.
+"""The per-rank DistD2 solve (reference distributed.py:308-366 run by
+transport.spawn_ranks, transport.py:105-139): one rank per B200 process
+(torchrun, `RankContext`) or several ranks in one process (`LocalRankContext`,
+one stream per rank; ranks may share a device), arithmetic in libtds_b200.so.
+
+Construction follows the reference's per-rank view: `preprocess` of the
+rank's local_slice, the one-time neighbour share of the pair couplings
+(share_pair_coeffs, distributed.py:308-324; D16) and a plan built from those
+local data only (tds_plan_create_local).
 
 DistD2Rank.solve(u_local) for a rank holding rows [off, off+m) of every line:
-    tds_halo_rows      -> rows {0,1}, {m-2,m-1}           (K1, tiny)
-    ROUND 1            -> halo_lo / halo_hi               (NCCL P2P)
-    tds_boundary_rows  -> d[0], d[m-1] of every line      (pass A: reads u)
-    ROUND 2            -> prev's d[m-1], next's d[0]      (NCCL P2P)
-    tds_finish         -> 2x2 pairs + substitution, out   (pass B: reads u,
-                                                           writes out)
-The two-pass path recomputes the decoupling in pass B instead of
-materialising d: 24 B/point of HBM traffic.
 
 FUSED path (default when every rank holds the same number of rows and the
 field is TMA-eligible): ONE kernel per rank per solve, `tds_fused_solve`
-(k_dd). Both neighbour rounds are NVLink peer stores into the neighbours'
-IPC-mapped mailboxes with per-tile acquire/release flags -- 16 B/point, no
-NCCL call and no host synchronisation on the solve path.
+(k_dd / k_dd2). Both neighbour rounds are NVLink peer stores into the
+neighbours' mailboxes -- 16 B/point, no NCCL call and no host
+synchronisation on the solve path. The mailbox status words (error, posted
+words) are copied back asynchronously and inspected at the next call:
+a neighbour that never arrived raises TimeoutError (the kernel poisons the
+affected rows with NaN instead of hanging) and the rank refuses further
+fused solves; posted words become the context's message accounting.
+
+TWO-PASS path (TDS_FUSED=0, ragged partitions, strict arithmetic):
+    tds_halo_rows      -> rows {0,1}, {m-2,m-1}           (K1, tiny)
+    ROUND 1            -> halo_lo / halo_hi               (ctx.round)
+    tds_boundary_rows  -> d[0], d[m-1] of every line      (pass A: reads u)
+    ROUND 2            -> prev's d[m-1], next's d[0]      (ctx.round)
+    tds_finish         -> 2x2 pairs + substitution, out   (pass B)
 """
 
+import ctypes
 import os
 
-import ctypes
-
 from . import _native as N
-from .distributed import (Plan, _flags, _stream_handle, decouple_fused, solve_boundary_pair,
-                          substitute, BoundaryPair)
+from .distributed import (BoundaryPair, Plan, _flags, _stream_handle, decouple_fused,
+                          local_slice, preprocess, rank_position, solve_boundary_pair,
+                          substitute)
 from .transport import (BOUNDARY_HIGH, BOUNDARY_LOW, HALO_HIGH, HALO_LOW, exchange_boundary,
-                        exchange_halo)
+                        exchange_halo, share_scalars)
 
 
 def _vp(t):
@@ -36,44 +44,40 @@ def _vp(t):
 
 
 def open_mailboxes(ctx, words):
-    """Allocate this rank's sentinel-filled mailbox of `words` 8-byte slots,
-    exchange CUDA IPC handles over the rank group, and map prev's / next's
-    mailboxes: returns (own, prev, next, [mapped pointers])."""
-    import torch.distributed as dist
-    lib = N.lib()
-    own = ctypes.c_void_p()
-    handle = ctypes.create_string_buffer(64)
-    N.check(lib.tds_ipc_alloc(words * 8, ctypes.byref(own), handle))
-    handles = [None] * ctx.rank_count
-    dist.all_gather_object(handles, handle.raw, group=ctx.group)
-    opened = {}
-
-    def open_rank(pos):
-        pos %= ctx.rank_count
-        if pos not in opened:
-            ptr = ctypes.c_void_p()
-            N.check(lib.tds_ipc_open(handles[pos], ctypes.byref(ptr)))
-            opened[pos] = ptr
-        return opened[pos]
-
-    prev = open_rank(ctx.rank_id - 1) if ctx.has_prev else ctypes.c_void_p(0)
-    nxt = open_rank(ctx.rank_id + 1) if ctx.has_next else ctypes.c_void_p(0)
-    return own, prev, nxt, list(opened.values())
+    """This rank's prepared mailbox of `words` slots + the neighbours' mapped
+    ones (collective over the rank group); returns a transport.Mailboxes."""
+    return ctx.open_mailboxes(words)
 
 
 def close_mailboxes(mb):
-    lib = N.lib()
-    own, _, _, opened = mb
-    for ptr in opened:
-        lib.tds_ipc_close(ptr)
-    lib.tds_ipc_free(own)
+    mb.close()
+
+
+def account_status(ctx, mb, halo_words_per_msg, bnd_words_per_msg, block=False):
+    """Fold the device-side posted-word counters of a mailbox into the
+    context's message accounting; raise TimeoutError if the kernel recorded
+    a timed-out wait. Returns True if the status was available."""
+    st = mb.status(block=block)
+    if st is None:
+        return False
+    err, halo, bnd = st
+    dh, db = halo - mb.counted[0], bnd - mb.counted[1]
+    if dh or db:
+        mb.counted = [halo, bnd]
+        ctx.messages_sent += dh // max(1, halo_words_per_msg) + db // max(1, bnd_words_per_msg)
+        ctx.bytes_sent += 8 * (dh + db)
+    if err:
+        raise TimeoutError(f"rank {ctx.rank_id}: fused solve timed out waiting for a neighbour "
+                           "(its rows were poisoned with NaN)")
+    return True
 
 
 class DistD2Rank:
-    """Per-rank solver object: plan (coefficient tables on this GPU) and the
-    neighbour buffers, reused across solves."""
+    """Per-rank solver object: plan (coefficient tables on this rank's GPU)
+    and the neighbour buffers / mailboxes, reused across solves. Collective:
+    every rank of the group constructs it (the pair couplings are shared)."""
 
-    def __init__(self, sys, stencil, part, ctx, arithmetic="fast"):
+    def __init__(self, sys, stencil, part, ctx, arithmetic="fast", warn_not_dominant=True):
         if part.rank_count != ctx.rank_count:
             raise ValueError("partition and rank context disagree on the rank count")
         if part.rank_count < 2:
@@ -82,12 +86,21 @@ class DistD2Rank:
             raise ValueError("rank topology must be a ring exactly when the system is periodic")
         self.ctx = ctx
         self.part = part
-        self.m = part.local_sizes[ctx.rank_id]
-        st = None if stencil is None else stencil.c
-        self.plan = Plan.create(sys, st, part.local_sizes, ctx.rank_id, _flags(arithmetic))
+        k = ctx.rank_id
+        self.m = part.local_sizes[k]
+        off = part.offsets()[k]
+        local_sys = local_slice(sys, part, k)
+        self.coeffs = preprocess(local_sys, rank_position(k, part.rank_count), sys.periodic,
+                                 warn_not_dominant=warn_not_dominant)
+        prev_sc, next_sa = share_scalars(ctx, self.coeffs.s_a[0], self.coeffs.s_c[-1])
+        self.pair_coeffs = (prev_sc, next_sa)
+        st = None if stencil is None else stencil.c[off:off + self.m]
+        self.plan = Plan.create_local(local_sys, st, ctx.has_prev, ctx.has_next, prev_sc,
+                                      next_sa, _flags(arithmetic))
         self._bufs = {}
         self._mail = {}
         self._epoch = 0
+        self.broken = None
         self.fused = (self.plan.path == "fast" and len(set(part.local_sizes)) == 1
                       and os.environ.get("TDS_FUSED", "1") != "0")
 
@@ -111,32 +124,39 @@ class DistD2Rank:
             self._bufs[key] = b
         return b
 
-    def _mailbox(self, groups, sz):
-        """Own mailbox + the neighbours' mailboxes mapped through CUDA IPC
-        (one collective handle exchange per field shape)."""
+    def mailbox(self, groups, sz):
+        """Own mailbox + the neighbours' (one collective per field shape)."""
         key = (groups, sz)
         mb = self._mail.get(key)
         if mb is None:
-            mb = open_mailboxes(self.ctx, N.lib().tds_mailbox_words(groups, sz))
+            mb = self.ctx.open_mailboxes(N.lib().tds_mailbox_words(groups, sz))
             self._mail[key] = mb
         return mb
 
+    def fused_eligible(self, groups, sz):
+        return bool(self.fused and N.lib().tds_fused_eligible(self.plan.handle, groups, sz))
+
+    def _poll(self, block=False):
+        for (groups, sz), mb in self._mail.items():
+            try:
+                account_status(self.ctx, mb, 2 * groups * sz, groups * sz, block)
+            except TimeoutError as exc:
+                self.broken = exc
+                raise
+
     def check(self):
-        """Raise if a fused solve timed out waiting for a neighbour (reads the
-        mailbox error words; synchronous)."""
-        for (groups, sz), (own, _, _, _) in self._mail.items():
-            err = ctypes.c_int(0)
-            N.check(N.lib().tds_mailbox_error(own, groups, sz, ctypes.byref(err)))
-            if err.value:
-                raise TimeoutError(f"rank {self.ctx.rank_id}: fused DistD2 solve timed out "
-                                   "waiting for a neighbour")
+        """Wait for the last fused solve's status words and raise TimeoutError
+        if a wait timed out (synchronous)."""
+        if self.broken is not None:
+            raise TimeoutError(str(self.broken))
+        self._poll(block=True)
 
     def close(self):
         for mb in self._mail.values():
-            close_mailboxes(mb)
+            mb.close()
         self._mail = {}
 
-    def solve(self, u, out=None):
+    def solve(self, u, out=None, stream=None):
         """u: this rank's (n_groups, m, sz) fp64 CUDA tensor -> out (same shape)."""
         import torch
         groups, m, sz = u.shape
@@ -147,16 +167,35 @@ class DistD2Rank:
             u = u.clone()
         if out is None:
             out = torch.empty_like(u)
-        if self.fused and N.lib().tds_fused_eligible(self.plan.handle, groups, sz):
-            own, prev, nxt, _ = self._mailbox(groups, sz)
-            self._epoch += 1
-            self.ctx.begin_solve()
-            self.ctx.exchange_rounds += 2          # both rounds run inside the kernel
-            N.check(N.lib().tds_fused_solve(self.plan.handle, _vp(u), _vp(out), groups, sz, own,
-                                            prev, nxt, self._epoch, _stream_handle()))
+        if self.fused_eligible(groups, sz):
+            self.launch_fused(u, out, stream)
             return out
+        return self._two_pass(u, out, stream)
+
+    def launch_fused(self, u, out, stream=None):
+        """Enqueue one fused solve (k_dd / k_dd2) on `stream` (default: the
+        current stream). Raises TimeoutError if an earlier solve timed out."""
+        import torch
+        if self.broken is not None:
+            raise TimeoutError(f"rank {self.ctx.rank_id}: an earlier fused solve timed out; "
+                               "the mailboxes are no longer usable")
+        self._poll()
+        groups, _, sz = u.shape
+        mb = self.mailbox(groups, sz)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self._epoch += 1
+        self.ctx.begin_solve()
+        self.ctx.exchange_rounds += 2          # both rounds run inside the kernel
+        N.check(N.lib().tds_fused_solve(self.plan.handle, _vp(u), _vp(out), groups, sz, mb.own,
+                                        mb.prev, mb.next, self._epoch, self.ctx.fused_grid_cap,
+                                        ctypes.c_void_p(s.cuda_stream)))
+        mb.post_status(s)
+
+    def _two_pass(self, u, out, stream=None):
+        groups, m, sz = u.shape
         b = self._buffers(groups, sz, u.device)
-        lib, h, s, ctx = N.lib(), self.plan.handle, _stream_handle(), self.ctx
+        lib, h, ctx = N.lib(), self.plan.handle, self.ctx
+        s = _stream_handle(stream)
         ctx.begin_solve()
         N.check(lib.tds_halo_rows(h, _vp(u), _vp(b["first2"]), _vp(b["last2"]), groups, sz, s))
         sends, recvs = [], []

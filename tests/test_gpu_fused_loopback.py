@@ -39,13 +39,14 @@ def _loopback(n, groups, sz, env, seed=0, epochs=3):
     out = torch.empty_like(u)
     mail = torch.full((lib.tds_mailbox_words(groups, sz),), -1, dtype=torch.int64, device="cuda")
     mp = ctypes.c_void_p(mail.data_ptr())
+    N.check(lib.tds_mailbox_init(mp, mail.numel(), _stream_handle()))
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
         for e in range(1, epochs + 1):
             N.check(lib.tds_fused_solve(plan.handle, ctypes.c_void_p(u.data_ptr()),
                                         ctypes.c_void_p(out.data_ptr()), groups, sz, mp, mp, mp,
-                                        e, _stream_handle()))
+                                        e, 0, _stream_handle()))
         torch.cuda.synchronize()
     finally:
         for k, v in old.items():

@@ -1,0 +1,291 @@
+"""Distributed DistD2 with P REAL ranks on ONE B200: the per-rank kernels the
+torchrun path runs (fused k_dd / k_dd2 with in-kernel neighbour rounds, the
+two-pass halo / pass A / pass B path, the reference-shaped distd2_solve and
+the fused transport term k_dd_transport), each rank with its own plan,
+stream and mailbox, cross-wired in one process (transport.LocalRankContext;
+persistent grids split with max_ctas so all ranks are co-resident).
+
+Parity: against the reference's own run_distd2 outputs (tests/golden, made by
+tests/golden/make_golden.py from /root/reference) and the pinned oracle on
+the same partitions -- the reference's truncation at the same rank
+boundaries (distributed.py:327-366, transport.py:105-191)."""
+
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import golden_run
+from oracle import tds_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2411_13532_b200 as T  # noqa: E402
+from paper_2411_13532_b200 import distributed as D  # noqa: E402
+from paper_2411_13532_b200 import transport as TR  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+@pytest.fixture
+def env(monkeypatch):
+    def set_env(d):
+        for k, v in d.items():
+            monkeypatch.setenv(k, v)
+    return set_env
+
+
+def _system(g):
+    s = T.TridiagonalSystem(g["lower"], g["diag"], g["upper"], periodic=g["periodic"])
+    st = None if g["stencil"] is None else T.StencilCoeffs(g["stencil"])
+    return s, st
+
+
+def _group(s, st, sizes, arithmetic="fast"):
+    p = len(sizes)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", T.NotDominantWarning)
+        return D._RankGroup(s, st, T.SubdomainPartition(tuple(sizes)), [0] * p, arithmetic,
+                            True)
+
+
+def _solve(group, field):
+    u = torch.from_numpy(np.ascontiguousarray(field)).cuda()
+    out = torch.empty_like(u)
+    group.solve(u, out)
+    torch.cuda.synchronize()
+    group.check()
+    return out.cpu().numpy()
+
+
+FUSED_TAGS = ["d1p1024_P2", "d1p1024_P8", "d1p512_P8", "d1o512_P8"]
+KNOBS = [{}, {"TDS_DEFER": "0"}, {"TDS_DEFER": "2"}, {"TDS_TL": "8"}, {"TDS_DD_TL32": "0"}]
+
+
+@pytest.mark.parametrize("knobs", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items())
+                         or "default")
+@pytest.mark.parametrize("tag", FUSED_TAGS)
+def test_fused_ranks_match_reference_golden(golden, tag, knobs, env):
+    env(knobs)
+    g = golden_run(golden, tag)
+    s, st = _system(g)
+    group = _group(s, st, g["sizes"])
+    try:
+        assert all(r.fused_eligible(g["field"].shape[0], g["field"].shape[2])
+                   for r in group.ranks), "fused kernel not eligible"
+        got = _solve(group, g["field"])
+        assert O.rel_linf(got, g["out"]) <= 1e-12
+        # second solve: the other mailbox parity half, same bits
+        assert np.array_equal(_solve(group, g["field"]), got)
+    finally:
+        group.close()
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_fused_ranks_many_items_vs_oracle(p, periodic):
+    # 1024-row lines, m = 512 / 256 / 128 (the per-GPU blocks of BASELINE
+    # config 3), enough lines that every CTA runs several persistent items
+    n, groups, sz = 1024, 40, 32
+    lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, periodic)
+    s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
+    sizes = O.balanced_sizes(n, p)
+    field = np.random.default_rng(p).standard_normal((groups, n, sz))
+    group = _group(s, T.StencilCoeffs(stc), sizes)
+    try:
+        got = None
+        for _ in range(3):             # epochs cycle the mailbox parity halves
+            got = _solve(group, field)
+        want = O.run_distd2(lo, di, up, periodic, field, stc, sizes)
+        assert O.rel_linf(got, want) <= 1e-12
+    finally:
+        group.close()
+
+
+def test_fused_d2_and_open_ranks_vs_oracle():
+    n, groups, sz = 512, 8, 16
+    for kind, periodic in (("d2", True), ("d1", False)):
+        lo, di, up, stc = O.assemble(kind, n, 2 * np.pi / n, periodic)
+        s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
+        sizes = O.balanced_sizes(n, 4)
+        field = np.random.default_rng(7).standard_normal((groups, n, sz))
+        group = _group(s, T.StencilCoeffs(stc), sizes)
+        try:
+            got = _solve(group, field)
+            want = O.run_distd2(lo, di, up, periodic, field, stc, sizes)
+            assert O.rel_linf(got, want) <= 1e-12, kind
+        finally:
+            group.close()
+
+
+ALL_P_TAGS = ["d1p64_P2", "d1o64_P2", "d2p64_P2", "rd96_P3", "rd128_P2", "rd128_P4", "rd20_P3",
+              "rd50_P3", "d1p512_P8", "d1o512_P8", "d1p1024_P2", "d1p1024_P8"]
+
+
+@pytest.mark.parametrize("tag", ALL_P_TAGS)
+def test_two_pass_ranks_strict_bitwise(golden, tag, env):
+    # halo rows -> ROUND 1 -> pass A -> ROUND 2 -> pass B, the rounds as
+    # device-to-device messages between the rank threads; strict arithmetic
+    # (staged kernels, reference operation order) is bit-identical
+    env({"TDS_FUSED": "0"})
+    g = golden_run(golden, tag)
+    s, st = _system(g)
+    group = _group(s, st, g["sizes"], arithmetic="strict")
+    try:
+        assert np.array_equal(_solve(group, g["field"]), g["out"])
+    finally:
+        group.close()
+
+
+@pytest.mark.parametrize("tag", ALL_P_TAGS)
+def test_two_pass_ranks_fast(golden, tag, env):
+    env({"TDS_FUSED": "0"})
+    g = golden_run(golden, tag)
+    s, st = _system(g)
+    group = _group(s, st, g["sizes"])
+    try:
+        assert O.rel_linf(_solve(group, g["field"]), g["out"]) <= 1e-12
+    finally:
+        group.close()
+
+
+@pytest.mark.parametrize("tag", ["d1p64_P2", "d1o64_P2", "rd96_P3", "rd50_P3", "d1o512_P8"])
+def test_reference_shaped_distd2_solve_bitwise(golden, tag):
+    # distributed.py:327-366 phase by phase: preprocess, one-time pair share,
+    # exchange_halo, decouple_fused, exchange_boundary, 2x2 pairs, substitute
+    g = golden_run(golden, tag)
+    s, st = _system(g)
+    part = T.SubdomainPartition(g["sizes"])
+    field = g["field"]
+    stc = st.c if st is not None else T.identity_stencil(s.n).c
+    offs = part.offsets()
+
+    def body(ctx):
+        k = ctx.rank_id
+        off, m = offs[k], part.local_sizes[k]
+        co = T.preprocess(T.local_slice(s, part, k), T.rank_position(k, part.rank_count),
+                          s.periodic, warn_not_dominant=False)
+        psc, nsa = TR.share_scalars(ctx, co.s_a[0], co.s_c[-1])
+        u = torch.from_numpy(np.ascontiguousarray(field[:, off:off + m, :])).to(ctx.device)
+        res = T.distd2_solve(ctx, u, co, T.StencilCoeffs(stc[off:off + m]), T.PairCoeffs(psc, nsa))
+        return res.cpu().numpy(), ctx.exchange_rounds, ctx.messages_sent
+
+    res = TR.spawn_ranks(part.rank_count, s.periodic, body, devices=[0] * part.rank_count)
+    got = np.concatenate([r[0] for r in res], axis=1)
+    assert np.array_equal(got, g["out"])
+    assert [r[1] for r in res] == [2] * part.rank_count
+    edges = 2 * part.rank_count if s.periodic else 2 * (part.rank_count - 1)
+    assert sum(r[2] for r in res) == 3 * edges
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("cyclic", [False, True])
+def test_audit_counts_real_messages_fused(p, cyclic):
+    # reference test_distributed.py:263-286 on the FUSED per-rank kernels:
+    # halo / boundary messages are counted on the device from the words the
+    # kernels posted into the neighbours' mailboxes; the pair share is a real
+    # context message
+    n, sz = 128 * p, 32
+    lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, cyclic)
+    s = T.TridiagonalSystem(lo, di, up, periodic=cyclic)
+    field = np.random.default_rng(p).standard_normal((2, n, sz))
+    audit = {}
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", T.NotDominantWarning)
+        got = T.run_distd2(s, field, part=T.SubdomainPartition.balanced(n, p),
+                           stencil=T.StencilCoeffs(stc), audit=audit)
+    edges = 2 * p if cyclic else 2 * (p - 1)
+    assert audit["rounds_per_rank"] == [2] * p
+    assert audit["messages_sent"] == 3 * edges
+    halo, bnd = 2 * 2 * sz * 8, 2 * sz * 8          # (G,2,sz) and (G,sz) fp64 payloads
+    assert audit["bytes_sent"] == edges * (8 + halo + bnd)
+    want = O.run_distd2(lo, di, up, cyclic, field, stc, O.balanced_sizes(n, p))
+    assert O.rel_linf(got, want) <= 1e-12
+
+
+def test_run_distd2_devices_keyword_drop_in(golden):
+    g = golden_run(golden, "d1p1024_P8")
+    s, st = _system(g)
+    got = T.run_distd2(s, g["field"], part=T.SubdomainPartition(g["sizes"]), stencil=st,
+                       devices=[0] * 8)
+    assert isinstance(got, np.ndarray)
+    assert O.rel_linf(got, g["out"]) <= 1e-12
+    u = torch.from_numpy(g["field"]).cuda()
+    got_t = T.run_distd2(s, u, part=T.SubdomainPartition(g["sizes"]), stencil=st,
+                         devices=[0] * 8)
+    assert got_t.is_cuda and np.array_equal(got_t.cpu().numpy(), got)
+
+
+def test_fused_timeout_raises_and_poisons(env):
+    # rank 1 never launches: rank 0's waits time out (TDS_FUSED_TIMEOUT_MS),
+    # its rows come back NaN and the rank refuses further fused solves
+    env({"TDS_FUSED_TIMEOUT_MS": "200"})
+    n, groups, sz = 1024, 4, 32
+    lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, True)
+    s = T.TridiagonalSystem(lo, di, up, periodic=True)
+    group = _group(s, T.StencilCoeffs(stc), O.balanced_sizes(n, 2))
+    try:
+        TR.run_on(group.contexts, lambda ctx: group.ranks[ctx.rank_id].mailbox(groups, sz))
+        u = torch.randn((groups, 512, sz), dtype=torch.float64, device="cuda")
+        out = torch.zeros_like(u)
+        r0 = group.ranks[0]
+        r0.launch_fused(u, out)
+        torch.cuda.synchronize()
+        with pytest.raises(TimeoutError):
+            r0.check()
+        assert torch.isnan(out).any()
+        with pytest.raises(TimeoutError):
+            r0.launch_fused(u, out)
+    finally:
+        group.close()
+
+
+@pytest.mark.parametrize("p,nu,sz", [(2, 0.02, 16), (2, 0.0, 32), (4, 0.01, 32)])
+def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz):
+    # BASELINE config 5's distributed RHS: z-slabs on P in-process ranks, the
+    # z terms as one k_dd_transport per rank (in-kernel neighbour rounds)
+    n = 128
+    h = 2 * np.pi / n
+    rng = np.random.default_rng(77)
+    u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
+
+    def body(ctx):
+        tr = T.SlabTransport(n, sz, nu, h, ctx)
+        loc = [tr.local_slab(a) for a in (u3, v3, w3)]
+        rhs = tr.rhs(*loc)
+        rhs2 = tr.rhs(*loc)
+        torch.cuda.current_stream().synchronize()
+        tr.check()
+        same = all(bool(torch.equal(a, b)) for a, b in zip(rhs, rhs2))
+        carts = [T.unpack(T.GroupedField(tr.lay["x"], c)).cpu().numpy() for c in rhs]
+        fused = tr.fused_z
+        tr.close()
+        return carts, same, fused
+
+    res = TR.spawn_ranks(p, True, body, devices=[0] * p)
+    assert all(r[1] for r in res) and all(r[2] for r in res)
+    full = [np.concatenate([r[0][i] for r in res], axis=2) for i in range(3)]
+    want = O.transport_rhs(u3, v3, w3, nu, h, sz, rank_counts=(1, 1, p))
+    assert max(O.rel_linf(g, w) for g, w in zip(full, want)) <= 1e-12
+
+
+def test_transport_rank_count_two_vs_oracle():
+    # evaluate_transport_rhs(rank_count=2) (momentum.py:142-169, the
+    # reference's rank_count applied in every direction) against the
+    # oracle's restatement with rank_counts=(2, 2, 2)
+    n, sz, nu = 32, 8, 0.02
+    h = 2 * np.pi / n
+    rng = np.random.default_rng(5)
+    u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
+    vel = T.VelocityField.from_arrays(u3, v3, w3, nu, h, sz=sz)
+    rhs = T.evaluate_transport_rhs(vel, rank_count=2)
+    got = [T.unpack(c) for c in rhs]
+    got = [g.cpu().numpy() if hasattr(g, "cpu") else np.asarray(g) for g in got]
+    want = O.transport_rhs(u3, v3, w3, nu, h, sz, rank_counts=(2, 2, 2))
+    assert max(O.rel_linf(g, w) for g, w in zip(got, want)) <= 1e-12

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
         assert name in N.SIGNATURES, f"{name} has no ctypes signature"
     assert set(N.SIGNATURES) == set(declared)
-    assert lib.tds_abi_version() == 1
+    assert lib.tds_abi_version() == N.ABI_VERSION == 2
 
 
 def test_library_is_sm100a_build():

@@ -38,12 +38,13 @@ def main():
     words = lib.tds_mailbox_words(G, sz)
     mail = torch.full((words,), -1, dtype=torch.int64, device="cuda")   # 0xFF.. sentinel
     mp = ctypes.c_void_p(mail.data_ptr())
+    N.check(lib.tds_mailbox_init(mp, mail.numel(), _stream_handle()))
     vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
     def fused(epoch):
         N.check(lib.tds_fused_solve(plan.handle, vp(u), vp(out), G, sz, mp, mp, mp, epoch,
-                                    _stream_handle()))
+                                    0, _stream_handle()))
 
     p1 = T.get_plan(T.TridiagonalSystem(loc.lower, loc.diag, loc.upper, periodic=True),
                     T.StencilCoeffs(st.c[:m]), T.SubdomainPartition((m,)))

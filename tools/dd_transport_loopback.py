@@ -42,11 +42,12 @@ def main():
     words = lib.tds_transport_mailbox_words(G, sz)
     mail = torch.full((words,), -1, dtype=torch.int64, device="cuda")
     mp = ctypes.c_void_p(mail.data_ptr())
+    N.check(lib.tds_mailbox_init(mp, mail.numel(), _stream_handle()))
     vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def fused(e):
         N.check(lib.tds_fused_transport(p1.handle, p2.handle, vp(ui), vp(uj), vp(out), args.nu,
-                                        G, sz, mp, mp, mp, e, _stream_handle()))
+                                        G, sz, mp, mp, mp, e, 0, _stream_handle()))
 
     def single(e):
         assert momentum._fused_contribution(ui, uj, out, m, h, args.nu, False)
