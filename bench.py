@@ -199,6 +199,9 @@ def run_single(args, torch):
     achieved = BYTES_PER_POINT * points / (launch_ms * 1e-3) / 1e9
 
     e2e = run_e2e(args, torch, T, sys_, st, part, fields, n)
+    del fields, outs
+    torch.cuda.empty_cache()
+    t1 = t1_anchor(args, torch) if not args.no_t1 else None
     res = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -224,9 +227,39 @@ def run_single(args, torch):
         "e2e": e2e,
         "gpu_launches": 3 * args.steps,
         "clocks": clocks,
+        "t1_1024": t1,
     }
     res["cpu_baseline"] = cpu_baseline(args, n)
     return res
+
+
+def t1_anchor(args, torch, n=1024, steps=10):
+    """T1 of BASELINE config 3: the 1024^3 x/y/z solve on ONE GPU (the
+    north star's E(N) = T1(1024^3) / (N * T_N)). One randn field in the
+    SZ-blocked layout serves x, y and z (cubic grid: identical shapes and
+    plans); ms per x/y/z step, CUDA events, after 3 warm-up steps."""
+    import paper_2411_13532_b200 as T
+    sys_, st = operator(T, args, n)
+    part = T.SubdomainPartition((n,))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234 + 3)
+    u = torch.randn((n * n // SZ, n, SZ), dtype=torch.float64, device="cuda", generator=g)
+    out = torch.empty_like(u)
+    for _ in range(3 * 3):
+        T.run_distd2(sys_, u, part=part, stencil=st, out=out)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(3 * steps):
+        T.run_distd2(sys_, u, part=part, stencil=st, out=out)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    del u, out
+    torch.cuda.empty_cache()
+    return {"n": n, "ms_per_step": round(ms, 4),
+            "gbs": round(3 * BYTES_PER_POINT * n ** 3 / (ms * 1e-3) / 1e9, 1),
+            "steps": steps, "path": T.get_plan(sys_, st, part).path}
 
 
 def run_e2e(args, torch, T, sys_, st, part, fields, n):
@@ -291,6 +324,8 @@ def run_multi(args, torch):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # T1(1024^3) on rank 0's GPU (the others wait at the barrier)
+    t1 = t1_anchor(args, torch) if rank == 0 and n == 1024 and not args.no_t1 else None
     dist.barrier()
     evs = [{d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for d in "xyz"} for _ in range(args.steps)]
@@ -344,6 +379,10 @@ def run_multi(args, torch):
                          "algorithmic_bytes_per_launch": BYTES_PER_POINT * local_points},
             "e2e": e2e, "gpu_launches": (1 if fused else 3) * 3 * args.steps,
             "clocks": clocks, "cpu_baseline": None,
+            "t1_1024": t1,
+            # north star: E(N) = T1(1024^3) / (N * T_N), same box, same operator
+            "efficiency_vs_t1": (round(t1["ms_per_step"] / (world * ms_step), 4)
+                                 if t1 else None),
         }
     dist.barrier()
     solver.close()
@@ -502,6 +541,7 @@ def main():
     ap.add_argument("--open", action="store_true", help="non-periodic (d1 only)")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-groups", type=int, default=256, help="max SZ-groups per CPU worker")
+    ap.add_argument("--no-t1", action="store_true", help="skip the T1(1024^3) anchor")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -207,6 +207,22 @@ def decouple_fused(u_ext, co, st):
     return d
 
 
+def decouple_unfused(d_rhs, co):
+    """distributed.py:242-254 -- the sweeps of Alg. 6 on an already-built RHS
+    (the test seam; bit-equal to decouple_fused on build_rhs, D12)."""
+    m = len(co["f"])
+    w, f, r = co["w"], co["f"], co["r"]
+    d = np.empty_like(d_rhs)
+    d[0] = d_rhs[0] * r[0]
+    d[1] = d_rhs[1] * r[1]
+    for j in range(2, m):
+        d[j] = (d_rhs[j] - r[j] * d[j - 1]) * f[j]
+    for j in range(m - 3, 0, -1):
+        d[j] = d[j] - w[j] * d[j + 1]
+    d[0] = (d[0] - w[0] * d[1]) * f[0]
+    return d
+
+
 def solve_boundary_pair(d_last, d_first, s_c_last, s_a_first):
     """distributed.py:279-293 -- Cramer's rule on the 2x2 pair."""
     det = 1.0 - s_c_last * s_a_first

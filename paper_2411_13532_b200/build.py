@@ -20,7 +20,7 @@ LIB = os.path.join(LIBDIR, "libtds_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["tds_kernels.cu", "tds_tma.cu", "tds_dd.cu", "tds_transport.cu"]
+CU_SOURCES = ["tds_kernels.cu", "tds_tma.cu", "tds_dd.cu", "tds_transport.cu", "tds_cluster.cu"]
 CXX_SOURCES = ["plan.cpp", "capi.cpp"]
 
 

@@ -107,7 +107,13 @@ extern "C" int tds_solve(const tds_plan* p, const double* u, double* out, long l
         a.u = u;
         a.out = out;
         a.edge_mode = p->periodic ? tds::EDGE_WRAP : tds::EDGE_ZERO;
-        return tds::launch_fast(p->M, tds::MODE_SOLVE, p->uniform, a, tiles_of(lines), S(stream));
+        if (p->C <= tds::MAX_CHUNKS)
+            return tds::launch_fast(p->M, tds::MODE_SOLVE, p->uniform, a, tiles_of(lines),
+                                    S(stream));
+        // a line longer than one CTA holds: split over a thread-block cluster
+        // (k_tmc), else the plan's staged tables
+        if (tds::tmc_eligible(p->M, p->uniform, a)) return tds::launch_tmc(p->M, p->uniform, a, S(stream));
+        if (!p->has_staged) return set_err(TDS_ERR_UNSUPPORTED, "no kernel for this line length");
     }
     tds::StagedArgs a = staged_args(p, lines, sz);
     a.u = u;

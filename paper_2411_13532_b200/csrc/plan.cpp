@@ -232,6 +232,10 @@ vector<double> reduced(const ChunkSet& cs, int k0, int k1, bool wrap) {
     return R;
 }
 
+// Whole-line plans (rank == -1) may hold up to this many chunks: lines longer
+// than one CTA are split over a thread-block cluster (k_tmc, <= 8 CTAs).
+constexpr int MAX_CHUNKS_CLUSTER = 8 * tds::MAX_CHUNKS;
+
 int pick_chunk(const vector<int>& blocks, int flags, bool rank_block = false) {
     if (flags & (TDS_FLAG_STRICT | TDS_FLAG_STAGED)) return 0;
     // A/B knob for per-rank blocks (fused kernel): TDS_RANK_CHUNK=32|16.
@@ -246,7 +250,8 @@ int pick_chunk(const vector<int>& blocks, int flags, bool rank_block = false) {
     long long total = 0;
     for (int m : blocks) total += m;
     for (int M : {first, 48 - first}) {
-        const int lim = M == 16 ? cmax : tds::MAX_CHUNKS;
+        const int lim = rank_block ? (M == 16 ? cmax : tds::MAX_CHUNKS)
+                                   : std::max(M == 16 ? cmax : tds::MAX_CHUNKS, MAX_CHUNKS_CLUSTER);
         bool ok = total / M <= lim;
         for (int m : blocks)
             if (m % M != 0) ok = false;
@@ -716,6 +721,65 @@ int plan_create_impl(const double* lower, const double* diag, const double* uppe
         det_prev[q] = det;
     }
 
+    // staged tables (reference-order kernels): the staged path itself, and
+    // the fallback of long-line fast plans when no cluster shape fits
+    auto build_staged = [&]() -> int {
+        int rc = TDS_OK;
+        if ((rc = upload(p, &p->d_st, g.st.data(), g.st.size()))) return rc;
+        if (P > 1) {
+            vector<const tds_rank_coeffs*> cos;
+            vector<double> bconst;
+            for (int k = 0; k < P; ++k) {
+                cos.push_back(&rcs[k]);
+                bconst.insert(bconst.end(), {rcs[k].sa[0], rcs[k].sc.back(), det_prev[k], det_next[k],
+                                             double(has_prev(k)), double(has_next(k))});
+            }
+            p->rc = rcs;
+            return staged_rank_tables(p, cos, offs, sizes, bconst);
+        }
+        // P == 1: thomas_solve / periodic_thomas_solve multipliers (serial.py:26-90)
+        vector<double> la = g.lower, lb = g.b, lc = g.upper;
+        vector<double> w(n, 0.0), cp(n, 0.0), z;
+        double gamma = 0.0;
+        if (g.periodic) {
+            gamma = -lb[0];
+            lb[0] = lb[0] - gamma;
+            lb[n - 1] = lb[n - 1] - lc[n - 1] * la[0] / gamma;
+        }
+        cp[0] = lc[0] / lb[0];
+        for (int i = 1; i < n; ++i) {
+            double den = lb[i] - la[i] * cp[i - 1];
+            if (std::fabs(den) <= p->pivot_floor)
+                return (set_err(TDS_ERR_SINGULAR_PIVOT,
+                                    fmt("pivot %.3e at row ", den) + std::to_string(i + 1)));
+            w[i] = 1.0 / den;
+            cp[i] = lc[i] * w[i];
+        }
+        p->th_b0 = lb[0];
+        if (g.periodic) {
+            z.assign(n, 0.0);
+            z[0] = gamma;
+            z[n - 1] = lc[n - 1];
+            z[0] /= lb[0];
+            for (int i = 1; i < n; ++i) {
+                z[i] -= la[i] * z[i - 1];
+                z[i] *= w[i];
+            }
+            for (int i = n - 2; i >= 0; --i) z[i] -= cp[i] * z[i + 1];
+            double ql = la[0] / gamma;
+            double den = 1.0 + 1.0 * z[0] + ql * z[n - 1];
+            if (std::fabs(den) <= p->pivot_floor)
+                return (set_err(TDS_ERR_SINGULAR_CORRECTION, fmt("correction denominator %.3e", den)));
+            p->th_qlast = ql;
+            p->th_den = den;
+            if ((rc = upload(p, &p->d_thz, z.data(), z.size()))) return rc;
+        }
+        if ((rc = upload(p, &p->d_tha, la.data(), la.size()))) return rc;
+        if ((rc = upload(p, &p->d_thw, w.data(), w.size()))) return rc;
+        if ((rc = upload(p, &p->d_thcp, cp.data(), cp.size()))) return rc;
+        return TDS_OK;
+    };
+
     vector<int> blocks = (P == 1) ? vector<int>{n} : sizes;
     const int M = pick_chunk(blocks, flags);
     if (M > 0) {
@@ -771,70 +835,20 @@ int plan_create_impl(const double* lower, const double* diag, const double* uppe
             }
         }
         if ((rc = upload_H(p, H, gv))) return fail(rc);
+        if (cs.C > tds::MAX_CHUNKS) {   // cluster kernel (k_tmc) or the staged fallback
+            if ((rc = build_staged())) return fail(rc);
+            p->has_staged = 1;
+        }
         *out = p;
         return TDS_OK;
     }
 
     // --------------------------- staged path ---------------------------------
     p->path = TDS_PATH_STAGED;
-    if ((rc = upload(p, &p->d_st, g.st.data(), g.st.size()))) return fail(rc);
-    if (P > 1) {
-        vector<const tds_rank_coeffs*> cos;
-        vector<double> bconst;
-        for (int k = 0; k < P; ++k) {
-            cos.push_back(&rcs[k]);
-            bconst.insert(bconst.end(), {rcs[k].sa[0], rcs[k].sc.back(), det_prev[k], det_next[k],
-                                         double(has_prev(k)), double(has_next(k))});
-        }
-        p->rc = rcs;
-        if ((rc = staged_rank_tables(p, cos, offs, sizes, bconst))) return fail(rc);
-        *out = p;
-        return TDS_OK;
-    }
-    // P == 1: thomas_solve / periodic_thomas_solve multipliers (serial.py:26-90)
-    vector<double> la = g.lower, lb = g.b, lc = g.upper;
-    vector<double> w(n, 0.0), cp(n, 0.0), z;
-    double gamma = 0.0;
-    if (g.periodic) {
-        gamma = -lb[0];
-        lb[0] = lb[0] - gamma;
-        lb[n - 1] = lb[n - 1] - lc[n - 1] * la[0] / gamma;
-    }
-    cp[0] = lc[0] / lb[0];
-    for (int i = 1; i < n; ++i) {
-        double den = lb[i] - la[i] * cp[i - 1];
-        if (std::fabs(den) <= p->pivot_floor)
-            return fail(set_err(TDS_ERR_SINGULAR_PIVOT,
-                                fmt("pivot %.3e at row ", den) + std::to_string(i + 1)));
-        w[i] = 1.0 / den;
-        cp[i] = lc[i] * w[i];
-    }
-    p->th_b0 = lb[0];
-    if (g.periodic) {
-        z.assign(n, 0.0);
-        z[0] = gamma;
-        z[n - 1] = lc[n - 1];
-        z[0] /= lb[0];
-        for (int i = 1; i < n; ++i) {
-            z[i] -= la[i] * z[i - 1];
-            z[i] *= w[i];
-        }
-        for (int i = n - 2; i >= 0; --i) z[i] -= cp[i] * z[i + 1];
-        double ql = la[0] / gamma;
-        double den = 1.0 + 1.0 * z[0] + ql * z[n - 1];
-        if (std::fabs(den) <= p->pivot_floor)
-            return fail(set_err(TDS_ERR_SINGULAR_CORRECTION, fmt("correction denominator %.3e", den)));
-        p->th_qlast = ql;
-        p->th_den = den;
-        if ((rc = upload(p, &p->d_thz, z.data(), z.size()))) return fail(rc);
-    }
-    if ((rc = upload(p, &p->d_tha, la.data(), la.size()))) return fail(rc);
-    if ((rc = upload(p, &p->d_thw, w.data(), w.size()))) return fail(rc);
-    if ((rc = upload(p, &p->d_thcp, cp.data(), cp.size()))) return fail(rc);
+    if ((rc = build_staged())) return fail(rc);
     *out = p;
     return TDS_OK;
 }
-
 }  // namespace tds
 
 extern "C" int tds_plan_query(const tds_plan* p, tds_plan_info* info) {

@@ -188,6 +188,7 @@ struct tds_plan {
     int* d_bsize = nullptr;
     double* d_bconst = nullptr;
     int nb = 1;
+    int has_staged = 0;   // fast plan that also carries staged tables (long lines)
     // P=1 Thomas tables
     double* d_tha = nullptr;
     double* d_thw = nullptr;

@@ -30,7 +30,37 @@ namespace tds {
 
 using namespace dev;
 
-template <int M, int MODE, int TAB, int TLT, int SZC>
+// Output row i of a chunk after the Alg. 7 substitution (the value
+// chunk_store_any writes), for the staged bulk-store path.
+template <int M, int TAB>
+__device__ __forceinline__ double chunk_row(const FastArgs& p, const double* __restrict__ tb,
+                                            const double (&d)[M], double F, double L, int i,
+                                            int chunk) {
+    if (i == 0) return F;
+    if (i == M - 1) return L;
+    double sa, sc;
+    if (TAB == TAB_EDGES && p.special_first && chunk == 0) {
+        sa = p.e_first.c[i][8];
+        sc = p.e_first.c[i][9];
+    } else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1) {
+        sa = p.e_last.c[i][8];
+        sc = p.e_last.c[i][9];
+    } else if (TAB != TAB_GLOBAL) {
+        sa = p.ut.sa[i];
+        sc = p.ut.sc[i];
+    } else {
+        sa = tb[i * NCOEF + 8];
+        sc = tb[i * NCOEF + 9];
+    }
+    return fma(-sc, L, fma(-sa, F, d[i]));
+}
+
+// BST (bulk stores; 32-line tiles of an sz = 32 field, where a chunk's M rows
+// of its 32 lines are one contiguous M x 256-byte block): each warp writes
+// its chunk 8 rows at a time into one of two 2 KiB shared-memory staging
+// buffers, and one lane hands each 2 KiB to the TMA engine
+// (cp.async.bulk shared -> global), instead of 32 warp-wide STG per thread.
+template <int M, int MODE, int TAB, int TLT, int SZC, int BST = 0>
 __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) {
     constexpr bool UNIFORM = TAB != TAB_GLOBAL;
     const FastArgs& p = A.f;
@@ -52,8 +82,8 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     // TAB_GLOBAL: the block's per-row table (shared by every line) is staged
     // in shared memory once per CTA when it fits
     double* stab = sY + 2 * ybuf;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(
-        stab + (TAB == TAB_GLOBAL && A.tab_smem ? (size_t)rows * NCOEF : 0));
+    double* sStage = stab + (TAB == TAB_GLOBAL && A.tab_smem ? (size_t)rows * NCOEF : 0);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sStage + (BST ? (size_t)blockDim.x * 16 : 0));
     if (TAB == TAB_GLOBAL && A.tab_smem)
         for (int k = t; k < rows * NCOEF; k += blockDim.x) stab[k] = __ldg(p.tab + k);
     const double* __restrict__ tb =
@@ -157,15 +187,38 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
                              F, L);
         else
             chunk_bounds<TLT>(p.Hp + (size_t)chunk * K, Y, K, lane, nullptr, nullptr, F, L);
-        if (valid)
+        if constexpr (BST != 0) {
+            static_assert(TLT == 32 && SZC == 32 && M % 8 == 0, "bulk stores: sz = 32 tiles");
+            // every line of a tile is valid (lines = groups x 32)
+            double* stg = sStage + (size_t)(t >> 5) * 512;
+            double* gout = p.out + (line >> 5) * (long long)rows * 32 + (long long)r0 * 32;
+#pragma unroll
+            for (int s8 = 0; s8 < M / 8; ++s8) {
+                double* buf = stg + (s8 & 1) * 256;
+                if (lane == 0) bulk_wait_read<1>();      // this buffer's last copy has read it
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    buf[r * 32 + lane] = chunk_row<M, TAB>(p, tb, d, F, L, s8 * 8 + r, chunk);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    bulk_store(gout + s8 * 256, buf, 8 * 32 * sizeof(double));
+                    bulk_commit();
+                }
+            }
+        } else if (valid) {
             chunk_store_any<M, TAB>(p, tb, p.out + line_base_t<SZC>(line, p.rows, p.sz), sz, r0, d, F,
-                                        L, A.store_cs != 0, chunk);
+                                    L, A.store_cs != 0, chunk);
+        }
     }
+    if constexpr (BST != 0)
+        if (lane == 0) bulk_wait_all();                // staging reads done before exit
 }
 
 namespace {
 
-template <int M, int MODE, int UNI, int TLT, int SZC = 0>
+template <int M, int MODE, int UNI, int TLT, int SZC = 0, int BST = 0>
 int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     TmaArgs A;
     A.f = a;
@@ -183,11 +236,12 @@ int launch_tma_t(const FastArgs& a, TileCfg cfg, cudaStream_t s) {
     A.tab_smem = UNI == TAB_GLOBAL && smem + tab_bytes <= 227 * 1024 &&
                  !(getenv("TDS_TAB_SMEM") && getenv("TDS_TAB_SMEM")[0] == '0');
     if (A.tab_smem) smem += tab_bytes;
-    const void* fn = reinterpret_cast<const void*>(k_tma<M, MODE, UNI, TLT, SZC>);
+    if (BST) smem += (size_t)threads * 16 * sizeof(double);   // 2 x 8 rows per warp
+    const void* fn = reinterpret_cast<const void*>(k_tma<M, MODE, UNI, TLT, SZC, BST>);
     if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_tma)"))) return rc;
     const long long grid = persistent_grid(fn, threads, smem, A.f.items, 0);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_tma does not fit on an SM");
-    k_tma<M, MODE, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_tma<M, MODE, UNI, TLT, SZC, BST><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_tma launch");
 }
 
@@ -203,10 +257,22 @@ int launch_tma_m(const FastArgs& a, cudaStream_t s) {
     const bool want32 = e32 ? e32[0] == '1' : true;
     if (want32 && MODE == MODE_SOLVE && a.sz % 32 == 0 && a.chunks * 32 <= 512 &&
         (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 <= 200 * 1024)
+    {
         // compile-time lane width: 5147 vs 4980 GB/s for open d/dx at 512^3
-        return getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '0'
-                   ? launch_tma_t<M, MODE, UNI, 32>(a, TileCfg{32, 1}, s)
-                   : launch_tma_t<M, MODE, UNI, 32, 32>(a, TileCfg{32, 1}, s);
+        // (the compile-time width is only right for sz == 32 itself)
+        if (a.sz != 32 || (getenv("TDS_SZC_TMA") && getenv("TDS_SZC_TMA")[0] == '0'))
+            return launch_tma_t<M, MODE, UNI, 32>(a, TileCfg{32, 1}, s);
+        // bulk (TMA-engine) stores through shared-memory staging: A/B knob
+        // TDS_BULK_ST=1 (needs an sz = 32 field, 16-byte aligned output)
+        const char* eb = getenv("TDS_BULK_ST");
+        const bool bulk = eb && eb[0] == '1' && a.sz == 32 &&
+                          reinterpret_cast<uintptr_t>(a.out) % 16 == 0 &&
+                          (size_t)a.rows * 32 * 8 + 4 * a.chunks * 32 * 8 +
+                                  (size_t)a.chunks * 32 * 16 * 8 <= 220 * 1024;
+        if constexpr (MODE == MODE_SOLVE)
+            if (bulk) return launch_tma_t<M, MODE, UNI, 32, 32, 1>(a, TileCfg{32, 1}, s);
+        return launch_tma_t<M, MODE, UNI, 32, 32>(a, TileCfg{32, 1}, s);
+    }
     if (cfg.tl == 8) return launch_tma_t<M, MODE, UNI, 8>(a, cfg, s);
     // compile-time lane width (sz = 32): a win for k_dd / k_dd2 (+9% at
     // m = 512 in loopback) and 32-line tiles, but measured slower for 16-line

@@ -39,4 +39,8 @@ int ensure_smem(const void* fn, size_t smem, const char* what);
 long long persistent_grid(const void* fn, int threads, size_t smem, long long items,
                           int max_ctas);
 
+// long lines split over a thread-block cluster (tds_cluster.cu)
+bool tmc_eligible(int M, bool uniform, const FastArgs& a);
+int launch_tmc(int M, bool uniform, const FastArgs& a, cudaStream_t s);
+
 }  // namespace tds

@@ -27,8 +27,8 @@ def main():
     import tds  # noqa: F401  (the reference)
     from tds.compact import (assemble, second_derivative_scheme,
                              sixth_order_first_derivative)
-    from tds.distributed import (BoundaryPair, StencilCoeffs, decouple_fused,
-                                 local_slice, preprocess, run_distd2,
+    from tds.distributed import (BoundaryPair, StencilCoeffs, build_rhs, decouple_fused,
+                                 decouple_unfused, local_slice, preprocess, run_distd2,
                                  solve_boundary_pair, substitute)
     from tds.layout import LayoutDescriptor, pack
     from tds.serial import periodic_thomas_solve, thomas_solve
@@ -84,6 +84,11 @@ def main():
     d = decouple_fused(u_ext, co, StencilCoeffs(st))
     out.update(dec_lower=s.lower, dec_diag=s.diag, dec_upper=s.upper,
                dec_stencil=st, dec_uext=u_ext, dec_d=d)
+    # decouple_unfused on the reference's own build_rhs (distributed.py:
+    # 227-254; D12: bit-equal to decouple_fused). No new random draws, so
+    # every other fixture is unchanged.
+    rhs_built = build_rhs(u_ext, StencilCoeffs(st))
+    out.update(decu_rhs=rhs_built, decu_d=decouple_unfused(rhs_built, co))
     u_s = rng.standard_normal(4)
     u_e = rng.standard_normal(4)
     out.update(sub_us=u_s, sub_ue=u_e, sub_out=substitute(d, co, u_s, u_e))

@@ -133,8 +133,12 @@ def test_phase_functions_bitwise(golden):
         assert ul[0] == want[0] and uf[0] == want[1]
     with pytest.raises(T.SingularPair):
         T.solve_boundary_pair(T.BoundaryPair(np.ones(1), np.ones(1), 1.0, 1.0))
-    # decouple_unfused == decouple_fused on the built RHS (reference D12)
-    dz = T.decouple_fused(np.zeros((20, 3)), co, T.identity_stencil(16))
+    # decouple_unfused on the reference's own build_rhs output (distributed.py:
+    # 242-254), bit-equal to the reference and to decouple_fused (D12)
+    du = T.decouple_unfused(g["decu_rhs"], co)
+    np.testing.assert_array_equal(du, g["decu_d"])
+    np.testing.assert_array_equal(du, d)
+    dz = T.decouple_unfused(np.zeros((16, 3)), co)
     np.testing.assert_array_equal(dz, np.zeros((16, 3)))
 
 
@@ -333,3 +337,38 @@ def test_pack_unpack_reorder_ragged_extents(sz):
         np.testing.assert_array_equal(T.unpack(f), cart)
         for d2 in "xyz":
             np.testing.assert_array_equal(T.unpack(T.reorder(f, d2)), cart)
+
+
+@pytest.mark.parametrize("n,p,periodic,kind,sz", [
+    (2048, 1, True, "d1", 32), (2048, 1, False, "d1", 32), (4096, 1, True, "d1", 32),
+    (8192, 1, True, "d1", 32), (8192, 1, False, "d1", 16), (2048, 4, True, "d1", 32),
+    (4096, 2, False, "d1", 16), (2048, 1, True, "d2", 32), (2048, 1, True, "rd", 32),
+    (4096, 1, False, "rd", 16), (2048, 1, True, "d1", 8), (2048, 2, True, "d1", 4)])
+def test_long_lines_cluster_kernel_vs_oracle(n, p, periodic, kind, sz):
+    """Lines of 2048..8192 rows (reference bench.py:178-219 sweeps n up to
+    8192): the fast 16 B/pt path with each line split over a thread-block
+    cluster (k_tmc, reduced rhs exchanged through distributed shared memory).
+    sz = 4 has no 8-lane tiles and takes the plan's staged tables instead
+    (reference operation order: bit-identical)."""
+    rng = np.random.default_rng(n + 7 * p + sz)
+    if kind == "rd":
+        lo = 0.3 * (2 * rng.random(n) - 1)
+        di = 2 + rng.random(n)
+        up = 0.3 * (2 * rng.random(n) - 1)
+        st = rng.standard_normal((n, 5))
+    else:
+        lo, di, up, st = O.assemble(kind, n, 2 * np.pi / n, periodic)
+    fld = rng.standard_normal((2, n, sz))
+    sizes = O.balanced_sizes(n, p)
+    want = O.run_distd2(lo, di, up, periodic, fld, st, sizes)
+    s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
+    part = T.SubdomainPartition(sizes)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", T.NotDominantWarning)
+        plan = T.get_plan(s, T.StencilCoeffs(st), part)
+        got = T.run_distd2(s, fld, part=part, stencil=T.StencilCoeffs(st))
+    assert plan.path == "fast" and plan.info.chunks > 32
+    if sz % 8:
+        np.testing.assert_array_equal(got, want)
+    else:
+        assert O.rel_linf(got, want) <= TOL

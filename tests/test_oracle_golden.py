@@ -38,6 +38,9 @@ def test_decouple_substitute_pair_bitwise(golden):
     co = O.preprocess(g["dec_lower"], g["dec_diag"], g["dec_upper"])
     d = O.decouple_fused(g["dec_uext"], co, g["dec_stencil"])
     np.testing.assert_array_equal(d, g["dec_d"])
+    # decouple_unfused on the reference's build_rhs (D12), and build_rhs itself
+    np.testing.assert_array_equal(O.build_rhs(g["dec_uext"], g["dec_stencil"]), g["decu_rhs"])
+    np.testing.assert_array_equal(O.decouple_unfused(g["decu_rhs"], co), g["decu_d"])
     np.testing.assert_array_equal(O.substitute(d, co, g["sub_us"], g["sub_ue"]),
                                   g["sub_out"])
     for row, want in zip(g["pair_in"], g["pair_out"]):

@@ -23,8 +23,9 @@ def main():
     ap.add_argument("--points", type=float, default=2 ** 27)
     ap.add_argument("--op", default="d1")
     ap.add_argument("--open", action="store_true")
-    args, extra = ap.parse_known_args()
-    for kv in extra:
+    kvs = [a for a in sys.argv[1:] if "=" in a and not a.startswith("-")]
+    args = ap.parse_args([a for a in sys.argv[1:] if a not in kvs])
+    for kv in kvs:
         k, v = kv.split("=", 1)
         os.environ[k] = v
     for n in args.n:
