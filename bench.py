@@ -115,9 +115,12 @@ class Clocks:
 def operator(T, args, n):
     """The solved operator: 6th-order compact d/dx (default) or d2/dx2
     (compact.py:49-56), periodic unless --open (one-sided closures,
-    compact.py:59-96; d/dx only, as in the reference)."""
+    compact.py:59-96; the open d2/dx2 is the closure="one-sided" extension,
+    the reference has none)."""
     scheme = (T.sixth_order_first_derivative if args.operator == "d1"
               else T.second_derivative_scheme)(2 * np.pi / n)
+    if args.open and args.operator == "d2":
+        return T.assemble(scheme, n, periodic=False, closure="one-sided")
     return T.assemble(scheme, n, periodic=not args.open)
 
 
@@ -538,7 +541,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=0, help="grid extent (default 512 / 1024)")
     ap.add_argument("--operator", default="d1", choices=["d1", "d2"])
-    ap.add_argument("--open", action="store_true", help="non-periodic (d1 only)")
+    ap.add_argument("--open", action="store_true", help="non-periodic (one-sided closures)")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-groups", type=int, default=256, help="max SZ-groups per CPU worker")
     ap.add_argument("--no-t1", action="store_true", help="skip the T1(1024^3) anchor")

@@ -78,26 +78,33 @@ int tds_last_error_rank(void);
  * periodic; system.py:31-51), its width-5 RHS stencil (n x 5 row-major,
  * NULL = identity; distributed.py:71-116) and a partition of the n rows
  * into `rank_count` blocks `sizes` (system.py:115-155).
+ * stencil_shift (NULL = none) is an EXTENSION for one-sided closures that
+ * need more than the width-5 window (the open d2/dx2 operator; the
+ * reference has none, compact.py:79-81): row j's weights apply to
+ * u[j + o + stencil_shift[j]], o = -2..2. Non-zero shifts are allowed only
+ * on rows 0, 1 (0..2) and n-2, n-1 (-2..0) of an open line (n >= 8).
  *   rank == -1 : this device runs the whole operator, all ranks emulated
  *                (replaces distributed.run_distd2, distributed.py:399-449);
  *   rank == k  : this device owns rank k's rows only (replaces the per-rank
  *                preprocess + distd2_solve, distributed.py:144-199,327-366).
  * Host-side, O(n + C^3): runs Alg. 5 (preprocess) per rank and per chunk and
  * uploads the coefficient tables with cudaMemcpy on the current device.
+ * SYNCHRONOUS.
  */
 int tds_plan_create(const double* lower, const double* diag, const double* upper,
-                    int periodic, const double* stencil, int n,
+                    int periodic, const double* stencil, const int* stencil_shift, int n,
                     const int* sizes, int rank_count, int rank, int flags,
                     tds_plan** out);
 /* Per-rank plan from rank-local data only, the reference's per-rank view:
  * a, b, c, stencil are rank k's local_slice bands (m rows; a[0] couples to
  * the previous rank's last row, c[m-1] to the next rank's first row; open
- * edges 0) and stencil rows; prev_sc_last / next_sa_first are the cached
+ * edges 0) and stencil rows (+ optional shifts, as above, on the rows of an
+ * edge without a neighbour); prev_sc_last / next_sa_first are the cached
  * neighbour couplings of share_pair_coeffs (distributed.py:308-324, D16). */
 int tds_plan_create_local(const double* a, const double* b, const double* c,
-                          const double* stencil, int m, int has_prev, int has_next,
-                          double prev_sc_last, double next_sa_first, int flags,
-                          tds_plan** out);
+                          const double* stencil, const int* stencil_shift, int m,
+                          int has_prev, int has_next, double prev_sc_last,
+                          double next_sa_first, int flags, tds_plan** out);
 int tds_plan_destroy(tds_plan* plan);
 int tds_plan_query(const tds_plan* plan, tds_plan_info* info);
 
@@ -196,9 +203,11 @@ int tds_peer_access(int peer_device);
  * functions take them. Coefficient arrays (stencil m x 5, w, f, r, s_a, s_c
  * of length m) are DEVICE arrays too: no allocation, copy or host
  * synchronisation per call. */
-/* decouple_fused: u_ext (m+4, lanes) -> d (m, lanes); distributed.py:257-276 */
-int tds_decouple_fused(const double* u_ext, const double* stencil, const double* w,
-                       const double* f, const double* r, double* d, int m,
+/* decouple_fused: u_ext (m+4, lanes) -> d (m, lanes); distributed.py:257-276.
+ * shift4: NULL, or the HOST array of the window shifts of rows 0, 1, m-2,
+ * m-1 (tds_plan_create's stencil_shift extension). */
+int tds_decouple_fused(const double* u_ext, const double* stencil, const int* shift4,
+                       const double* w, const double* f, const double* r, double* d, int m,
                        long long lanes, void* stream);
 /* substitute: d (m, lanes) -> out (m, lanes); distributed.py:296-305 */
 int tds_substitute(const double* d, const double* s_a, const double* s_c,

@@ -12,6 +12,10 @@ results are bit-identical to the reference (NumPy ufuncs round every
 product/sum; no FMA). Parity is PINNED: `tests/test_oracle_golden.py` checks
 every function here bit-for-bit against fixtures produced by importing the
 reference itself (`tests/golden/make_golden.py`, committed with its output).
+One exception, marked where it lives: the open d2/dx2 closures
+(`assemble_open_d2`, shifted stencil windows) restate a B200-side EXTENSION
+the reference does not have (it raises, compact.py:79-81) -- PARITY UNPINNED,
+validated by order of accuracy instead (tests/test_open_d2.py).
 
 Reference anchors (file:line under /root/reference/pkg/src/tds):
   system.py:148-155  SubdomainPartition.balanced     -> balanced_sizes
@@ -120,6 +124,37 @@ def assemble(kind, n, h, periodic=True):
     return lower, diag, upper, st
 
 
+# Open d2/dx2 closures -- a B200-side EXTENSION: the reference raises
+# NotImplementedError for non-periodic second derivatives (compact.py:79-81),
+# so these rows are PARITY UNPINNED against the reference; they are validated
+# by their order of accuracy (tests/test_open_d2.py). Row 0: explicit
+# one-sided 5-point formula (offsets 0..4, third-order truncation, no LHS
+# coupling); row 1: the fourth-order Pade scheme beta = 1/10 with
+# 6/5 (u0 - 2 u1 + u2) / h^2; mirrored at the end. Row 0 / n-1 reach past
+# the width-5 window: their stencil window is shifted by +2 / -2.
+D2_EDGE0_W = np.array([35.0 / 12.0, -26.0 / 3.0, 19.0 / 2.0, -14.0 / 3.0, 11.0 / 12.0])
+D2_EDGE1_BETA = 0.1
+D2_EDGE1_W = np.array([0.0, 1.2, -2.4, 1.2, 0.0])
+
+
+def assemble_open_d2(n, h):
+    """-> (lower, diag, upper, stencil(n,5), shift(n,)) of the open d2/dx2."""
+    order, alpha, a_w, b_w = SCHEMES["d2"]
+    lower = np.full(n, alpha)
+    diag = np.ones(n)
+    upper = np.full(n, alpha)
+    st = np.tile(interior_weights(order, a_w, b_w, h), (n, 1))
+    shift = np.zeros(n, dtype=np.int32)
+    h2 = h * h
+    lower[0], upper[0], st[0], shift[0] = 0.0, 0.0, D2_EDGE0_W / h2, 2
+    lower[1] = upper[1] = D2_EDGE1_BETA
+    st[1] = D2_EDGE1_W / h2
+    lower[n - 2] = upper[n - 2] = D2_EDGE1_BETA
+    st[n - 2] = D2_EDGE1_W / h2
+    lower[n - 1], upper[n - 1], st[n - 1], shift[n - 1] = 0.0, 0.0, D2_EDGE0_W[::-1] / h2, -2
+    return lower, diag, upper, st, shift
+
+
 # ----------------------------------------------------------- distributed.py
 
 def local_slice(lower, diag, upper, periodic, sizes, k):
@@ -175,32 +210,39 @@ def preprocess(a, b, c, pivot_floor=PIVOT_FLOOR):
                 dropped_first=float(drop_first), dropped_last=float(drop_last))
 
 
-def _stencil(u_ext, row, j):
-    """distributed.py:205-208 -- strict left-to-right sum of 5 products."""
+def _stencil(u_ext, row, j, s=0):
+    """distributed.py:205-208 -- strict left-to-right sum of 5 products.
+    s: window shift of the row (the B200 extension for one-sided closures,
+    not in the reference: row j reads u_ext[j+s .. j+s+4])."""
+    j = j + s
     return ((((row[0] * u_ext[j] + row[1] * u_ext[j + 1]) + row[2] * u_ext[j + 2])
              + row[3] * u_ext[j + 3]) + row[4] * u_ext[j + 4])
 
 
-def build_rhs(u_ext, st):
+def _sh(shift, j):
+    return 0 if shift is None else int(shift[j])
+
+
+def build_rhs(u_ext, st, shift=None):
     """distributed.py:233-239 -- (m+4, lanes) -> (m, lanes)."""
     m = u_ext.shape[0] - 4
     out = np.empty((m,) + u_ext.shape[1:])
     for j in range(m):
-        out[j] = _stencil(u_ext, st[j], j)
+        out[j] = _stencil(u_ext, st[j], j, _sh(shift, j))
     return out
 
 
-def decouple_fused(u_ext, co, st):
+def decouple_fused(u_ext, co, st, shift=None):
     """Alg. 6, distributed.py:257-276 (row kernels :211-224)."""
     m = len(co["f"])
     if u_ext.shape[0] != m + 4:
         raise ValueError("expected m+4 positions including halo")
     w, f, r = co["w"], co["f"], co["r"]
     d = np.empty((m,) + u_ext.shape[1:])
-    d[0] = _stencil(u_ext, st[0], 0) * r[0]
-    d[1] = _stencil(u_ext, st[1], 1) * r[1]
+    d[0] = _stencil(u_ext, st[0], 0, _sh(shift, 0)) * r[0]
+    d[1] = _stencil(u_ext, st[1], 1, _sh(shift, 1)) * r[1]
     for j in range(2, m):
-        d[j] = (_stencil(u_ext, st[j], j) - r[j] * d[j - 1]) * f[j]
+        d[j] = (_stencil(u_ext, st[j], j, _sh(shift, j)) - r[j] * d[j - 1]) * f[j]
     for j in range(m - 3, 0, -1):
         d[j] = d[j] - w[j] * d[j + 1]
     d[0] = (d[0] - w[0] * d[1]) * f[0]
@@ -296,7 +338,7 @@ def periodic_thomas_solve(a, b, c, rhs, pivot_floor=PIVOT_FLOOR):
 
 # ------------------------------------------------------------- the operator
 
-def _serial_solve(lower, diag, upper, periodic, field, st):
+def _serial_solve(lower, diag, upper, periodic, field, st, shift=None):
     """distributed.py:380-396 -- P=1: stencil then (periodic) Thomas."""
     groups, n, sz = field.shape
     u = _lanes(field)
@@ -308,7 +350,7 @@ def _serial_solve(lower, diag, upper, periodic, field, st):
         ext[:HALO] = 0.0
         ext[HALO + n:] = 0.0
     ext[HALO:HALO + n] = u
-    rhs = np.ascontiguousarray(build_rhs(ext, st).T)
+    rhs = np.ascontiguousarray(build_rhs(ext, st, shift).T)
     if periodic:
         sol = periodic_thomas_solve(lower, diag, upper, rhs).T
     else:
@@ -317,7 +359,7 @@ def _serial_solve(lower, diag, upper, periodic, field, st):
     return sol.reshape(n, groups, sz).transpose(1, 0, 2).copy()
 
 
-def _rank_solve(lower, diag, upper, periodic, field, st, sizes):
+def _rank_solve(lower, diag, upper, periodic, field, st, sizes, shift=None):
     """distributed.py:327-366 + 399-449 for P>1, ranks run one after the
     other: round 1 (halo) and round 2 (boundary rows) are plain array
     lookups into the neighbour's block, with the same path/ring topology as
@@ -344,7 +386,8 @@ def _rank_solve(lower, diag, upper, periodic, field, st, sizes):
         ext[:HALO] = 0.0 if pk is None else _lanes(blocks[pk][:, sizes[pk] - HALO:, :])
         ext[HALO:HALO + m] = _lanes(blocks[k])
         ext[HALO + m:] = 0.0 if nk is None else _lanes(blocks[nk][:, :HALO, :])
-        ds.append(decouple_fused(ext, co[k], st[offs[k]:offs[k] + m]))
+        ds.append(decouple_fused(ext, co[k], st[offs[k]:offs[k] + m],
+                                 None if shift is None else shift[offs[k]:offs[k] + m]))
     # round 2 + boundary pairs + substitution (distributed.py:345-366)
     outs = []
     for k in range(p):
@@ -367,8 +410,9 @@ def _rank_solve(lower, diag, upper, periodic, field, st, sizes):
 
 
 def run_distd2(lower, diag, upper, periodic, field, stencil=None,
-               sizes=None, rank_count=1):
-    """distributed.py:399-449 -- global (G, n, sz) in, (G, n, sz) out."""
+               sizes=None, rank_count=1, shift=None):
+    """distributed.py:399-449 -- global (G, n, sz) in, (G, n, sz) out.
+    shift: per-row stencil window shifts (B200 extension, see _stencil)."""
     field = np.asarray(field, dtype=np.float64)
     groups, n, sz = field.shape
     if sizes is None:
@@ -379,8 +423,8 @@ def run_distd2(lower, diag, upper, periodic, field, stencil=None,
         stencil = np.zeros((n, 5))
         stencil[:, 2] = 1.0
     if len(sizes) == 1:
-        return _serial_solve(lower, diag, upper, periodic, field, stencil)
-    return _rank_solve(lower, diag, upper, periodic, field, stencil, tuple(sizes))
+        return _serial_solve(lower, diag, upper, periodic, field, stencil, shift)
+    return _rank_solve(lower, diag, upper, periodic, field, stencil, tuple(sizes), shift)
 
 
 def run_distd2_threaded(lower, diag, upper, periodic, field, stencil=None,

@@ -53,9 +53,9 @@ SIGNATURES = {
     "tds_abi_version": (_I, []),
     "tds_last_error": (ctypes.c_char_p, []),
     "tds_last_error_rank": (_I, []),
-    "tds_plan_create": (_I, [_DP, _DP, _DP, _I, _DP, _I, _IP, _I, _I, _I,
+    "tds_plan_create": (_I, [_DP, _DP, _DP, _I, _DP, _IP, _I, _IP, _I, _I, _I,
                              ctypes.POINTER(_P)]),
-    "tds_plan_create_local": (_I, [_DP, _DP, _DP, _DP, _I, _I, _I, _D, _D, _I,
+    "tds_plan_create_local": (_I, [_DP, _DP, _DP, _DP, _IP, _I, _I, _I, _D, _D, _I,
                                    ctypes.POINTER(_P)]),
     "tds_plan_destroy": (_I, [_P]),
     "tds_plan_query": (_I, [_P, ctypes.POINTER(PlanInfo)]),
@@ -65,7 +65,7 @@ SIGNATURES = {
     "tds_halo_rows": (_I, [_P, _P, _P, _P, _LL, _I, _P]),
     "tds_boundary_rows": (_I, [_P, _P, _P, _P, _P, _P, _P, _LL, _I, _P]),
     "tds_finish": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _LL, _I, _P]),
-    "tds_decouple_fused": (_I, [_P, _P, _P, _P, _P, _P, _I, _LL, _P]),
+    "tds_decouple_fused": (_I, [_P, _P, _IP, _P, _P, _P, _P, _I, _LL, _P]),
     "tds_substitute": (_I, [_P, _P, _P, _P, _P, _P, _I, _LL, _P]),
     "tds_boundary_pair": (_I, [_P, _P, _D, _D, _P, _P, _LL, _P]),
     "tds_thomas": (_I, [_DP, _DP, _DP, _I, _P, _P, _I, _LL, _I, _D, _P]),
@@ -128,6 +128,13 @@ def dptr(arr):
 
 def f64(x):
     return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def iptr(arr):
+    """Pointer to a C-contiguous int32 NumPy array, or None."""
+    if arr is None:
+        return None
+    return arr.ctypes.data_as(_IP)
 
 
 _EXC = {

@@ -53,6 +53,8 @@ tds::FastArgs fast_args(const tds_plan* p, long long lines, int sz) {
     a.special_last = p->special_last;
     a.dd_defer16 = p->dd_defer[0];
     a.dd_defer8 = p->dd_defer[1];
+    for (int i = 0; i < 4; ++i) a.sh[i] = p->sh[i];
+    a.has_shift = p->sh[0] | p->sh[1] | p->sh[2] | p->sh[3];
     return a;
 }
 
@@ -82,6 +84,8 @@ tds::StagedArgs staged_args(const tds_plan* p, long long lines, int sz) {
     a.th_qlast = p->th_qlast;
     a.th_den = p->th_den;
     a.periodic = p->periodic;
+    for (int i = 0; i < 4; ++i) a.sh[i] = p->sh[i];
+    a.has_shift = p->sh[0] | p->sh[1] | p->sh[2] | p->sh[3];
     return a;
 }
 
@@ -201,13 +205,21 @@ extern "C" int tds_finish(const tds_plan* p, const double* u, const double* halo
 // ------------------------------------------------------------ phase kernels
 
 
-extern "C" int tds_decouple_fused(const double* u_ext, const double* stencil, const double* w,
-                                  const double* f, const double* r, double* d, int m,
-                                  long long lanes, void* stream) {
+extern "C" int tds_decouple_fused(const double* u_ext, const double* stencil,
+                                  const int* shift4, const double* w, const double* f,
+                                  const double* r, double* d, int m, long long lanes,
+                                  void* stream) {
     if (m < 4) return set_err(TDS_ERR_INVALID, "local block needs at least 4 rows");
     if (lanes > 0 && (!u_ext || !stencil || !w || !f || !r || !d))
         return set_err(TDS_ERR_INVALID, "null argument");
-    return tds::launch_decouple_pm(u_ext, stencil, w, f, r, d, m, lanes, S(stream));
+    int sh[4] = {0, 0, 0, 0};
+    if (shift4) {
+        for (int i = 0; i < 4; ++i) sh[i] = shift4[i];
+        if (sh[0] < 0 || sh[0] > 2 || sh[1] < 0 || sh[1] > 2 || sh[2] > 0 || sh[2] < -2 ||
+            sh[3] > 0 || sh[3] < -2 || (m < 8 && (sh[0] | sh[1] | sh[2] | sh[3])))
+            return set_err(TDS_ERR_INVALID, "bad stencil shifts");
+    }
+    return tds::launch_decouple_pm(u_ext, stencil, sh, w, f, r, d, m, lanes, S(stream));
 }
 
 extern "C" int tds_substitute(const double* d, const double* s_a, const double* s_c,

@@ -147,6 +147,7 @@ struct Global {
     vector<double> a, b, c;   // effective bands (system.py:57-71)
     vector<double> lower, upper;
     vector<double> st;        // n x 5
+    vector<int> sh;           // per-row window shift of the stencil (0: offsets -2..2)
     int n;
     bool periodic;
 };
@@ -484,7 +485,7 @@ int staged_rank_tables(tds_plan* p, const vector<const tds_rank_coeffs*>& cos,
 }
 
 Global make_global(const double* lower, const double* diag, const double* upper, bool periodic,
-                   const double* stencil, int n) {
+                   const double* stencil, int n, const int* shift = nullptr) {
     Global g;
     g.n = n;
     g.periodic = periodic;
@@ -504,7 +505,40 @@ Global make_global(const double* lower, const double* diag, const double* upper,
         else
             g.st[size_t(j) * 5 + 2] = 1.0;   // identity_stencil, distributed.py:112-116
     }
+    g.sh.assign(n, 0);
+    if (shift) g.sh.assign(shift, shift + n);
     return g;
+}
+
+// Stencil window shifts (an extension for one-sided closures that need more
+// than the width-5 window, e.g. the open d2/dx2 operator): row j uses
+// u[j + o + sh_j], o = -2..2. Allowed only on the first two rows of a line
+// start without a neighbour (0 <= sh <= 2) and the last two rows of a line end
+// without one (-2 <= sh <= 0), so every kernel can take the shifted window
+// from the rows it already holds.
+int check_shift(const Global& g, bool start_open, bool end_open, int rank) {
+    const int n = g.n;
+    for (int j = 0; j < n; ++j) {
+        const int s = g.sh[j];
+        if (s == 0) continue;
+        const bool front = j < 2 && start_open && s > 0 && s <= 2;
+        const bool back = j >= n - 2 && end_open && s < 0 && s >= -2;
+        if (!(front || back) || n < 8)
+            return set_err(TDS_ERR_INVALID,
+                           "stencil shifts are allowed only on the first / last two rows of an "
+                           "open line (0..2 / -2..0), got " + std::to_string(s) + " at row " +
+                               std::to_string(j),
+                           rank);
+    }
+    return TDS_OK;
+}
+
+void set_block_shifts(tds_plan* p, const Global& blk) {
+    const int m = blk.n;
+    p->sh[0] = blk.sh[0];
+    p->sh[1] = blk.sh[1];
+    p->sh[2] = blk.sh[m - 2];
+    p->sh[3] = blk.sh[m - 1];
 }
 
 double margin_of(const Global& g) {
@@ -595,9 +629,9 @@ tds_plan* new_plan(int n, bool periodic, int P, int rank, int flags) {
 }  // namespace
 
 extern "C" int tds_plan_create_local(const double* a, const double* b, const double* c,
-                                     const double* stencil, int m, int has_prev, int has_next,
-                                     double prev_sc_last, double next_sa_first, int flags,
-                                     tds_plan** out) {
+                                     const double* stencil, const int* stencil_shift, int m,
+                                     int has_prev, int has_next, double prev_sc_last,
+                                     double next_sa_first, int flags, tds_plan** out) {
     if (!out) return set_err(TDS_ERR_INVALID, "null plan output");
     *out = nullptr;
     if (!a || !b || !c) return set_err(TDS_ERR_INVALID, "null band pointer");
@@ -605,15 +639,18 @@ extern "C" int tds_plan_create_local(const double* a, const double* b, const dou
     for (int j = 0; j < m; ++j)
         if (b[j] == 0.0) return set_err(TDS_ERR_INVALID, "diagonal entries must be nonzero");
     // bands are taken as given: a[0] / c[m-1] are the external couplings
-    Global loc = make_global(a, b, c, true, stencil, m);
+    Global loc = make_global(a, b, c, true, stencil, m, stencil_shift);
     loc.periodic = false;
+    int rc = check_shift(loc, !has_prev, !has_next, -1);
+    if (rc) return rc;
     tds_plan* p = new_plan(m, false, 2, 0, flags);
     p->block_off = 0;
     p->block_rows = m;
     p->sizes = {m};
     p->offs = {0};
     p->margin = margin_of(loc);
-    int rc = build_local(p, loc, has_prev != 0, has_next != 0, prev_sc_last, next_sa_first, -1);
+    set_block_shifts(p, loc);
+    rc = build_local(p, loc, has_prev != 0, has_next != 0, prev_sc_last, next_sa_first, -1);
     if (rc) {
         tds_plan_destroy(p);
         return rc;
@@ -623,16 +660,17 @@ extern "C" int tds_plan_create_local(const double* a, const double* b, const dou
 }
 
 extern "C" int tds_plan_create(const double* lower, const double* diag, const double* upper,
-                               int periodic, const double* stencil, int n, const int* sizes_in,
-                               int P, int rank, int flags, tds_plan** out) {
-    return tds::plan_create_impl(lower, diag, upper, periodic, stencil, n, sizes_in, P, rank,
-                                 flags, tds::PIVOT_FLOOR, out);
+                               int periodic, const double* stencil, const int* stencil_shift,
+                               int n, const int* sizes_in, int P, int rank, int flags,
+                               tds_plan** out) {
+    return tds::plan_create_impl(lower, diag, upper, periodic, stencil, stencil_shift, n,
+                                 sizes_in, P, rank, flags, tds::PIVOT_FLOOR, out);
 }
 
 namespace tds {
 int plan_create_impl(const double* lower, const double* diag, const double* upper, int periodic,
-                     const double* stencil, int n, const int* sizes_in, int P, int rank,
-                     int flags, double pivot_floor, tds_plan** out) {
+                     const double* stencil, const int* stencil_shift, int n, const int* sizes_in,
+                     int P, int rank, int flags, double pivot_floor, tds_plan** out) {
     if (!out) return set_err(TDS_ERR_INVALID, "null plan output");
     *out = nullptr;
     if (!lower || !diag || !upper) return set_err(TDS_ERR_INVALID, "null band pointer");
@@ -653,7 +691,8 @@ int plan_create_impl(const double* lower, const double* diag, const double* uppe
     for (int j = 0; j < n; ++j)
         if (diag[j] == 0.0) return set_err(TDS_ERR_INVALID, "diagonal entries must be nonzero");
 
-    const Global g = make_global(lower, diag, upper, periodic != 0, stencil, n);
+    const Global g = make_global(lower, diag, upper, periodic != 0, stencil, n, stencil_shift);
+    if (int rs = check_shift(g, !g.periodic, !g.periodic, -1)) return rs;
     tds_plan* p = new_plan(n, g.periodic, P, rank, flags);
     p->pivot_floor = pivot_floor;
     p->sizes = sizes;
@@ -690,10 +729,12 @@ int plan_create_impl(const double* lower, const double* diag, const double* uppe
         const int m = sizes[rank];
         vector<double> st(g.st.begin() + size_t(offs[rank]) * 5,
                           g.st.begin() + size_t(offs[rank] + m) * 5);
-        Global loc = make_global(a.data(), b.data(), c.data(), true, st.data(), m);
+        vector<int> shl(g.sh.begin() + offs[rank], g.sh.begin() + offs[rank] + m);
+        Global loc = make_global(a.data(), b.data(), c.data(), true, st.data(), m, shl.data());
         loc.periodic = false;
         p->block_off = 0;
         p->block_rows = m;
+        set_block_shifts(p, loc);
         double psc = has_prev(rank) ? rcs[prev_of(rank)].sc.back() : 0.0;
         double nsa = has_next(rank) ? rcs[next_of(rank)].sa[0] : 0.0;
         double md = p->max_dropped;
@@ -710,6 +751,7 @@ int plan_create_impl(const double* lower, const double* diag, const double* uppe
     p->block_off = 0;
     p->block_rows = n;
     p->rc = rcs;
+    set_block_shifts(p, g);
     vector<double> det_prev(P, 1.0), det_next(P, 1.0);
     for (int k = 0; k < P && P > 1; ++k) {
         if (!has_next(k)) continue;
@@ -926,10 +968,6 @@ constexpr size_t THOMAS_CACHE = 16;
 }  // namespace
 
 namespace tds {
-int plan_create_impl(const double* lower, const double* diag, const double* upper, int periodic,
-                     const double* stencil, int n, const int* sizes_in, int P, int rank,
-                     int flags, double pivot_floor, tds_plan** out);
-
 int thomas_plan(const double* lower, const double* diag, const double* upper, int periodic, int n,
                 double pivot_floor, const tds_plan** out) {
     if (!lower || !diag || !upper || !out) return set_err(TDS_ERR_INVALID, "null argument");
@@ -954,7 +992,7 @@ int thomas_plan(const double* lower, const double* diag, const double* upper, in
         }
     int one = n;
     tds_plan* p = nullptr;
-    int rc = plan_create_impl(lower, diag, upper, periodic, nullptr, n, &one, 1, -1,
+    int rc = plan_create_impl(lower, diag, upper, periodic, nullptr, nullptr, n, &one, 1, -1,
                               TDS_FLAG_STAGED, pivot_floor, &p);
     if (rc) return rc;
     if (g_thomas.size() >= THOMAS_CACHE) {

@@ -118,11 +118,32 @@ __device__ __forceinline__ long long halo_base_t(long long line, int sz) {
     return halo_base(line, sz);
 }
 
+// Window value v[i + o + s] of chunk row i for a stencil window shifted by s
+// (one-sided closures; plan.cpp check_shift): s in 1..2 only on rows 0, 1 of
+// a line start, s in -2..-1 only on its last two rows. i and o are
+// compile-time after unrolling, so every candidate is a register.
+template <int M>
+__device__ __forceinline__ double wv(const double (&v)[M + 4], int i, int o, int s) {
+    if (i < 2) return s == 2 ? v[i + o + 2] : (s == 1 ? v[i + o + 1] : v[i + o]);
+    if (i >= M - 2) return s == -2 ? v[i + o - 2] : (s == -1 ? v[i + o - 1] : v[i + o]);
+    return v[i + o];
+}
+
+// shifts of chunk rows 0, 1, M-2, M-1 (non-zero only in the block's first /
+// last chunk)
+struct RowShift {
+    int f0, f1, b0, b1;
+    __device__ __forceinline__ int of(int i, int M) const {
+        return i == 0 ? f0 : (i == 1 ? f1 : (i == M - 2 ? b0 : (i == M - 1 ? b1 : 0)));
+    }
+};
+
 // Fused width-5 stencil + Alg. 6 (reference distributed.py:257-276) on one
 // chunk of M rows held in registers: v = rows r0-2 .. r0+M+1, d = decoupled.
-template <int M, bool UNIFORM>
+template <int M, bool UNIFORM, bool SHIFT = false>
 __device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __restrict__ tb,
-                                             const double (&v)[M + 4], double (&d)[M]) {
+                                             const double (&v)[M + 4], double (&d)[M],
+                                             RowShift rs = RowShift{0, 0, 0, 0}) {
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         double s0, s1, s2, s3, s4, f, r;
@@ -141,11 +162,12 @@ __device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __
             s0 = c01.x; s1 = c01.y; s2 = c23.x; s3 = c23.y; s4 = c4f.x; f = c4f.y;
             r = tr[6];
         }
-        double rhs = s0 * v[i];
-        rhs = fma(s1, v[i + 1], rhs);
-        rhs = fma(s2, v[i + 2], rhs);
-        rhs = fma(s3, v[i + 3], rhs);
-        rhs = fma(s4, v[i + 4], rhs);
+        const int sh = SHIFT ? rs.of(i, M) : 0;
+        double rhs = s0 * wv<M>(v, i, 0, sh);
+        rhs = fma(s1, wv<M>(v, i, 1, sh), rhs);
+        rhs = fma(s2, wv<M>(v, i, 2, sh), rhs);
+        rhs = fma(s3, wv<M>(v, i, 3, sh), rhs);
+        rhs = fma(s4, wv<M>(v, i, 4, sh), rhs);
         if (i < 2) d[i] = rhs * r;
         else d[i] = fma(-r, d[i - 1], rhs) * f;
     }
@@ -312,17 +334,18 @@ __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __r
 // Sweeps / store of a special (edge) chunk of a uniform plan: per-row
 // coefficients from an EdgeTable in kernel-parameter space, so they stay
 // constant-bank operands like the uniform table (no global loads to hoist).
-template <int M>
+template <int M, bool SHIFT = false>
 __device__ __forceinline__ void edge_sweeps(const EdgeTable& T, const double (&v)[M + 4],
-                                            double (&d)[M]) {
+                                            double (&d)[M], RowShift rs = RowShift{0, 0, 0, 0}) {
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         const double* c = T.c[i];
-        double rhs = c[0] * v[i];
-        rhs = fma(c[1], v[i + 1], rhs);
-        rhs = fma(c[2], v[i + 2], rhs);
-        rhs = fma(c[3], v[i + 3], rhs);
-        rhs = fma(c[4], v[i + 4], rhs);
+        const int sh = SHIFT ? rs.of(i, M) : 0;
+        double rhs = c[0] * wv<M>(v, i, 0, sh);
+        rhs = fma(c[1], wv<M>(v, i, 1, sh), rhs);
+        rhs = fma(c[2], wv<M>(v, i, 2, sh), rhs);
+        rhs = fma(c[3], wv<M>(v, i, 3, sh), rhs);
+        rhs = fma(c[4], wv<M>(v, i, 4, sh), rhs);
         if (i < 2) d[i] = rhs * c[6];
         else d[i] = fma(-c[6], d[i - 1], rhs) * c[5];
     }
@@ -350,15 +373,38 @@ __device__ __forceinline__ void edge_store(const EdgeTable& T, double* __restric
     }
 }
 
-// Chunk sweeps / store of a (possibly edge-special) chunk.
+// Chunk sweeps / store of a (possibly edge-special) chunk. Plans with
+// shifted stencil rows (p.has_shift, uniform across the grid) take a second
+// copy of the sweeps that applies the shifts; every other plan runs the
+// unshifted code.
+template <int M, int TAB, bool SHIFT>
+__device__ __forceinline__ void chunk_sweeps_sel(const FastArgs& p, const double* __restrict__ tb,
+                                                 const double (&v)[M + 4], double (&d)[M],
+                                                 int chunk, RowShift rs) {
+    if (TAB == TAB_EDGES && p.special_first && chunk == 0) edge_sweeps<M, SHIFT>(p.e_first, v, d, rs);
+    else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
+        edge_sweeps<M, SHIFT>(p.e_last, v, d, rs);
+    else chunk_sweeps<M, TAB != TAB_GLOBAL, SHIFT>(p, tb, v, d, rs);
+}
+
 template <int M, int TAB>
 __device__ __forceinline__ void chunk_sweeps_any(const FastArgs& p, const double* __restrict__ tb,
                                                  const double (&v)[M + 4], double (&d)[M],
                                                  int chunk) {
-    if (TAB == TAB_EDGES && p.special_first && chunk == 0) edge_sweeps<M>(p.e_first, v, d);
-    else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
-        edge_sweeps<M>(p.e_last, v, d);
-    else chunk_sweeps<M, TAB != TAB_GLOBAL>(p, tb, v, d);
+    if (p.has_shift) {
+        RowShift rs{0, 0, 0, 0};
+        if (chunk == 0) {
+            rs.f0 = p.sh[0];
+            rs.f1 = p.sh[1];
+        }
+        if (chunk == p.chunks - 1) {
+            rs.b0 = p.sh[2];
+            rs.b1 = p.sh[3];
+        }
+        chunk_sweeps_sel<M, TAB, true>(p, tb, v, d, chunk, rs);
+    } else {
+        chunk_sweeps_sel<M, TAB, false>(p, tb, v, d, chunk, RowShift{0, 0, 0, 0});
+    }
 }
 
 template <int M, int TAB>

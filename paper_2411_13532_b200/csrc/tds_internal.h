@@ -69,6 +69,8 @@ struct FastArgs {
     int has_prev, has_next;
     int dd_defer16, dd_defer8;   // deferred-edge fused kernel allowed (see plan.cpp)
     int special_first, special_last;   // uniform plan whose first / last chunk uses e_first / e_last
+    int has_shift;         // some stencil row is shifted (one-sided closures)
+    int sh[4];             // window shift of block rows 0, 1, rows-2, rows-1
     double sa_first, sc_last, prev_sc_last, next_sa_first, det_prev, det_next;
     UniformTable ut;
     EdgeTable e_first, e_last;
@@ -105,6 +107,8 @@ struct StagedArgs {
     const double* th_z;
     double th_b0, th_qlast, th_den;
     int periodic;
+    int has_shift;
+    int sh[4];              // window shift of block rows 0, 1, rows-2, rows-1
 };
 
 // launchers (tds_kernels.cu)
@@ -118,7 +122,7 @@ int launch_staged_finish(const StagedArgs& a, cudaStream_t s);
 int launch_thomas(const StagedArgs& a, cudaStream_t s);
 int launch_halo_rows(const double* u, double* first2, double* last2, long long lines,
                      int rows, int sz, cudaStream_t s);
-int launch_decouple_pm(const double* u_ext, const double* st, const double* w,
+int launch_decouple_pm(const double* u_ext, const double* st, const int* sh4, const double* w,
                        const double* f, const double* r, double* d, int m,
                        long long lanes, cudaStream_t s);
 int launch_substitute_pm(const double* d, const double* sa, const double* sc,
@@ -136,8 +140,8 @@ struct tds_plan;
 namespace tds {
 // tds_plan_create with an explicit pivot floor (plan.cpp)
 int plan_create_impl(const double* lower, const double* diag, const double* upper, int periodic,
-                     const double* stencil, int n, const int* sizes_in, int P, int rank,
-                     int flags, double pivot_floor, tds_plan** out);
+                     const double* stencil, const int* stencil_shift, int n, const int* sizes_in,
+                     int P, int rank, int flags, double pivot_floor, tds_plan** out);
 }  // namespace tds
 
 // Rank-level DistD2 coefficients (distributed.py:43-68), dropped couplings kept.
@@ -195,6 +199,9 @@ struct tds_plan {
     double* d_thcp = nullptr;
     double* d_thz = nullptr;
     double th_b0 = 1, th_qlast = 0, th_den = 1;
+    // stencil window shifts of block rows 0, 1, rows-2, rows-1 (one-sided
+    // closures that reach past the width-5 window: open d2/dx2)
+    int sh[4] = {0, 0, 0, 0};
 
     std::vector<void*> allocs;
 };

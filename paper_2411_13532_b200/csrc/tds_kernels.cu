@@ -195,6 +195,10 @@ static int launch_fast_t(const FastArgs& a, long long tiles, cudaStream_t s) {
 int launch_fast(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
                 cudaStream_t s) {
     if (tma_eligible(M, a)) return launch_tma(M, mode, uniform, a, tiles, s);
+    if (a.has_shift)
+        return set_err(TDS_ERR_UNSUPPORTED,
+                       "shifted (one-sided) stencil rows need the TMA kernels: sz % 8 == 0 and a "
+                       "16-byte aligned field");
     // k_fast has no per-chunk table switch: edge-special plans use the table path
     if (a.special_first || a.special_last) uniform = false;
 #define DISPATCH_MODE(MM)                                                             \
@@ -242,6 +246,24 @@ __device__ __forceinline__ double fetch(const StagedArgs& p, const double* ub, l
     return 0.0;
 }
 
+// window shift of block row `row` (one-sided closures, plan.cpp check_shift)
+__device__ __forceinline__ int row_shift(const StagedArgs& p, int row) {
+    if (!p.has_shift) return 0;
+    if (row < 2) return p.sh[row];
+    if (row >= p.rows - 2) return p.sh[4 - (p.rows - row)];
+    return 0;
+}
+
+// stencil row with a shifted window: sum over u[row + o + s], o = -2..2, in
+// the reference's left-to-right order (distributed.py:205-208)
+__device__ __forceinline__ double stencil_shifted(const StagedArgs& p, const double* c,
+                                                  const double* ub, long long hb, int row,
+                                                  int s) {
+    return stencil5(c, fetch(p, ub, hb, row - 2 + s), fetch(p, ub, hb, row - 1 + s),
+                    fetch(p, ub, hb, row + s), fetch(p, ub, hb, row + 1 + s),
+                    fetch(p, ub, hb, row + 2 + s));
+}
+
 // Alg. 6 decouple_fused per (line, block): distributed.py:257-276.
 __global__ void k_staged_decouple(const StagedArgs p) {
     const long long line = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -257,8 +279,10 @@ __global__ void k_staged_decouple(const StagedArgs p) {
     double dprev = 0.0;
     for (int j = 0; j < m; ++j) {
         const double u4 = fetch(p, ub, hb, off + j + 2);
-        const double rhs = stencil5(p.st + (size_t)(off + j) * 5, u0, u1, u2, u3, u4);
         const int row = off + j;
+        const int sh = row_shift(p, row);
+        const double rhs = sh ? stencil_shifted(p, p.st + (size_t)row * 5, ub, hb, row, sh)
+                              : stencil5(p.st + (size_t)row * 5, u0, u1, u2, u3, u4);
         double dj = (j < 2) ? mul(rhs, p.r[row]) : mul(sub(rhs, mul(p.r[row], dprev)), p.f[row]);
         ob[row * sz] = dj;
         dprev = dj;
@@ -330,7 +354,9 @@ __global__ void k_thomas(const StagedArgs p) {
     double dprev = 0.0;
     for (int j = 0; j < n; ++j) {
         const double u4 = fetch(p, ub, hb, j + 2);
-        const double rhs = stencil5(p.st + (size_t)j * 5, u0, u1, u2, u3, u4);
+        const int sh = row_shift(p, j);
+        const double rhs = sh ? stencil_shifted(p, p.st + (size_t)j * 5, ub, hb, j, sh)
+                              : stencil5(p.st + (size_t)j * 5, u0, u1, u2, u3, u4);
         const double dj = (j == 0) ? dvd(rhs, p.th_b0)
                                    : mul(sub(rhs, mul(p.th_a[j], dprev)), p.th_w[j]);
         ob[j * sz] = dj;
@@ -394,17 +420,29 @@ int launch_halo_rows(const double* u, double* first2, double* last2, long long l
 }
 
 // position-major phase kernels (reference phase functions)
+struct Shift4 {
+    int s[4];   // window shifts of rows 0, 1, m-2, m-1
+};
+
 __global__ void k_decouple_pm(const double* __restrict__ ue, const double* __restrict__ st,
-                              const double* __restrict__ w, const double* __restrict__ f,
-                              const double* __restrict__ r, double* __restrict__ d, int m,
-                              long long lanes) {
+                              const Shift4 sh4, const double* __restrict__ w,
+                              const double* __restrict__ f, const double* __restrict__ r,
+                              double* __restrict__ d, int m, long long lanes) {
     const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= lanes) return;
     double u0 = ue[l], u1 = ue[lanes + l], u2 = ue[2 * lanes + l], u3 = ue[3 * lanes + l];
     double dprev = 0.0;
     for (int j = 0; j < m; ++j) {
         const double u4 = ue[(long long)(j + 4) * lanes + l];
-        const double rhs = stencil5(st + (size_t)j * 5, u0, u1, u2, u3, u4);
+        const int sh = j < 2 ? sh4.s[j] : (j >= m - 2 ? sh4.s[4 - (m - j)] : 0);
+        // shifted window: u_ext rows j + sh .. j + sh + 4 (ue row = position + 2)
+        const double rhs =
+            sh ? stencil5(st + (size_t)j * 5, ue[(long long)(j + sh) * lanes + l],
+                          ue[(long long)(j + sh + 1) * lanes + l],
+                          ue[(long long)(j + sh + 2) * lanes + l],
+                          ue[(long long)(j + sh + 3) * lanes + l],
+                          ue[(long long)(j + sh + 4) * lanes + l])
+               : stencil5(st + (size_t)j * 5, u0, u1, u2, u3, u4);
         const double dj = (j < 2) ? mul(rhs, r[j]) : mul(sub(rhs, mul(r[j], dprev)), f[j]);
         d[(long long)j * lanes + l] = dj;
         dprev = dj;
@@ -444,10 +482,13 @@ __global__ void k_pair(const double* __restrict__ dl, const double* __restrict__
     uf[l] = dvd(sub(b, mul(sa, a)), det);
 }
 
-int launch_decouple_pm(const double* u_ext, const double* st, const double* w, const double* f,
-                       const double* r, double* d, int m, long long lanes, cudaStream_t s) {
+int launch_decouple_pm(const double* u_ext, const double* st, const int* sh4, const double* w,
+                       const double* f, const double* r, double* d, int m, long long lanes,
+                       cudaStream_t s) {
     if (lanes == 0) return TDS_OK;
-    k_decouple_pm<<<(unsigned)((lanes + 127) / 128), 128, 0, s>>>(u_ext, st, w, f, r, d, m, lanes);
+    Shift4 sh{{sh4[0], sh4[1], sh4[2], sh4[3]}};
+    k_decouple_pm<<<(unsigned)((lanes + 127) / 128), 128, 0, s>>>(u_ext, st, sh, w, f, r, d, m,
+                                                                  lanes);
     return cuda_check(cudaGetLastError(), "k_decouple_pm launch");
 }
 int launch_substitute_pm(const double* d, const double* sa, const double* sc, const double* us,

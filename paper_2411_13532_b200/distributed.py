@@ -54,20 +54,46 @@ class DistCoeffs:
 
 @dataclass(frozen=True)
 class StencilCoeffs:
-    """Per-row width-5 RHS weights, offsets -2..+2 (distributed.py:71-86)."""
+    """Per-row width-5 RHS weights, offsets -2..+2 (distributed.py:71-86).
+
+    `shift` (extension, default None): per-row window shift s_j, row j's
+    weights then apply to u[j + o + s_j], o = -2..2. It carries one-sided
+    closures that need points beyond the width-5 window (the open d2/dx2
+    operator, assemble(..., closure="one-sided")); only rows 0, 1 (0..2)
+    and n-2, n-1 (-2..0) of an open line may be shifted."""
 
     c: np.ndarray
     halo_depth: int = HALO_DEPTH
+    shift: np.ndarray = None
 
     def __post_init__(self):
         arr = np.ascontiguousarray(self.c, dtype=np.float64)
         if arr.ndim != 2 or arr.shape[1] != 5:
             raise ValueError(f"stencil must be (n, 5), got {arr.shape}")
         object.__setattr__(self, "c", arr)
+        if self.shift is not None:
+            sh = np.ascontiguousarray(self.shift, dtype=np.int32)
+            if sh.shape != (arr.shape[0],):
+                raise ValueError(f"stencil shift must be ({arr.shape[0]},), got {sh.shape}")
+            if np.any(np.abs(sh) > 2):
+                raise ValueError("stencil shifts must lie in -2..2")
+            object.__setattr__(self, "shift", sh if np.any(sh) else None)
 
     @property
     def n(self):
         return self.c.shape[0]
+
+    def rows(self, start, stop):
+        """The stencil of rows [start, stop) (a rank's local stencil)."""
+        sh = None if self.shift is None else self.shift[start:stop]
+        return StencilCoeffs(self.c[start:stop], self.halo_depth, sh)
+
+    def shift4(self):
+        """Window shifts of rows 0, 1, n-2, n-1 (int32), or None."""
+        if self.shift is None:
+            return None
+        n = self.n
+        return np.ascontiguousarray(self.shift[[0, 1, n - 2, n - 1]], dtype=np.int32)
 
 
 @dataclass(frozen=True)
@@ -229,28 +255,30 @@ class Plan:
             pass
 
     @classmethod
-    def create(cls, sys, stencil_c, sizes, rank=-1, flags=0):
+    def create(cls, sys, stencil_c, sizes, rank=-1, flags=0, shift=None):
         torch = _torch()
         lo, di, up = (N.f64(x) for x in (sys.lower, sys.diag, sys.upper))
         st = None if stencil_c is None else N.f64(stencil_c)
+        sh = None if shift is None else np.ascontiguousarray(shift, dtype=np.int32)
         sz = (ctypes.c_int * len(sizes))(*sizes)
         h = ctypes.c_void_p()
         N.check(N.lib().tds_plan_create(
             N.dptr(lo), N.dptr(di), N.dptr(up), int(bool(sys.periodic)),
-            None if st is None else N.dptr(st), sys.n, sz, len(sizes), rank, flags,
+            None if st is None else N.dptr(st), N.iptr(sh), sys.n, sz, len(sizes), rank, flags,
             ctypes.byref(h)), rank_count=len(sizes))
         return cls(h, len(sizes), torch.cuda.current_device())
 
     @classmethod
     def create_local(cls, local_sys, stencil_c, has_prev, has_next, prev_sc_last,
-                     next_sa_first, flags=0):
+                     next_sa_first, flags=0, shift=None):
         torch = _torch()
         a, b, c = (N.f64(x) for x in (local_sys.lower, local_sys.diag, local_sys.upper))
         st = None if stencil_c is None else N.f64(stencil_c)
+        sh = None if shift is None else np.ascontiguousarray(shift, dtype=np.int32)
         h = ctypes.c_void_p()
         N.check(N.lib().tds_plan_create_local(
-            N.dptr(a), N.dptr(b), N.dptr(c), None if st is None else N.dptr(st), local_sys.n,
-            int(has_prev), int(has_next), float(prev_sc_last or 0.0),
+            N.dptr(a), N.dptr(b), N.dptr(c), None if st is None else N.dptr(st), N.iptr(sh),
+            local_sys.n, int(has_prev), int(has_next), float(prev_sc_last or 0.0),
             float(next_sa_first or 0.0), flags, ctypes.byref(h)))
         return cls(h, 2, torch.cuda.current_device())
 
@@ -274,15 +302,16 @@ def get_plan(sys, stencil, part, rank=-1, arithmetic="fast", chunk_rows=None):
     chunk_rows=16 asks for 16-row chunks (TDS_FLAG_CHUNK16)."""
     torch = _torch()
     st = None if stencil is None else stencil.c
+    sh = None if stencil is None else stencil.shift
     key = (sys.lower.tobytes(), sys.diag.tobytes(), sys.upper.tobytes(), bool(sys.periodic),
-           None if st is None else st.tobytes(), part.local_sizes, rank, arithmetic,
-           chunk_rows, torch.cuda.current_device())
+           None if st is None else st.tobytes(), None if sh is None else sh.tobytes(),
+           part.local_sizes, rank, arithmetic, chunk_rows, torch.cuda.current_device())
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
             _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
         flags = _flags(arithmetic) | (N.TDS_FLAG_CHUNK16 if chunk_rows == 16 else 0)
-        plan = Plan.create(sys, st, part.local_sizes, rank, flags)
+        plan = Plan.create(sys, st, part.local_sizes, rank, flags, shift=sh)
         _PLAN_CACHE[key] = plan
     return plan
 
@@ -389,8 +418,9 @@ def _rank_group(sys, stencil, part, devices, arithmetic, warn_not_dominant, fres
     if fresh:
         return _RankGroup(sys, stencil, part, devs, arithmetic, warn_not_dominant)
     st = None if stencil is None else stencil.c
+    sh = None if stencil is None or stencil.shift is None else stencil.shift.tobytes()
     key = (sys.lower.tobytes(), sys.diag.tobytes(), sys.upper.tobytes(), bool(sys.periodic),
-           None if st is None else st.tobytes(), part.local_sizes, devs, arithmetic)
+           None if st is None else st.tobytes(), sh, part.local_sizes, devs, arithmetic)
     g = _GROUPS.get(key)
     if g is None:
         if len(_GROUPS) >= _GROUPS_MAX:
@@ -608,8 +638,9 @@ def decouple_fused(u_ext, coeffs, stencil):
     dev = fld.t.device
     st = _dev(stencil.c, dev)[:m].contiguous()
     w, f, r = (_dev(x, dev) for x in (coeffs.w, coeffs.f, coeffs.r))
-    N.check(N.lib().tds_decouple_fused(fld.ptr, *(ctypes.c_void_p(x.data_ptr())
-                                                  for x in (st, w, f, r)),
+    sh4 = stencil.rows(0, m).shift4() if stencil.n != m else stencil.shift4()
+    st_p, w_p, f_p, r_p = (ctypes.c_void_p(x.data_ptr()) for x in (st, w, f, r))
+    N.check(N.lib().tds_decouple_fused(fld.ptr, st_p, N.iptr(sh4), w_p, f_p, r_p,
                                        ctypes.c_void_p(d.data_ptr()), m,
                                        _lanes_of(u_ext.shape), _stream_handle()))
     return fld.give(d)

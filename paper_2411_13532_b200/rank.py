@@ -94,9 +94,11 @@ class DistD2Rank:
                                  warn_not_dominant=warn_not_dominant)
         prev_sc, next_sa = share_scalars(ctx, self.coeffs.s_a[0], self.coeffs.s_c[-1])
         self.pair_coeffs = (prev_sc, next_sa)
-        st = None if stencil is None else stencil.c[off:off + self.m]
-        self.plan = Plan.create_local(local_sys, st, ctx.has_prev, ctx.has_next, prev_sc,
-                                      next_sa, _flags(arithmetic))
+        loc_st = None if stencil is None else stencil.rows(off, off + self.m)
+        self.plan = Plan.create_local(local_sys, None if loc_st is None else loc_st.c,
+                                      ctx.has_prev, ctx.has_next, prev_sc, next_sa,
+                                      _flags(arithmetic),
+                                      shift=None if loc_st is None else loc_st.shift)
         self._bufs = {}
         self._mail = {}
         self._epoch = 0

@@ -31,7 +31,8 @@ def main():
     for n in args.n:
         scheme = (T.sixth_order_first_derivative if args.op == "d1"
                   else T.second_derivative_scheme)(2 * np.pi / n)
-        s, st = T.assemble(scheme, n, periodic=not args.open)
+        s, st = T.assemble(scheme, n, periodic=not args.open,
+                           closure="one-sided" if args.open and args.op == "d2" else None)
         groups = max(1, int(args.points) // (n * 32))
         u = torch.randn((groups, n, 32), dtype=torch.float64, device="cuda")
         out = torch.empty_like(u)
