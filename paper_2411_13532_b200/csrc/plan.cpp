@@ -355,13 +355,32 @@ int fast_tables(tds_plan* p, const Global& g, int M, ChunkSet& cs) {
         if (!chunk_is_ref(k)) uni = false;
     p->special_first = p->special_last = 0;
     if (uni && C >= 3) {
-        p->special_first = chunk_is_ref(0) ? 0 : 1;
-        p->special_last = chunk_is_ref(C - 1) ? 0 : 1;
+        // a shifted row makes its chunk special (its window differs)
+        auto shifted = [&](int k) {
+            for (int i = 0; i < M; ++i)
+                if (g.sh[p->block_off + k * M + i]) return true;
+            return false;
+        };
+        p->special_first = chunk_is_ref(0) && !shifted(0) ? 0 : 1;
+        p->special_last = chunk_is_ref(C - 1) && !shifted(C - 1) ? 0 : 1;
         for (int i = 0; i < M; ++i)
             for (int o = 0; o < tds::NCOEF; ++o) {
                 p->e_first.c[i][o] = tab[size_t(i) * tds::NCOEF + o];
                 p->e_last.c[i][o] = tab[size_t((C - 1) * M + i) * tds::NCOEF + o];
             }
+        // 7-tap rows 0, 1, M-2, M-1 of both edge chunks
+        auto fill7 = [&](tds::EdgeTable& E, int k) {
+            const int rows[4] = {0, 1, M - 2, M - 1};
+            for (int q = 0; q < 4; ++q) {
+                const int row = p->block_off + k * M + rows[q];
+                const int s = g.sh[row];
+                for (int j = 0; j < 7; ++j) E.x7[q][j] = 0.0;
+                for (int o = -2; o <= 2; ++o)
+                    E.x7[q][(q < 2 ? o + 2 : o + 4) + s] = g.st[size_t(row) * 5 + o + 2];
+            }
+        };
+        fill7(p->e_first, 0);
+        fill7(p->e_last, C - 1);
     } else if (uni) {
         for (int k = 0; k < C && uni; ++k)
             if (!chunk_is_ref(k)) uni = false;

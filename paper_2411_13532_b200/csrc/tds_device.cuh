@@ -130,13 +130,14 @@ __device__ __forceinline__ double wv(const double (&v)[M + 4], int i, int o, int
 }
 
 // shifts of chunk rows 0, 1, M-2, M-1 (non-zero only in the block's first /
-// last chunk)
+// last chunk). Plain scalars picked by the compile-time row index (a struct
+// with an accessor was demoted to local memory: an LDL at the head of the
+// edge warps' sweep chain, -11% for the whole kernel).
 struct RowShift {
     int f0, f1, b0, b1;
-    __device__ __forceinline__ int of(int i, int M) const {
-        return i == 0 ? f0 : (i == 1 ? f1 : (i == M - 2 ? b0 : (i == M - 1 ? b1 : 0)));
-    }
 };
+#define TDS_ROW_SHIFT(rs, i, M) \
+    ((i) == 0 ? (rs).f0 : ((i) == 1 ? (rs).f1 : ((i) == (M) - 2 ? (rs).b0 : ((i) == (M) - 1 ? (rs).b1 : 0))))
 
 // Fused width-5 stencil + Alg. 6 (reference distributed.py:257-276) on one
 // chunk of M rows held in registers: v = rows r0-2 .. r0+M+1, d = decoupled.
@@ -162,7 +163,7 @@ __device__ __forceinline__ void chunk_sweeps(const FastArgs& p, const double* __
             s0 = c01.x; s1 = c01.y; s2 = c23.x; s3 = c23.y; s4 = c4f.x; f = c4f.y;
             r = tr[6];
         }
-        const int sh = SHIFT ? rs.of(i, M) : 0;
+        const int sh = SHIFT ? TDS_ROW_SHIFT(rs, i, M) : 0;
         double rhs = s0 * wv<M>(v, i, 0, sh);
         rhs = fma(s1, wv<M>(v, i, 1, sh), rhs);
         rhs = fma(s2, wv<M>(v, i, 2, sh), rhs);
@@ -334,18 +335,31 @@ __device__ __forceinline__ void chunk_store(const FastArgs& p, const double* __r
 // Sweeps / store of a special (edge) chunk of a uniform plan: per-row
 // coefficients from an EdgeTable in kernel-parameter space, so they stay
 // constant-bank operands like the uniform table (no global loads to hoist).
-template <int M, bool SHIFT = false>
+// Sweeps of a special (edge) chunk of a uniform plan: per-row coefficients
+// from an EdgeTable in kernel-parameter space (constant-bank operands, no
+// loads to hoist). Rows 0, 1, M-2, M-1 use the table's 7-tap rows, which
+// carry any window shift (one-sided closures) as plain coefficients.
+template <int M>
 __device__ __forceinline__ void edge_sweeps(const EdgeTable& T, const double (&v)[M + 4],
-                                            double (&d)[M], RowShift rs = RowShift{0, 0, 0, 0}) {
+                                            double (&d)[M]) {
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         const double* c = T.c[i];
-        const int sh = SHIFT ? rs.of(i, M) : 0;
-        double rhs = c[0] * wv<M>(v, i, 0, sh);
-        rhs = fma(c[1], wv<M>(v, i, 1, sh), rhs);
-        rhs = fma(c[2], wv<M>(v, i, 2, sh), rhs);
-        rhs = fma(c[3], wv<M>(v, i, 3, sh), rhs);
-        rhs = fma(c[4], wv<M>(v, i, 4, sh), rhs);
+        double rhs;
+        if (i < 2 || i >= M - 2) {
+            const int q = i < 2 ? i : i - (M - 4);      // 0, 1 | 2, 3
+            const int b = i < 2 ? i : i - 2;            // first window row
+            const double* x = T.x7[q];
+            rhs = x[0] * v[b];
+#pragma unroll
+            for (int j = 1; j < 7; ++j) rhs = fma(x[j], v[b + j], rhs);
+        } else {
+            rhs = c[0] * v[i];
+            rhs = fma(c[1], v[i + 1], rhs);
+            rhs = fma(c[2], v[i + 2], rhs);
+            rhs = fma(c[3], v[i + 3], rhs);
+            rhs = fma(c[4], v[i + 4], rhs);
+        }
         if (i < 2) d[i] = rhs * c[6];
         else d[i] = fma(-c[6], d[i - 1], rhs) * c[5];
     }
@@ -373,38 +387,33 @@ __device__ __forceinline__ void edge_store(const EdgeTable& T, double* __restric
     }
 }
 
-// Chunk sweeps / store of a (possibly edge-special) chunk. Plans with
-// shifted stencil rows (p.has_shift, uniform across the grid) take a second
-// copy of the sweeps that applies the shifts; every other plan runs the
-// unshifted code.
-template <int M, int TAB, bool SHIFT>
-__device__ __forceinline__ void chunk_sweeps_sel(const FastArgs& p, const double* __restrict__ tb,
-                                                 const double (&v)[M + 4], double (&d)[M],
-                                                 int chunk, RowShift rs) {
-    if (TAB == TAB_EDGES && p.special_first && chunk == 0) edge_sweeps<M, SHIFT>(p.e_first, v, d, rs);
-    else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
-        edge_sweeps<M, SHIFT>(p.e_last, v, d, rs);
-    else chunk_sweeps<M, TAB != TAB_GLOBAL, SHIFT>(p, tb, v, d, rs);
-}
-
+// Chunk sweeps of a (possibly edge-special) chunk. Measured at 512^3: a
+// select-based shifted window on the edge warps (the barrier-critical path
+// of every item) cost open d2/dx2 ~11%; the 7-tap edge rows cost nothing.
 template <int M, int TAB>
 __device__ __forceinline__ void chunk_sweeps_any(const FastArgs& p, const double* __restrict__ tb,
                                                  const double (&v)[M + 4], double (&d)[M],
                                                  int chunk) {
-    if (p.has_shift) {
-        RowShift rs{0, 0, 0, 0};
-        if (chunk == 0) {
-            rs.f0 = p.sh[0];
-            rs.f1 = p.sh[1];
-        }
-        if (chunk == p.chunks - 1) {
-            rs.b0 = p.sh[2];
-            rs.b1 = p.sh[3];
-        }
-        chunk_sweeps_sel<M, TAB, true>(p, tb, v, d, chunk, rs);
-    } else {
-        chunk_sweeps_sel<M, TAB, false>(p, tb, v, d, chunk, RowShift{0, 0, 0, 0});
+    // only the block's first / last chunk can hold shifted rows
+    RowShift rs{0, 0, 0, 0};
+    if (chunk == 0) {
+        rs.f0 = p.sh[0];
+        rs.f1 = p.sh[1];
     }
+    if (chunk == p.chunks - 1) {
+        rs.b0 = p.sh[2];
+        rs.b1 = p.sh[3];
+    }
+    // TAB_EDGES: the special (edge) chunks carry their shifts in the 7-tap
+    // rows of their EdgeTable; other chunks with shifted rows (uncommon
+    // table layouts) take the select-based copy
+    if (TAB == TAB_EDGES && p.special_first && chunk == 0)
+        edge_sweeps<M>(p.e_first, v, d);
+    else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
+        edge_sweeps<M>(p.e_last, v, d);
+    else if (p.has_shift && (chunk == 0 || chunk == p.chunks - 1))
+        chunk_sweeps<M, TAB != TAB_GLOBAL, true>(p, tb, v, d, rs);
+    else chunk_sweeps<M, TAB != TAB_GLOBAL, false>(p, tb, v, d);
 }
 
 template <int M, int TAB>

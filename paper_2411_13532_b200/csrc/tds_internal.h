@@ -34,6 +34,11 @@ struct UniformTable {
 // stencil s0..s4, f, r, w, sa, sc -- the layout of the global `tab`.
 struct EdgeTable {
     double c[MMAX_UNIFORM][NCOEF];
+    // 7-tap stencils of chunk rows 0, 1 (window rows i .. i+6, offsets -2..4)
+    // and M-2, M-1 (rows i-2 .. i+4, offsets -4..2): the width-5 row placed
+    // at its window shift (plan.cpp check_shift), zeros elsewhere -- shifted
+    // one-sided closures cost two FMAs instead of per-row selects
+    double x7[4][7];
 };
 
 // Coefficient source of the fast kernels (template parameter TAB): the

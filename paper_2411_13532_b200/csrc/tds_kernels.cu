@@ -24,6 +24,7 @@
 
 #include <cstdint>
 
+#include "tds_device.cuh"
 #include "tds_internal.h"
 
 namespace tds {
@@ -85,38 +86,10 @@ __global__ void __launch_bounds__(512) k_fast(const __grid_constant__ FastArgs p
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
 #define TAB(i, k) (UNIFORM ? 0.0 : __ldg(tb + (i) * NCOEF + (k)))
 
+    // fused stencil + Alg. 6 sweeps (tds_device.cuh; shifted one-sided rows
+    // of the first / last chunk included)
     double d[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        double s0, s1, s2, s3, s4, f, r;
-        if (UNIFORM) {
-            s0 = p.ut.st[0]; s1 = p.ut.st[1]; s2 = p.ut.st[2]; s3 = p.ut.st[3]; s4 = p.ut.st[4];
-            f = p.ut.f[i]; r = p.ut.r[i];
-        } else {
-            const double2 c01 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF));
-            const double2 c23 = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 2));
-            const double2 c4f = __ldg(reinterpret_cast<const double2*>(tb + i * NCOEF + 4));
-            s0 = c01.x; s1 = c01.y; s2 = c23.x; s3 = c23.y; s4 = c4f.x; f = c4f.y;
-            r = __ldg(tb + i * NCOEF + 6);
-        }
-        double rhs = s0 * v[i];
-        rhs = fma(s1, v[i + 1], rhs);
-        rhs = fma(s2, v[i + 2], rhs);
-        rhs = fma(s3, v[i + 3], rhs);
-        rhs = fma(s4, v[i + 4], rhs);
-        if (i < 2) d[i] = rhs * r;
-        else d[i] = fma(-r, d[i - 1], rhs) * f;
-    }
-#pragma unroll
-    for (int i = M - 3; i >= 1; --i) {
-        const double w = UNIFORM ? p.ut.w[i] : TAB(i, 7);
-        d[i] = fma(-w, d[i + 1], d[i]);
-    }
-    {
-        const double w0 = UNIFORM ? p.ut.w[0] : TAB(0, 7);
-        const double f0 = UNIFORM ? p.ut.f[0] : TAB(0, 5);
-        d[0] = fma(-w0, d[1], d[0]) * f0;
-    }
+    dev::chunk_sweeps_any<M, UNIFORM ? TAB_UNIFORM : TAB_GLOBAL>(p, tb, v, d, chunk);
 
     // reduced rhs of this chunk -> shared memory
     double* Y = sY + (size_t)tl * K * TL;
@@ -195,10 +168,6 @@ static int launch_fast_t(const FastArgs& a, long long tiles, cudaStream_t s) {
 int launch_fast(int M, int mode, bool uniform, const FastArgs& a, long long tiles,
                 cudaStream_t s) {
     if (tma_eligible(M, a)) return launch_tma(M, mode, uniform, a, tiles, s);
-    if (a.has_shift)
-        return set_err(TDS_ERR_UNSUPPORTED,
-                       "shifted (one-sided) stencil rows need the TMA kernels: sz % 8 == 0 and a "
-                       "16-byte aligned field");
     // k_fast has no per-chunk table switch: edge-special plans use the table path
     if (a.special_first || a.special_last) uniform = false;
 #define DISPATCH_MODE(MM)                                                             \
