@@ -246,10 +246,13 @@ def test_fused_timeout_raises_and_poisons(env):
         group.close()
 
 
-@pytest.mark.parametrize("p,nu,sz", [(2, 0.02, 16), (2, 0.0, 32), (4, 0.01, 32)])
-def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz):
+@pytest.mark.parametrize("p,nu,sz,tl", [(2, 0.02, 16, "16"), (2, 0.0, 32, "16"),
+                                         (4, 0.01, 32, "16"), (2, 0.02, 32, "8")])
+def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz, tl, env):
     # BASELINE config 5's distributed RHS: z-slabs on P in-process ranks, the
-    # z terms as one k_dd_transport per rank (in-kernel neighbour rounds)
+    # z terms as one k_dd_transport per rank (in-kernel neighbour rounds);
+    # TDS_TRANSPORT_TL=8: the kernel's 8-line tiles
+    env({"TDS_TRANSPORT_TL": tl})
     n = 128
     h = 2 * np.pi / n
     rng = np.random.default_rng(77)
@@ -289,3 +292,67 @@ def test_transport_rank_count_two_vs_oracle():
     got = [g.cpu().numpy() if hasattr(g, "cpu") else np.asarray(g) for g in got]
     want = O.transport_rhs(u3, v3, w3, nu, h, sz, rank_counts=(2, 2, 2))
     assert max(O.rel_linf(g, w) for g, w in zip(got, want)) <= 1e-12
+
+
+two_gpus = pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                              reason="needs at least two GPUs")
+
+
+@two_gpus
+@pytest.mark.parametrize("devices", [[0, 1], [0, 1, 0, 1], [1, 0, 1, 0, 1, 0, 1, 0]])
+def test_ranks_across_devices_golden(golden, devices):
+    # one process driving several B200s (the reference's spawn_ranks shape):
+    # per-rank fused kernels exchanging through peer-mapped mailboxes over
+    # NVLink, global field in / out
+    tag = {2: "d1p1024_P2", 4: None, 8: "d1p1024_P8"}[len(devices)]
+    if tag is None:
+        n = 1024
+        lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, False)
+        s = T.TridiagonalSystem(lo, di, up, periodic=False)
+        field = np.random.default_rng(4).standard_normal((8, n, 32))
+        want = O.run_distd2(lo, di, up, False, field, stc, O.balanced_sizes(n, 4))
+        st, sizes = T.StencilCoeffs(stc), O.balanced_sizes(n, 4)
+    else:
+        g = golden_run(golden, tag)
+        s, st = _system(g)
+        field, want, sizes = g["field"], g["out"], g["sizes"]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", T.NotDominantWarning)
+        got = T.run_distd2(s, field, part=T.SubdomainPartition(tuple(sizes)), stencil=st,
+                           devices=devices)
+        got2 = T.run_distd2(s, field, part=T.SubdomainPartition(tuple(sizes)), stencil=st,
+                            devices=devices)
+    assert O.rel_linf(got, want) <= 1e-12
+    assert np.array_equal(got, got2)
+
+
+@two_gpus
+def test_two_pass_ranks_across_devices_strict(golden, env):
+    env({"TDS_FUSED": "0"})
+    g = golden_run(golden, "rd128_P4")
+    s, st = _system(g)
+    got = T.run_distd2(s, g["field"], part=T.SubdomainPartition(g["sizes"]), stencil=st,
+                       arithmetic="strict", devices=[0, 1, 0, 1])
+    assert np.array_equal(got, g["out"])
+
+
+@two_gpus
+def test_slab_transport_across_devices():
+    n, nu, sz, p = 128, 0.01, 32, 2
+    h = 2 * np.pi / n
+    rng = np.random.default_rng(8)
+    u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
+
+    def body(ctx):
+        tr = T.SlabTransport(n, sz, nu, h, ctx)
+        rhs = tr.rhs(*[tr.local_slab(a) for a in (u3, v3, w3)])
+        torch.cuda.current_stream().synchronize()
+        tr.check()
+        out = [T.unpack(T.GroupedField(tr.lay["x"], c)).cpu().numpy() for c in rhs]
+        tr.close()
+        return out
+
+    res = TR.spawn_ranks(p, True, body, devices=[0, 1])
+    full = [np.concatenate([r[i] for r in res], axis=2) for i in range(3)]
+    want = O.transport_rhs(u3, v3, w3, nu, h, sz, rank_counts=(1, 1, p))
+    assert max(O.rel_linf(g, w) for g, w in zip(full, want)) <= 1e-12
