@@ -182,6 +182,13 @@ int tds_mailbox_init(double* mail, long long words, void* stream);
 int tds_mailbox_status(const double* mail, long long words, unsigned long long* host_status,
                        void* stream);
 int tds_fused_eligible(const tds_plan* plan, long long groups, int sz);
+/* The fused kernel variant (deferred edges or not, for 16 / 8-line tiles) is
+ * a per-plan property, but all ranks MUST launch the same variant: AND the
+ * plan's variant mask (bit 0: deferral allowed with 16-line tiles, bit 1:
+ * with 8-line tiles) with `mask` and return the result. Ranks agree by
+ * calling it with 3, reducing the results with AND over the group and
+ * calling it again with the agreed mask (rank.DistD2Rank does this). */
+int tds_plan_restrict_fused(tds_plan* plan, int mask);
 int tds_fused_solve(const tds_plan* plan, const double* u, double* out,
                     long long groups, int sz, double* mail, double* mail_prev,
                     double* mail_next, unsigned long long epoch, int max_ctas, void* stream);

@@ -300,6 +300,13 @@ extern "C" long long tds_mailbox_words(long long groups, int sz) {
     return tds::dd_mail_words(groups * sz);
 }
 
+extern "C" int tds_plan_restrict_fused(tds_plan* p, int mask) {
+    if (!p) return -1;
+    p->dd_defer[0] &= (mask & 1) ? 1 : 0;
+    p->dd_defer[1] &= (mask & 2) ? 1 : 0;
+    return (p->dd_defer[0] ? 1 : 0) | (p->dd_defer[1] ? 2 : 0);
+}
+
 extern "C" int tds_fused_eligible(const tds_plan* p, long long groups, int sz) {
     if (!p || p->rank < 0 || p->P < 2 || p->path != TDS_PATH_FAST) return 0;
     tds::FastArgs a = fast_args(p, groups * sz, sz);

@@ -20,6 +20,7 @@
 // error word instead of hanging the GPU.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -616,12 +617,19 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     A.t.store_cs = store_policy();
     const int threads = cfg.tpc * a.chunks * TLT;
     const size_t smem = dd_smem(a, cfg);
-    const void* fn = reinterpret_cast<const void*>(k_dd<M, UNI, TLT, SZC>);
-    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd)"))) return rc;
+    const void* fns[3] = {reinterpret_cast<const void*>(k_dd<M, TAB_GLOBAL, TLT, SZC>),
+                          reinterpret_cast<const void*>(k_dd<M, TAB_UNIFORM, TLT, SZC>),
+                          reinterpret_cast<const void*>(k_dd<M, TAB_EDGES, TLT, SZC>)};
     // at most the resident capacity (every CTA co-resident: no wait on an
-    // unscheduled CTA), capped by max_ctas when several ranks share a device;
-    // identical on every rank
-    const long long grid = persistent_grid(fn, threads, smem, a.items, A.max_ctas);
+    // unscheduled CTA), capped by max_ctas when several ranks share a device.
+    // IDENTICAL on every rank: the minimum over the coefficient-table
+    // variants, since neighbouring ranks may run different ones (edge ranks
+    // of an open operator hold special chunks)
+    long long grid = a.items;
+    for (const void* f : fns) {
+        if ((rc = ensure_smem(f, smem, "cudaFuncSetAttribute(k_dd)"))) return rc;
+        grid = std::min(grid, persistent_grid(f, threads, smem, a.items, A.max_ctas));
+    }
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
     k_dd<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd launch");
@@ -645,9 +653,14 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     if (rc) return rc;
     const int threads = cfg.tpc * a.chunks * TLT;
     const size_t smem = dd2_smem(a, cfg, M);
-    const void* fn = reinterpret_cast<const void*>(k_dd2<M, UNI, TLT, SZC>);
-    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd2)"))) return rc;
-    const long long grid = persistent_grid(fn, threads, smem, a.items, A.max_ctas);
+    const void* fns[3] = {reinterpret_cast<const void*>(k_dd2<M, TAB_GLOBAL, TLT, SZC>),
+                          reinterpret_cast<const void*>(k_dd2<M, TAB_UNIFORM, TLT, SZC>),
+                          reinterpret_cast<const void*>(k_dd2<M, TAB_EDGES, TLT, SZC>)};
+    long long grid = a.items;    // identical on every rank (see launch_dd_t)
+    for (const void* f : fns) {
+        if ((rc = ensure_smem(f, smem, "cudaFuncSetAttribute(k_dd2)"))) return rc;
+        grid = std::min(grid, persistent_grid(f, threads, smem, a.items, A.max_ctas));
+    }
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
     k_dd2<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd2 launch");

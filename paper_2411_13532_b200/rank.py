@@ -105,6 +105,12 @@ class DistD2Rank:
         self.broken = None
         self.fused = (self.plan.path == "fast" and len(set(part.local_sizes)) == 1
                       and os.environ.get("TDS_FUSED", "1") != "0")
+        # every rank must launch the same fused-kernel variant (persistent
+        # schedules must match): agree on the deferral mask (collective)
+        lib = N.lib()
+        mask = lib.tds_plan_restrict_fused(self.plan.handle, 3)
+        agreed = ctx.allreduce_and(mask if self.fused else 3)
+        lib.tds_plan_restrict_fused(self.plan.handle, agreed)
 
     @property
     def path(self):

@@ -222,6 +222,15 @@ class RankContext:
     def barrier(self):
         _dist().barrier(group=self.group)
 
+    def allreduce_and(self, mask, bits=8):
+        """Bitwise AND of a small non-negative int over the group."""
+        torch = _torch()
+        dist = _dist()
+        t = torch.tensor([(mask >> b) & 1 for b in range(bits)], dtype=torch.int32,
+                         device=self.payload_device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return sum(int(v) << b for b, v in enumerate(t.tolist()))
+
 
 # ------------------------------------------------------- in-process ranks
 
@@ -376,6 +385,16 @@ class LocalRankContext:
             self._world.barrier.wait(timeout=RECV_TIMEOUT)
         except threading.BrokenBarrierError:
             raise TimeoutError(f"rank {self.rank_id}: barrier broken (a peer failed)") from None
+
+    def allreduce_and(self, mask, bits=8):
+        """Bitwise AND of a small non-negative int over the group (collective)."""
+        self._world.boxes[("and", self.rank_id)] = int(mask)
+        self.barrier()
+        res = mask
+        for r in range(self.rank_count):
+            res &= self._world.boxes[("and", r)]
+        self.barrier()
+        return res
 
     def open_mailboxes(self, words):
         """Collective over the group (every rank calls it in the same

@@ -131,3 +131,10 @@ def test_grid_cap_of_shared_devices():
     assert TR.make_contexts(2, True, [0, 1])[0].fused_grid_cap == 0
     with pytest.raises(ValueError):
         TR.make_contexts(2, True, [0])
+
+
+def test_allreduce_and_agrees_on_masks():
+    masks = [3, 1, 3, 3]
+    assert TR.spawn_ranks(4, True, lambda ctx: ctx.allreduce_and(masks[ctx.rank_id])) == [1] * 4
+    assert TR.spawn_ranks(2, False, lambda ctx: [ctx.allreduce_and(2 + ctx.rank_id),
+                                                 ctx.allreduce_and(3)]) == [[2, 3]] * 2

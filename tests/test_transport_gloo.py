@@ -36,7 +36,8 @@ def _worker(rank, world, cyclic, port, q):
         prev_last, next_first = exchange_boundary(ctx, first, last)
         sc, sa = share_scalars(ctx, 10.0 + rank, 20.0 + rank)
         full = gather_to_root(ctx, local)
-        q.put((rank, None if low is None else low.numpy(), None if high is None else high.numpy(),
+        agreed = ctx.allreduce_and(3 if rank else 1)        # fused-variant agreement
+        q.put((rank, agreed, None if low is None else low.numpy(), None if high is None else high.numpy(),
                None if prev_last is None else prev_last.numpy(),
                None if next_first is None else next_first.numpy(), sc, sa,
                ctx.exchange_rounds, ctx.messages_sent,
@@ -55,7 +56,8 @@ def _run(world, cyclic):
     res = {}
     for _ in range(world):
         item = q.get(timeout=120)
-        res[item[0]] = item[1:]
+        assert item[1] == 1
+        res[item[0]] = item[2:]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
