@@ -330,7 +330,7 @@ def run_multi(args, torch):
         step()
     torch.cuda.synchronize()
     # T1(1024^3) on rank 0's GPU (the others wait at the barrier)
-    t1 = t1_anchor(args, torch) if rank == 0 and n == 1024 and not args.no_t1 else None
+    anchor = t1_anchor(args, torch) if rank == 0 and n == 1024 and not args.no_t1 else None
     dist.barrier()
     evs = [{d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for d in "xyz"} for _ in range(args.steps)]
@@ -384,10 +384,10 @@ def run_multi(args, torch):
                          "algorithmic_bytes_per_launch": BYTES_PER_POINT * local_points},
             "e2e": e2e, "gpu_launches": (1 if fused else 3) * 3 * args.steps,
             "clocks": clocks, "cpu_baseline": None,
-            "t1_1024": t1,
+            "t1_1024": anchor,
             # north star: E(N) = T1(1024^3) / (N * T_N), same box, same operator
-            "efficiency_vs_t1": (round(t1["ms_per_step"] / (world * ms_step), 4)
-                                 if t1 else None),
+            "efficiency_vs_t1": (round(anchor["ms_per_step"] / (world * ms_step), 4)
+                                 if anchor else None),
         }
     dist.barrier()
     solver.close()

@@ -189,6 +189,12 @@ int tds_fused_eligible(const tds_plan* plan, long long groups, int sz);
  * calling it with 3, reducing the results with AND over the group and
  * calling it again with the agreed mask (rank.DistD2Rank does this). */
 int tds_plan_restrict_fused(tds_plan* plan, int mask);
+/* The persistent grid tds_fused_solve would use for this plan and shape
+ * (max_ctas as there; -1: not eligible). Ranks whose table variants differ
+ * (edge ranks of open operators) can have different occupancies: they take
+ * the MINIMUM over the group and pass it as max_ctas (rank.DistD2Rank). With
+ * max_ctas <= 0 the launch itself uses the minimum over all variants. */
+long long tds_fused_grid(const tds_plan* plan, long long groups, int sz, int max_ctas);
 int tds_fused_solve(const tds_plan* plan, const double* u, double* out,
                     long long groups, int sz, double* mail, double* mail_prev,
                     double* mail_next, unsigned long long epoch, int max_ctas, void* stream);

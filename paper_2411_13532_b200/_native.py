@@ -72,6 +72,7 @@ SIGNATURES = {
     "tds_mailbox_words": (_LL, [_LL, _I]),
     "tds_fused_eligible": (_I, [_P, _LL, _I]),
     "tds_plan_restrict_fused": (_I, [_P, _I]),
+    "tds_fused_grid": (_LL, [_P, _LL, _I, _I]),
     "tds_mailbox_init": (_I, [_P, _LL, _P]),
     "tds_mailbox_status": (_I, [_P, _LL, _P, _P]),
     "tds_peer_access": (_I, [_I]),

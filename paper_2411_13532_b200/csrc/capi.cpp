@@ -293,7 +293,8 @@ namespace tds {
 long long dd_mail_words(long long lines);
 bool dd_eligible(int M, const FastArgs& a);
 int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
-              double* mail_next, unsigned long long epoch, int max_ctas, cudaStream_t s);
+              double* mail_next, unsigned long long epoch, int max_ctas, cudaStream_t s,
+              bool query = false);
 }  // namespace tds
 
 extern "C" long long tds_mailbox_words(long long groups, int sz) {
@@ -312,6 +313,16 @@ extern "C" int tds_fused_eligible(const tds_plan* p, long long groups, int sz) {
     tds::FastArgs a = fast_args(p, groups * sz, sz);
     a.u = reinterpret_cast<const double*>(uintptr_t(256));   // alignment probe only
     return tds::dd_eligible(p->M, a) ? 1 : 0;
+}
+
+extern "C" long long tds_fused_grid(const tds_plan* p, long long groups, int sz, int max_ctas) {
+    if (!tds_fused_eligible(p, groups, sz)) return -1;
+    tds::FastArgs a = fast_args(p, groups * sz, sz);
+    a.u = reinterpret_cast<const double*>(uintptr_t(256));   // no launch: shape only
+    a.edge_mode = tds::EDGE_HALO;
+    const int g = tds::launch_dd(p->M, p->uniform, a, nullptr, nullptr, nullptr, 0, max_ctas,
+                                 nullptr, true);
+    return g;
 }
 
 extern "C" int tds_fused_solve(const tds_plan* p, const double* u, double* out, long long groups,

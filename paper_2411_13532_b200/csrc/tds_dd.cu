@@ -39,6 +39,7 @@ struct DDArgs {
     unsigned long long epoch;
     unsigned long long timeout_ns;
     int max_ctas;          // host-side grid cap (0: resident capacity)
+    int query;             // host-side: return the grid instead of launching
 };
 
 // Mailbox layout (8-byte words), L = lines. Two parity halves (epoch & 1)
@@ -625,11 +626,14 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     // IDENTICAL on every rank: the minimum over the coefficient-table
     // variants, since neighbouring ranks may run different ones (edge ranks
     // of an open operator hold special chunks)
+    // (max_ctas > 0: a grid the ranks agreed on, tds_fused_grid)
     long long grid = a.items;
     for (const void* f : fns) {
         if ((rc = ensure_smem(f, smem, "cudaFuncSetAttribute(k_dd)"))) return rc;
+        if (A.max_ctas > 0 && f != fns[UNI]) continue;
         grid = std::min(grid, persistent_grid(f, threads, smem, a.items, A.max_ctas));
     }
+    if (A.query) return (int)std::min<long long>(grid, 1 << 30);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
     k_dd<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd launch");
@@ -659,8 +663,10 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     long long grid = a.items;    // identical on every rank (see launch_dd_t)
     for (const void* f : fns) {
         if ((rc = ensure_smem(f, smem, "cudaFuncSetAttribute(k_dd2)"))) return rc;
+        if (A.max_ctas > 0 && f != fns[UNI]) continue;
         grid = std::min(grid, persistent_grid(f, threads, smem, a.items, A.max_ctas));
     }
+    if (A.query) return (int)std::min<long long>(grid, 1 << 30);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
     k_dd2<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd2 launch");
@@ -714,10 +720,12 @@ bool dd_eligible(int M, const FastArgs& a) {
 }
 
 int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail_prev,
-              double* mail_next, unsigned long long epoch, int max_ctas, cudaStream_t s) {
+              double* mail_next, unsigned long long epoch, int max_ctas, cudaStream_t s,
+              bool query) {
     DDArgs A;
     std::memset(&A, 0, sizeof(A));
     A.max_ctas = max_ctas;
+    A.query = query ? 1 : 0;
     A.t.f = a;
     A.mail = mail;
     A.mail_prev = mail_prev;

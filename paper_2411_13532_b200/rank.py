@@ -133,11 +133,17 @@ class DistD2Rank:
         return b
 
     def mailbox(self, groups, sz):
-        """Own mailbox + the neighbours' (one collective per field shape)."""
+        """Own mailbox + the neighbours' and the agreed persistent grid (one
+        collective per field shape)."""
         key = (groups, sz)
         mb = self._mail.get(key)
         if mb is None:
-            mb = self.ctx.open_mailboxes(N.lib().tds_mailbox_words(groups, sz))
+            lib = N.lib()
+            mb = self.ctx.open_mailboxes(lib.tds_mailbox_words(groups, sz))
+            # every rank runs the same persistent schedule: the smallest grid
+            # any rank's kernel variant allows (ranks sharing a device split it)
+            mine = lib.tds_fused_grid(self.plan.handle, groups, sz, self.ctx.fused_grid_cap)
+            mb.grid = self.ctx.allreduce_min(mine if mine > 0 else 1 << 30)
             self._mail[key] = mb
         return mb
 
@@ -195,7 +201,7 @@ class DistD2Rank:
         self.ctx.begin_solve()
         self.ctx.exchange_rounds += 2          # both rounds run inside the kernel
         N.check(N.lib().tds_fused_solve(self.plan.handle, _vp(u), _vp(out), groups, sz, mb.own,
-                                        mb.prev, mb.next, self._epoch, self.ctx.fused_grid_cap,
+                                        mb.prev, mb.next, self._epoch, mb.grid,
                                         ctypes.c_void_p(s.cuda_stream)))
         mb.post_status(s)
 

@@ -231,6 +231,14 @@ class RankContext:
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
         return sum(int(v) << b for b, v in enumerate(t.tolist()))
 
+    def allreduce_min(self, value):
+        """Minimum of an int over the group."""
+        torch = _torch()
+        dist = _dist()
+        t = torch.tensor([int(value)], dtype=torch.int64, device=self.payload_device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
 
 # ------------------------------------------------------- in-process ranks
 
@@ -386,15 +394,22 @@ class LocalRankContext:
         except threading.BrokenBarrierError:
             raise TimeoutError(f"rank {self.rank_id}: barrier broken (a peer failed)") from None
 
-    def allreduce_and(self, mask, bits=8):
-        """Bitwise AND of a small non-negative int over the group (collective)."""
-        self._world.boxes[("and", self.rank_id)] = int(mask)
+    def _allreduce(self, value, op):
+        self._world.boxes[("reduce", self.rank_id)] = int(value)
         self.barrier()
-        res = mask
+        res = int(value)
         for r in range(self.rank_count):
-            res &= self._world.boxes[("and", r)]
+            res = op(res, self._world.boxes[("reduce", r)])
         self.barrier()
         return res
+
+    def allreduce_and(self, mask, bits=8):
+        """Bitwise AND of a small non-negative int over the group (collective)."""
+        return self._allreduce(mask, lambda a, b: a & b)
+
+    def allreduce_min(self, value):
+        """Minimum of an int over the group (collective)."""
+        return self._allreduce(value, min)
 
     def open_mailboxes(self, words):
         """Collective over the group (every rank calls it in the same
