@@ -350,7 +350,11 @@ int fast_tables(tds_plan* p, const Global& g, int M, ChunkSet& cs) {
         }
         return true;
     };
-    bool uni = M <= tds::MMAX_UNIFORM && chunk_is_ref(ref);
+    // shifted (one-sided) rows live only in special edge chunks of a uniform
+    // plan (the kernels' TAB_EDGES 7-tap rows) or in a per-row table
+    bool any_shift = false;
+    for (int i = 0; i < p->block_rows; ++i) any_shift |= g.sh[p->block_off + i] != 0;
+    bool uni = M <= tds::MMAX_UNIFORM && chunk_is_ref(ref) && !(any_shift && C < 3);
     for (int k = 1; k + 1 < C && uni; ++k)
         if (!chunk_is_ref(k)) uni = false;
     p->special_first = p->special_last = 0;

@@ -114,11 +114,23 @@ template <class Args>
 __device__ __forceinline__ double take(double* slot, const Args& A, unsigned long long* err) {
     return take_v(slot, SENTINEL, A, err);
 }
-// add this warp's posted-word counts to the rank's own status words
-// (err + 1: halo words, err + 2: boundary words); one atomic per warp
-__device__ __forceinline__ void flush_counts(unsigned long long* err, unsigned nh, unsigned nb) {
+// Message accounting (status words err + 1 / err + 2: halo / boundary-row
+// words this rank posted). At kernel exit every thread adds the words its
+// role posts per item times the valid items it processed -- the posts are
+// unconditional, so this is exactly what the kernel stored, and the hot
+// loop carries no counter (a live per-store counter cost k_dd2 7% at
+// m = 512: it sits at the 128-register cap). One atomic per warp.
+__device__ __forceinline__ unsigned valid_items(long long items, long long lines, int tpc, int tl,
+                                                int TLT, int lane) {
+    unsigned n = 0;
+    for (long long it = blockIdx.x; it < items; it += gridDim.x)
+        n += ((it * tpc + tl) * TLT + lane < lines) ? 1u : 0u;
+    return n;
+}
+__device__ __forceinline__ void flush_counts(unsigned long long* err, unsigned halo_words,
+                                             unsigned bnd_words) {
     const unsigned mask = __activemask();
-    const unsigned a = __reduce_add_sync(mask, nh), b = __reduce_add_sync(mask, nb);
+    const unsigned a = __reduce_add_sync(mask, halo_words), b = __reduce_add_sync(mask, bnd_words);
     if ((threadIdx.x & 31) == __ffs(mask) - 1) {
         if (a) atomicAdd(err + 1, (unsigned long long)a);
         if (b) atomicAdd(err + 2, (unsigned long long)b);
@@ -168,7 +180,6 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
                             l0, b * A.t.boxr, g);
         }
     };
-    unsigned nh = 0, nbw = 0;   // words posted (halo / boundary rows)
     // ROUND 1 for `item`: my first two rows -> prev's high halo, my last two
     // rows -> next's low halo (read straight from my block in HBM)
     auto publish_halo = [&](long long item) {
@@ -180,14 +191,12 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
             post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
-            nh += 2;
         }
         if (last_chunk && A.mail_next) {
             const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
             const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
             post(A.mail_next + par + mb.h_lo() + hb, a0);
             post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
-            nh += 2;
         }
     };
 
@@ -271,11 +280,9 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             g1y = last_chunk ? gdot<TLT>(p, 1, Y, K, lane) : 0.0;
             if (first_chunk && A.mail_prev) {
                 post(A.mail_prev + par + mb.d_from_next() + line, g0y);
-                ++nbw;
             }
             if (last_chunk && A.mail_next) {
                 post(A.mail_next + par + mb.d_from_prev() + line, g1y);
-                ++nbw;
             }
         }
         double F, L;
@@ -317,7 +324,11 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             chunk_store_any<M, TAB>(p, tb, p.out + line_base_t<SZC>(line, rows, p.sz), sz, r0, d, F, L,
                                         A.t.store_cs != 0, chunk);
     }
-    flush_counts(err, nh, nbw);
+    {
+        const unsigned n = valid_items(p.items, p.lines, tpc, tl, TLT, lane);
+        const unsigned per = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
+        flush_counts(err, 2 * per * n, per * n);   // 2 halo rows + 1 boundary row per edge
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -386,7 +397,6 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                             l0, b * A.t.boxr, g);
         }
     };
-    unsigned nh = 0, nbw = 0;   // words posted (halo / boundary rows)
     auto publish_halo = [&](long long item) {
         if (!halo_lo_poster && !halo_hi_poster) return;
         const long long ln = (item * tpc + tl) * TLT + lane;
@@ -397,14 +407,12 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             const double a0 = __ldg(ub), a1 = __ldg(ub + sz);
             post(A.mail_prev + par + mb.h_hi() + hb, a0);
             post(A.mail_prev + par + mb.h_hi() + hb + sz, a1);
-            nh += 2;
         }
         if (halo_hi_poster && A.mail_next) {
             const double a0 = __ldg(ub + (long long)(rows - 2) * sz);
             const double a1 = __ldg(ub + (long long)(rows - 1) * sz);
             post(A.mail_next + par + mb.h_lo() + hb, a0);
             post(A.mail_next + par + mb.h_lo() + hb + sz, a1);
-            nh += 2;
         }
     };
     auto edge_finish = [&](const EdgeTable& T, double* ob, double F, double L) {
@@ -546,11 +554,9 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             const double gy = gdot<TLT>(p, role, Y, K, lane);
             if (role == 0 && A.mail_prev) {
                 post(A.mail_prev + par + mb.d_from_next() + line, gy);
-                ++nbw;
             }
             if (role == 1 && A.mail_next) {
                 post(A.mail_next + par + mb.d_from_prev() + line, gy);
-                ++nbw;
             }
             sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
         }
@@ -573,12 +579,10 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                     const double gy = gdot<TLT>(p, r, Y, K, lane);
                     if (r == 0 && A.mail_prev) {
                         post(A.mail_prev + par + mb.d_from_next() + line, gy);
-                        ++nbw;
-                    }
+                            }
                     if (r == 1 && A.mail_next) {
                         post(A.mail_next + par + mb.d_from_prev() + line, gy);
-                        ++nbw;
-                    }
+                            }
                     sGY[(((size_t)(it & 1) * tpc + tl) * 2 + r) * TLT + lane] = gy;
                 }
             }
@@ -596,7 +600,19 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         __syncthreads();   // the helper warp's g.Y of the last item
         if (edge_warp) finish(prev_item, (it - 1) & 1);
     }
-    flush_counts(err, nh, nbw);
+    {
+        const unsigned n = valid_items(p.items, p.lines, tpc, tl, TLT, lane);
+        const unsigned h = (halo_lo_poster && A.mail_prev ? 2u : 0u) +
+                           (halo_hi_poster && A.mail_next ? 2u : 0u);
+        unsigned b = 0;
+        if (helpers) {
+            if (!edge_warp && wt == 1 && role == 0 && A.mail_prev) b = 1;
+            if (!edge_warp && wt == 1 && role == 1 && A.mail_next) b = 1;
+        } else {
+            b = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
+        }
+        flush_counts(err, h * n, b * n);
+    }
 }
 
 namespace {
@@ -630,7 +646,7 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     long long grid = a.items;
     for (const void* f : fns) {
         if ((rc = ensure_smem(f, smem, "cudaFuncSetAttribute(k_dd)"))) return rc;
-        if (A.max_ctas > 0 && f != fns[UNI]) continue;
+        if ((A.max_ctas > 0 || A.query) && f != fns[UNI]) continue;   // own variant
         grid = std::min(grid, persistent_grid(f, threads, smem, a.items, A.max_ctas));
     }
     if (A.query) return (int)std::min<long long>(grid, 1 << 30);
@@ -663,7 +679,7 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     long long grid = a.items;    // identical on every rank (see launch_dd_t)
     for (const void* f : fns) {
         if ((rc = ensure_smem(f, smem, "cudaFuncSetAttribute(k_dd2)"))) return rc;
-        if (A.max_ctas > 0 && f != fns[UNI]) continue;
+        if ((A.max_ctas > 0 || A.query) && f != fns[UNI]) continue;   // own variant
         grid = std::min(grid, persistent_grid(f, threads, smem, a.items, A.max_ctas));
     }
     if (A.query) return (int)std::min<long long>(grid, 1 << 30);
@@ -880,7 +896,6 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             }
         }
     };
-    unsigned nh = 0, nbw = 0;   // words posted (halo / boundary rows)
     // ROUND 1 of `item`: first two rows of u_i, u_j -> prev, last two -> next
     auto publish_halo = [&](long long item) {
         if (!first_chunk && !last_chunk) return;
@@ -896,7 +911,6 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             post(m + mb.hhi_i() + hb + sz, __ldg(bi + sz));
             post(m + mb.hhi_j() + hb, __ldg(bj));
             post(m + mb.hhi_j() + hb + sz, __ldg(bj + sz));
-            nh += 4;
         }
         if (last_chunk && A.mail_next) {
             double* m = A.mail_next + par;
@@ -905,7 +919,6 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             post(m + mb.hlo_i() + hb + sz, __ldg(bi + b));
             post(m + mb.hlo_j() + hb, __ldg(bj + a));
             post(m + mb.hlo_j() + hb + sz, __ldg(bj + b));
-            nh += 4;
         }
     };
     auto release = [&](long long nxt) {
@@ -993,16 +1006,14 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
                     const double g0y = gdot<TLT>(p, 0, Y, K, lane);
                     if (A.mail_prev) {
                         post(A.mail_prev + par + mb.dn(s) + line, g0y);
-                        ++nbw;
-                    }
+                            }
                     P[lane] = g0y;
                 }
                 if (last_chunk) {
                     const double g1y = gdot<TLT>(p, 1, Y, K, lane);
                     if (A.mail_next) {
                         post(A.mail_next + par + mb.dp(s) + line, g1y);
-                        ++nbw;
-                    }
+                            }
                     P[TLT + lane] = g1y;
                 }
             }
@@ -1084,7 +1095,12 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
         }
     }
-    flush_counts(err, nh, nbw);
+    {
+        const unsigned n = valid_items(A.items, A.lines, tpc, tl, TLT, lane);
+        const unsigned per = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
+        // u_i and u_j halos (4 rows) + one boundary row per solve
+        flush_counts(err, 4 * per * n, (A.has_nu ? 3u : 2u) * per * n);
+    }
 }
 
 namespace {

@@ -394,15 +394,24 @@ template <int M, int TAB>
 __device__ __forceinline__ void chunk_sweeps_any(const FastArgs& p, const double* __restrict__ tb,
                                                  const double (&v)[M + 4], double (&d)[M],
                                                  int chunk) {
-    // only the block's first / last chunk can hold shifted rows
-    RowShift rs{0, 0, 0, 0};
-    if (chunk == 0) {
-        rs.f0 = p.sh[0];
-        rs.f1 = p.sh[1];
-    }
-    if (chunk == p.chunks - 1) {
-        rs.b0 = p.sh[2];
-        rs.b1 = p.sh[3];
+    // only the block's first / last chunk can hold shifted rows; the plan
+    // (plan.cpp fast_tables) keeps them out of TAB_UNIFORM tables and inside
+    // the special chunks of TAB_EDGES ones, so only TAB_GLOBAL needs the
+    // select-based copy
+    if constexpr (TAB == TAB_GLOBAL) {
+        if (p.has_shift && (chunk == 0 || chunk == p.chunks - 1)) {
+            RowShift rs{0, 0, 0, 0};
+            if (chunk == 0) {
+                rs.f0 = p.sh[0];
+                rs.f1 = p.sh[1];
+            }
+            if (chunk == p.chunks - 1) {
+                rs.b0 = p.sh[2];
+                rs.b1 = p.sh[3];
+            }
+            chunk_sweeps<M, false, true>(p, tb, v, d, rs);
+            return;
+        }
     }
     // TAB_EDGES: the special (edge) chunks carry their shifts in the 7-tap
     // rows of their EdgeTable; other chunks with shifted rows (uncommon
@@ -411,8 +420,6 @@ __device__ __forceinline__ void chunk_sweeps_any(const FastArgs& p, const double
         edge_sweeps<M>(p.e_first, v, d);
     else if (TAB == TAB_EDGES && p.special_last && chunk == p.chunks - 1)
         edge_sweeps<M>(p.e_last, v, d);
-    else if (p.has_shift && (chunk == 0 || chunk == p.chunks - 1))
-        chunk_sweeps<M, TAB != TAB_GLOBAL, true>(p, tb, v, d, rs);
     else chunk_sweeps<M, TAB != TAB_GLOBAL, false>(p, tb, v, d);
 }
 
