@@ -356,3 +356,36 @@ def test_slab_transport_across_devices():
     full = [np.concatenate([r[i] for r in res], axis=2) for i in range(3)]
     want = O.transport_rhs(u3, v3, w3, nu, h, sz, rank_counts=(1, 1, p))
     assert max(O.rel_linf(g, w) for g, w in zip(full, want)) <= 1e-12
+
+
+@pytest.mark.parametrize("p,periodic,knobs", [(2, True, {}), (4, False, {"TDS_DEFER": "0"}),
+                                              (8, True, {"TDS_TL": "8"})])
+def test_fused_protocol_stress_many_epochs(p, periodic, knobs, env):
+    # compute-sanitizer is unavailable on the GPU pool: instead hammer the
+    # fence-free mailbox protocol (both parity halves, every CTA posting
+    # ahead and waiting) for many epochs on co-resident ranks and require
+    # every solve to be bitwise identical and error-free -- a stale or torn
+    # slot would show up as a differing bit or a timeout
+    env(knobs)
+    n, groups, sz = 512, 24, 32
+    lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, periodic)
+    s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
+    sizes = O.balanced_sizes(n, p)
+    field = np.random.default_rng(p).standard_normal((groups, n, sz))
+    group = _group(s, T.StencilCoeffs(stc), sizes)
+    try:
+        u = torch.from_numpy(field).cuda()
+        outs = [torch.empty_like(u) for _ in range(2)]
+        group.solve(u, outs[0])
+        for e in range(150):
+            group.solve(u, outs[1])
+            if e % 25 == 0:
+                torch.cuda.synchronize()
+                assert torch.equal(outs[0], outs[1]), e
+        torch.cuda.synchronize()
+        group.check()
+        assert torch.equal(outs[0], outs[1])
+        want = O.run_distd2(lo, di, up, periodic, field, stc, sizes)
+        assert O.rel_linf(outs[0].cpu().numpy(), want) <= 1e-12
+    finally:
+        group.close()
