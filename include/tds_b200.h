@@ -126,7 +126,8 @@ int tds_preprocess(const double* a, const double* b, const double* c, int m,
 /*
  * Whole-operator solve (rank == -1 plans): out = A^{-1} stencil(u) with the
  * reference's truncation at the partition's rank boundaries
- * (run_distd2, distributed.py:399-449). u, out: (groups, n, sz) device.
+ * (run_distd2, distributed.py:399-449). u, out: (groups, n, sz) device,
+ * distinct (non-aliasing) buffers -- the reference returns fresh arrays.
  */
 int tds_solve(const tds_plan* plan, const double* u, double* out,
               long long groups, int sz, void* stream);

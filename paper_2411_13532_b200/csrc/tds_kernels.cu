@@ -203,7 +203,7 @@ __device__ __forceinline__ double stencil5(const double* c, double u0, double u1
 }
 
 // value of row `row` (relative to the array) of a line, with the edge rule
-__device__ __forceinline__ double fetch(const StagedArgs& p, const double* ub, long long hb,
+__device__ __forceinline__ double fetch(const StagedArgs& p, const double* __restrict__ ub, long long hb,
                                         int row) {
     const long long sz = p.sz;
     if (row >= 0 && row < p.rows) return ub[row * sz];
@@ -226,7 +226,7 @@ __device__ __forceinline__ int row_shift(const StagedArgs& p, int row) {
 // stencil row with a shifted window: sum over u[row + o + s], o = -2..2, in
 // the reference's left-to-right order (distributed.py:205-208)
 __device__ __forceinline__ double stencil_shifted(const StagedArgs& p, const double* c,
-                                                  const double* ub, long long hb, int row,
+                                                  const double* __restrict__ ub, long long hb, int row,
                                                   int s) {
     return stencil5(c, fetch(p, ub, hb, row - 2 + s), fetch(p, ub, hb, row - 1 + s),
                     fetch(p, ub, hb, row + s), fetch(p, ub, hb, row + 1 + s),
@@ -240,12 +240,13 @@ __global__ void k_staged_decouple(const StagedArgs p) {
     if (line >= p.lines) return;
     const int off = p.boff[b], m = p.bsize[b];
     const long long sz = p.sz;
-    const double* ub = p.u + line_base(line, p.rows, p.sz);
-    double* ob = p.out + line_base(line, p.rows, p.sz);
+    const double* __restrict__ ub = p.u + line_base(line, p.rows, p.sz);
+    double* __restrict__ ob = p.out + line_base(line, p.rows, p.sz);
     const long long hb = halo_base(line, p.sz);
     double u0 = fetch(p, ub, hb, off - 2), u1 = fetch(p, ub, hb, off - 1);
     double u2 = fetch(p, ub, hb, off), u3 = fetch(p, ub, hb, off + 1);
     double dprev = 0.0;
+    #pragma unroll 8
     for (int j = 0; j < m; ++j) {
         const double u4 = fetch(p, ub, hb, off + j + 2);
         const int row = off + j;
@@ -260,6 +261,7 @@ __global__ void k_staged_decouple(const StagedArgs p) {
     double dn = dprev;   // d[m-1] (untouched by the backward sweep)
     double dl = dn;
     double dnext = ob[(long long)(off + m - 2) * sz];
+    #pragma unroll 8
     for (int j = m - 3; j >= 1; --j) {
         const int row = off + j;
         const double dj = sub(ob[row * sz], mul(p.w[row], dnext));
@@ -301,6 +303,7 @@ __global__ void k_staged_finish(const StagedArgs p) {
         ue = dvd(sub(dl, mul(sc_last, next_first)), det_next);
     }
     ob[(long long)off * sz] = us;
+    #pragma unroll 8
     for (int j = 1; j < m - 1; ++j) {
         const int row = off + j;
         ob[row * sz] = sub(ob[row * sz], add(mul(p.sa[row], us), mul(p.sc[row], ue)));
@@ -315,12 +318,15 @@ __global__ void k_thomas(const StagedArgs p) {
     if (line >= p.lines) return;
     const int n = p.rows;
     const long long sz = p.sz;
-    const double* ub = p.u + line_base(line, p.rows, p.sz);
-    double* ob = p.out + line_base(line, p.rows, p.sz);
+    // u and out never alias (the ABI requires distinct buffers): the row
+    // loads can run ahead of the stores
+    const double* __restrict__ ub = p.u + line_base(line, p.rows, p.sz);
+    double* __restrict__ ob = p.out + line_base(line, p.rows, p.sz);
     const long long hb = halo_base(line, p.sz);
     double u0 = fetch(p, ub, hb, -2), u1 = fetch(p, ub, hb, -1);
     double u2 = fetch(p, ub, hb, 0), u3 = fetch(p, ub, hb, 1);
     double dprev = 0.0;
+    #pragma unroll 8
     for (int j = 0; j < n; ++j) {
         const double u4 = fetch(p, ub, hb, j + 2);
         const int sh = row_shift(p, j);
@@ -333,6 +339,7 @@ __global__ void k_thomas(const StagedArgs p) {
         u0 = u1; u1 = u2; u2 = u3; u3 = u4;
     }
     double dnext = dprev;
+    #pragma unroll 8
     for (int j = n - 2; j >= 0; --j) {
         const double dj = sub(ob[j * sz], mul(p.th_cp[j], dnext));
         ob[j * sz] = dj;
@@ -341,6 +348,7 @@ __global__ void k_thomas(const StagedArgs p) {
     if (p.periodic) {
         const double y0 = dnext, yl = ob[(long long)(n - 1) * sz];
         const double fac = dvd(add(y0, mul(p.th_qlast, yl)), p.th_den);
+        #pragma unroll 8
         for (int j = 0; j < n; ++j) ob[j * sz] = sub(ob[j * sz], mul(fac, p.th_z[j]));
     }
 }
