@@ -245,6 +245,41 @@ __device__ __forceinline__ void sweeps_src(const UniformTable& T, Src v, double 
     d[0] = fma(-T.w[0], d[1], d[0]) * T.f[0];
 }
 
+// Two solves of the SAME window (d/dx and d2/dx2 of u_i) in one pass: every
+// window value is read once for both stencils and both forward / backward
+// sweeps interleave (independent recurrences: twice the ILP per thread).
+template <int M, typename Src>
+__device__ __forceinline__ void sweeps2_src(const UniformTable& T1, const UniformTable& T2, Src v,
+                                            double (&d1)[M], double (&d2)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const double v0 = v(i), v1 = v(i + 1), v2 = v(i + 2), v3 = v(i + 3), v4 = v(i + 4);
+        double a = T1.st[0] * v0, b = T2.st[0] * v0;
+        a = fma(T1.st[1], v1, a);
+        b = fma(T2.st[1], v1, b);
+        a = fma(T1.st[2], v2, a);
+        b = fma(T2.st[2], v2, b);
+        a = fma(T1.st[3], v3, a);
+        b = fma(T2.st[3], v3, b);
+        a = fma(T1.st[4], v4, a);
+        b = fma(T2.st[4], v4, b);
+        if (i < 2) {
+            d1[i] = a * T1.r[i];
+            d2[i] = b * T2.r[i];
+        } else {
+            d1[i] = fma(-T1.r[i], d1[i - 1], a) * T1.f[i];
+            d2[i] = fma(-T2.r[i], d2[i - 1], b) * T2.f[i];
+        }
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) {
+        d1[i] = fma(-T1.w[i], d1[i + 1], d1[i]);
+        d2[i] = fma(-T2.w[i], d2[i + 1], d2[i]);
+    }
+    d1[0] = fma(-T1.w[0], d1[1], d1[0]) * T1.f[0];
+    d2[0] = fma(-T2.w[0], d2[1], d2[0]) * T2.f[0];
+}
+
 __device__ __forceinline__ double subst(const UniformTable& T, int i, int M, double F, double L,
                                         double di) {
     return i == 0 ? F : (i == M - 1 ? L : fma(-T.sc[i], L, fma(-T.sa[i], F, di)));
@@ -391,39 +426,51 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
         double acc[M], d[M];
         double F, L;
 
-        // (A) d(u_i)/dx_j -> acc = u_j * du_i
-        sweeps_src<M>(T1, [&](int i) { return Ti[wrap(i)]; }, d);
-        double* Y = Y0;
-        Y[(2 * chunk) * TLT + lane] = d[0];
-        Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
-        __syncthreads();
-        band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, Y, K, lane, F, L);
-#pragma unroll
-        for (int i = 0; i < M; ++i) acc[i] = Tj[wrap(i + 2)] * subst(T1, i, M, F, L, d[i]);
-
-        // (B) d(u_j u_i)/dx_j -> acc = -1/2 (acc + dprod)
-        sweeps_src<M>(T1, [&](int i) { const int o = wrap(i); return Tj[o] * Ti[o]; }, d);
-        if (!p.has_nu) release(nxt);
-        Y += ybuf;
-        Y[(2 * chunk) * TLT + lane] = d[0];
-        Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
-        __syncthreads();
-        band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, Y, K, lane, F, L);
-#pragma unroll
-        for (int i = 0; i < M; ++i) acc[i] = -0.5 * (acc[i] + subst(T1, i, M, F, L, d[i]));
-
-        // (C) acc += nu d2(u_i)/dx_j2
+        // Pass 1 -- the two solves of u_i: (A) d(u_i)/dx_j and (C) d2(u_i)/dx_j2
+        // from one read of the window, one barrier for both reduced systems:
+        //   acc = -1/2 u_j du_i + nu d2u_i
         if (p.has_nu) {
-            sweeps_src<M>(T2, [&](int i) { return Ti[wrap(i)]; }, d);
-            release(nxt);
-            Y += ybuf;
-            Y[(2 * chunk) * TLT + lane] = d[0];
-            Y[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            double d2[M];
+            sweeps2_src<M>(T1, T2, [&](int i) { return Ti[wrap(i)]; }, d, d2);
+            double* YA = Y0;
+            double* YC = Y0 + 2 * ybuf;
+            YA[(2 * chunk) * TLT + lane] = d[0];
+            YA[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            YC[(2 * chunk) * TLT + lane] = d2[0];
+            YC[(2 * chunk + 1) * TLT + lane] = d2[M - 1];
             __syncthreads();
-            band_bounds<TLT>(p.Hb2 + (size_t)chunk * p.nb2, bq2, p.nb2, Y, K, lane, F, L);
+            double F2, L2;
+            band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, YA, K, lane, F, L);
+            band_bounds<TLT>(p.Hb2 + (size_t)chunk * p.nb2, bq2, p.nb2, YC, K, lane, F2, L2);
 #pragma unroll
-            for (int i = 0; i < M; ++i) acc[i] = fma(p.nu, subst(T2, i, M, F, L, d[i]), acc[i]);
+            for (int i = 0; i < M; ++i)
+                acc[i] = fma(-0.5 * Tj[wrap(i + 2)], subst(T1, i, M, F, L, d[i]),
+                             p.nu * subst(T2, i, M, F2, L2, d2[i]));
+        } else {
+            sweeps_src<M>(T1, [&](int i) { return Ti[wrap(i)]; }, d);
+            double* YA = Y0;
+            YA[(2 * chunk) * TLT + lane] = d[0];
+            YA[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            __syncthreads();
+            band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, YA, K, lane, F, L);
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                acc[i] = -0.5 * Tj[wrap(i + 2)] * subst(T1, i, M, F, L, d[i]);
         }
+
+        // Pass 2 -- (B) d(u_j u_i)/dx_j: acc -= 1/2 dprod. Its sweeps are the
+        // last reads of the tiles: hand them to the next item's TMA.
+        sweeps_src<M>(T1, [&](int i) { const int o = wrap(i); return Tj[o] * Ti[o]; }, d);
+        release(nxt);
+        {
+            double* YB = Y0 + ybuf;
+            YB[(2 * chunk) * TLT + lane] = d[0];
+            YB[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            __syncthreads();
+            band_bounds<TLT>(p.Hb1 + (size_t)chunk * p.nb1, bq1, p.nb1, YB, K, lane, F, L);
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) acc[i] = fma(-0.5, subst(T1, i, M, F, L, d[i]), acc[i]);
         if (valid && GEOM == GEOM_XY) {
             // x-layout address of (x, y, z): ((y/sz + z n/sz) n + x) sz + y % sz
             const long long tile = line / TLT;
