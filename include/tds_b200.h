@@ -280,6 +280,19 @@ int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const double* u_
 int tds_transport_contribution_in_x(const tds_plan* d1, const tds_plan* d2, const double* u_i,
                                     const double* u_j, double* acc, double nu, int nx, int ny,
                                     int nz, int sz, int dir, void* stream);
+/* All three components' contributions along ONE direction `dir` (0 x, 1 y,
+ * 2 z) for an (nx, ny, nz) block with every array in the x layout (groups =
+ * ny nz/sz, rows, sz): out_i = (dir 0) or += (dir 1, 2) -1/2 (u_dir du_i +
+ * d(u_dir u_i)) + nu d2u_i along dir, for i = 0, 1, 2, in one pass that reads
+ * u0, u1, u2 once (k_transport_dir). Replaces the three
+ * directional_contribution calls of one direction plus their reorders
+ * (momentum.py:102-169): three launches evaluate the whole RHS. Plans as for
+ * tds_transport_contribution_in_x (16-row-chunk P=1 d/dx and d2/dx2 of the
+ * line length); y needs sz = 32 and 8 | nx. TDS_ERR_UNSUPPORTED otherwise. */
+int tds_transport_direction(const tds_plan* d1, const tds_plan* d2, const double* u0,
+                            const double* u1, const double* u2, double* out0, double* out1,
+                            double* out2, double nu, int nx, int ny, int nz, int sz, int dir,
+                            void* stream);
 /* cubic n^3 field: SZ-blocked layout of src_dir -> dst_dir in one pass
  * (reorder, layout.py:144-152); accumulate = 1 adds into dst */
 int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,

@@ -86,6 +86,7 @@ SIGNATURES = {
     "tds_transport_combine": (_I, [_P, _P, _P, _P, _D, _P, _LL, _I, _P]),
     "tds_reorder": (_I, [_P, _P, _I, _I, _I, _I, _I, _P]),
     "tds_transport_contribution_in_x": (_I, [_P, _P, _P, _P, _P, _D, _I, _I, _I, _I, _I, _P]),
+    "tds_transport_direction": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _D, _I, _I, _I, _I, _I, _P]),
     "tds_transport_mailbox_words": (_LL, [_LL, _I]),
     "tds_transport_mailbox_error": (_I, [_P, _LL, _I, ctypes.POINTER(_I)]),
     "tds_fused_transport": (_I, [_P, _P, _P, _P, _P, _D, _LL, _I, _P, _P, _P,

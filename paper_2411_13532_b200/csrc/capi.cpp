@@ -482,6 +482,9 @@ int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const do
                                 const double* uj, double* out, double nu, int accumulate,
                                 long long lines, int sz, cudaStream_t s, int geom, int nx = 0,
                                 int ny = 0, int nz = 0);
+int transport_direction_from_plans(const tds_plan* d1, const tds_plan* d2, const double* const* u,
+                                   double* const* out, double nu, int nx, int ny, int nz, int sz,
+                                   int dir, cudaStream_t s);
 }  // namespace tds
 
 extern "C" int tds_transport_contribution(const tds_plan* d1, const tds_plan* d2,
@@ -522,6 +525,31 @@ extern "C" int tds_transport_contribution_in_x(const tds_plan* d1, const tds_pla
     const long long lines = dir == 1 ? (long long)nx * nz : (long long)nx * ny;
     return tds::transport_launch_from_plans(d1, nu != 0.0 ? d2 : nullptr, u_i, u_j, acc, nu, 1,
                                             lines, sz, S(stream), dir == 2 ? 1 : 2, nx, ny, nz);
+}
+
+extern "C" int tds_transport_direction(const tds_plan* d1, const tds_plan* d2, const double* u0,
+                                       const double* u1, const double* u2, double* out0,
+                                       double* out1, double* out2, double nu, int nx, int ny,
+                                       int nz, int sz, int dir, void* stream) {
+    if (!d1 || !u0 || !u1 || !u2 || !out0 || !out1 || !out2)
+        return set_err(TDS_ERR_INVALID, "null argument");
+    if (dir < 0 || dir > 2) return set_err(TDS_ERR_INVALID, "dir must be 0, 1 or 2");
+    if (nx < 1 || ny < 1 || nz < 1 || sz < 1 || ny % sz)
+        return set_err(TDS_ERR_INVALID, "bad block extents (sz must divide ny)");
+    const int rows = dir == 0 ? nx : (dir == 1 ? ny : nz);
+    const bool ok1 = d1->path == TDS_PATH_FAST && d1->uniform && d1->M == 16 && d1->P == 1 &&
+                     d1->rank < 0 && !d1->special_first && !d1->special_last &&
+                     d1->block_rows == rows;
+    const bool ok2 = !d2 || (d2->path == TDS_PATH_FAST && d2->uniform && d2->M == 16 &&
+                             d2->P == 1 && d2->rank < 0 && d2->C == d1->C &&
+                             !d2->special_first && !d2->special_last);
+    if (!ok1 || !ok2 || (nu != 0.0 && !d2))
+        return set_err(TDS_ERR_UNSUPPORTED,
+                       "direction transport needs uniform P=1 plans with 16-row chunks");
+    const double* u[3] = {u0, u1, u2};
+    double* out[3] = {out0, out1, out2};
+    return tds::transport_direction_from_plans(d1, nu != 0.0 ? d2 : nullptr, u, out, nu, nx, ny,
+                                               nz, sz, dir, S(stream));
 }
 
 extern "C" int tds_reorder3(const double* src, double* dst, int nx, int ny, int nz, int sz,

@@ -458,6 +458,28 @@ int upload_H(tds_plan* p, const vector<double>& H, const vector<double>& gv) {
             for (int j = 0; j < nb; ++j) Hb[size_t(k) * nb + j] = Hp[size_t(k) * K + (st + j) % K];
         }
         p->band_n = nb;
+        // block-circulant check on the whole map: row k is row 0 shifted by
+        // two columns per chunk (to 2^-45 of its largest entry); chunk k's
+        // band then starts at (q0[0] + 2k) mod K
+        p->band_circ = 0;
+        p->band_row.clear();
+        if (p->periodic && p->P == 1 && p->uniform && C >= 2) {
+            double mx = 0.0;
+            for (int q = 0; q < K; ++q)
+                mx = std::max({mx, std::fabs(Hp[q].x), std::fabs(Hp[q].y)});
+            const double tol = std::ldexp(mx, -45);
+            bool circ = true;
+            for (int k = 1; k < C && circ; ++k)
+                for (int q = 0; q < K && circ; ++q) {
+                    const double2 a = Hp[size_t(k) * K + (q + 2 * k) % K], b = Hp[q];
+                    if (std::fabs(a.x - b.x) > tol || std::fabs(a.y - b.y) > tol) circ = false;
+                }
+            if (circ) {
+                p->band_circ = 1;
+                p->band_q0 = q0[0];
+                p->band_row.assign(Hb.begin(), Hb.begin() + nb);
+            }
+        }
         if ((rc = upload(p, &p->d_Hb, Hb.data(), Hb.size()))) return rc;
         if ((rc = upload(p, &p->d_bq0, q0.data(), q0.size()))) return rc;
     }

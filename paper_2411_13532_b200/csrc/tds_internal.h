@@ -208,5 +208,12 @@ struct tds_plan {
     // closures that reach past the width-5 window: open d2/dx2)
     int sh[4] = {0, 0, 0, 0};
 
+    // banded reduced map of a block-circulant H (uniform periodic P=1 plan:
+    // every chunk's band row is the same nb values, chunk k's window starting
+    // at (band_q0 + 2k) mod K): the row, for kernels that keep it in the
+    // kernel-parameter bank (k_transport_dir). band_circ = 0 otherwise.
+    int band_circ = 0, band_q0 = 0;
+    std::vector<double2> band_row;
+
     std::vector<void*> allocs;
 };

@@ -15,6 +15,7 @@
 //   k_transport_combine   elementwise combine for the rank-emulated path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -626,6 +627,513 @@ int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
         if (tl == 8) return launch_transport_tma_t<16, 8, GEOM_LINES>(a, s);
     }
     return set_err(TDS_ERR_UNSUPPORTED, "fused transport: shape not TMA-tileable");
+}
+
+// ------------------------------------------- one direction, all components
+//
+// k_transport_dir<TLT, GEOM, SZC>: the three contributions of ONE direction
+// j (components i = 0, 1, 2) in one pass. Per item the u_0, u_1, u_2 tiles of
+// TLT lines arrive by TMA, each on its own mbarrier, and feed the nine
+// compact solves of the item. HBM sees every velocity component once per
+// direction (instead of 5 tile reads for 3 per-term launches) and every
+// output once: 48 B/pt for the x pass (3 reads + 3 writes), 72 B/pt for the
+// in-place y / z passes (3 reads + 3 read-modify-writes).
+//
+// A component phase is the two passes of k_transport_tma: d/dx and d2/dx2
+// of u_i from one read of the window (one barrier for both reduced
+// systems), then d/dx of u_j u_i. Its product sweeps are the phase's last
+// reads of u_i, so right after the second barrier thread 0 re-arms that
+// tile for the next item. Components run in the order a, b, j (j = the
+// advecting one, read by every phase): u_a loads during phases b and j, u_b
+// during j and the next item's a, u_j during the next item's first sweeps
+// (it is first needed by the a combine). 16-line tiles: one CTA of 512
+// threads and 3 x 64 KB of tiles per SM at n = 512.
+//
+// Instruction diet (the kernel is issue / latency bound, not HBM bound):
+// per-row coefficients of both operators sit in shared memory as 16-byte
+// pairs (DirRow, one LDS.128 per pair); and the periodic P = 1 reduced map
+// is block-circulant, so every chunk's band row is the same nb values --
+// they travel in the kernel-parameter bank and enter the bounds as
+// constant DFMA operands (no loads), fully unrolled.
+constexpr int NBC_MAX = 24;
+
+// per-row coefficients of the d/dx (1) and d2/dx2 (2) chunk tables
+struct DirRow {
+    double2 rf1, rf2;         // (r, f)
+    double2 w12;              // (w1, w2)
+    double2 s1, s2;           // (sa, sc)
+};
+
+struct TransportDirArgs {
+    TransportArgs p;          // geometry, tables and reduced maps (ui/uj/out unused)
+    const double* u[3];
+    double* out[3];
+    CUtensorMap map[3];
+    int boxr;
+    int jdir;                 // solve direction = the advecting component
+    long long items;
+    int nbc1, nbc2;           // circulant band length and first column of chunk 0
+    int q01, q02;
+    int ydup;                 // Y entries duplicated past K (>= both band lengths, even)
+    double2 hc1[NBC_MAX], hc2[NBC_MAX];
+};
+
+
+namespace {
+
+// two solves of one window (tables 1 and 2) / one solve (table 1), the
+// arithmetic of sweeps2_src / sweeps_src with the DirRow table
+template <int M, typename Src>
+__device__ __forceinline__ void dsweeps2(const DirRow (&R)[16], const double* st1,
+                                         const double* st2, Src v, double (&d1)[M],
+                                         double (&d2)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const double v0 = v(i), v1 = v(i + 1), v2 = v(i + 2), v3 = v(i + 3), v4 = v(i + 4);
+        double a = st1[0] * v0, b = st2[0] * v0;
+        a = fma(st1[1], v1, a);
+        b = fma(st2[1], v1, b);
+        a = fma(st1[2], v2, a);
+        b = fma(st2[2], v2, b);
+        a = fma(st1[3], v3, a);
+        b = fma(st2[3], v3, b);
+        a = fma(st1[4], v4, a);
+        b = fma(st2[4], v4, b);
+        const double2 rf1 = R[i].rf1, rf2 = R[i].rf2;
+        if (i < 2) {
+            d1[i] = a * rf1.x;
+            d2[i] = b * rf2.x;
+        } else {
+            d1[i] = fma(-rf1.x, d1[i - 1], a) * rf1.y;
+            d2[i] = fma(-rf2.x, d2[i - 1], b) * rf2.y;
+        }
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) {
+        const double2 w = R[i].w12;
+        d1[i] = fma(-w.x, d1[i + 1], d1[i]);
+        d2[i] = fma(-w.y, d2[i + 1], d2[i]);
+    }
+    const double2 w = R[0].w12;
+    d1[0] = fma(-w.x, d1[1], d1[0]) * R[0].rf1.y;
+    d2[0] = fma(-w.y, d2[1], d2[0]) * R[0].rf2.y;
+}
+
+template <int M, typename Src>
+__device__ __forceinline__ void dsweeps1(const DirRow (&R)[16], const double* st, Src v,
+                                         double (&d)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double rhs = st[0] * v(i);
+        rhs = fma(st[1], v(i + 1), rhs);
+        rhs = fma(st[2], v(i + 2), rhs);
+        rhs = fma(st[3], v(i + 3), rhs);
+        rhs = fma(st[4], v(i + 4), rhs);
+        const double2 rf = R[i].rf1;
+        if (i < 2) d[i] = rhs * rf.x;
+        else d[i] = fma(-rf.x, d[i - 1], rhs) * rf.y;
+    }
+#pragma unroll
+    for (int i = M - 3; i >= 1; --i) d[i] = fma(-R[i].w12.x, d[i + 1], d[i]);
+    d[0] = fma(-R[0].w12.x, d[1], d[0]) * R[0].rf1.y;
+}
+
+__device__ __forceinline__ double subst2(double2 s, int i, int M, double F, double L, double di) {
+    return i == 0 ? F : (i == M - 1 ? L : fma(-s.y, L, fma(-s.x, F, di)));
+}
+
+// (F, L) of a chunk from a circulant band row held in the parameter bank:
+// the same terms and association as band_bounds (even columns into F0 / L0,
+// odd into F1 / L1). Yb = this chunk's first band column in the extended Y
+// buffer (K entries plus a copy of the first NBC_MAX: no wrap), so every
+// read is an immediate offset from one address.
+template <int TLT>
+__device__ __forceinline__ void circ_bounds(const double2 (&h)[NBC_MAX], int nb,
+                                            const double* Yb, double& F, double& L) {
+    double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NBC_MAX; ++j) {
+        if (j < nb) {
+            const double y = Yb[j * TLT];
+            if (j & 1) {
+                F1 = fma(h[j].x, y, F1);
+                L1 = fma(h[j].y, y, L1);
+            } else {
+                F0 = fma(h[j].x, y, F0);
+                L0 = fma(h[j].y, y, L0);
+            }
+        }
+    }
+    F = F0 + F1;
+    L = L0 + L1;
+}
+
+}  // namespace
+
+template <int TLT, int GEOM, int SZC>
+__global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ TransportDirArgs A) {
+    constexpr int M = 16;
+    constexpr bool ACC = GEOM != GEOM_LINES;   // x pass writes, y / z passes add
+    const TransportArgs& p = A.p;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int C = p.chunks, K = 2 * C, rows = p.rows, tpc = p.tiles_per_cta;
+    const int t = threadIdx.x;
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
+    const long long sz = SZC ? SZC : p.sz;
+    const int r0 = chunk * M;
+    const size_t tile_elems = (size_t)rows * TLT;
+    const size_t field_elems = (size_t)tpc * tile_elems;
+    double* tiles = reinterpret_cast<double*>(smem);            // [3][tpc][rows][TLT]
+    const int KE = K + A.ydup;                                   // extended Y: no wrap
+    double* sY = tiles + 3 * field_elems;                        // [3][tpc][KE][TLT]
+    const size_t ybuf = (size_t)tpc * KE * TLT;
+    DirRow* sR = reinterpret_cast<DirRow*>(sY + 3 * ybuf);       // [M]
+    double* sst = reinterpret_cast<double*>(sR + M);             // stencils [2][5] (+ pad)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sst + 12);       // one per component tile
+    for (int i = t; i < M; i += blockDim.x) {
+        DirRow r;
+        r.rf1 = make_double2(p.t1.r[i], p.t1.f[i]);
+        r.rf2 = make_double2(p.t2.r[i], p.t2.f[i]);
+        r.w12 = make_double2(p.t1.w[i], p.t2.w[i]);
+        r.s1 = make_double2(p.t1.sa[i], p.t1.sc[i]);
+        r.s2 = make_double2(p.t2.sa[i], p.t2.sc[i]);
+        sR[i] = r;
+    }
+    if (t < 10) sst[t] = t < 5 ? p.t1.st[t] : p.t2.st[t - 5];
+    // (a kernel-parameter copy of the table is hoisted into registers and
+    // spills: measured 10.6 vs 9.87 ms for the 512^3 RHS)
+    const DirRow (&RT)[16] = *reinterpret_cast<const DirRow(*)[16]>(sR);
+    const double* st1 = sst;
+    const double* st2 = sst + 5;
+    // circulant band: chunk k's window starts at (q0 + 2k) mod K
+    const int q1 = (A.q01 + 2 * chunk) % K, q2 = (A.q02 + 2 * chunk) % K;
+    const bool dup = 2 * chunk < A.ydup;   // this chunk's Y entries also go to K + 2k
+    const int jd = A.jdir;
+    const int ca = jd == 0 ? 1 : 0, cb = jd == 2 ? 1 : 2;
+
+    auto issue = [&](int c, long long item) {
+        uint32_t bytes = 0;
+        for (int q = 0; q < tpc; ++q)
+            if ((item * tpc + q) * TLT < p.lines)
+                bytes += (uint32_t)(tile_elems * sizeof(double));
+        mbar_expect_tx(bar + c, bytes);
+        double* dst0 = tiles + c * field_elems;
+        const CUtensorMap* map = &A.map[c];
+        for (int q = 0; q < tpc; ++q) {
+            const long long first = (item * tpc + q) * TLT;
+            if (first >= p.lines) break;
+            double* dst = dst0 + q * tile_elems;
+            if (GEOM == GEOM_XY) {
+                const long long tile = first / TLT;
+                const int nxb = p.nx / TLT;
+                const int x0 = (int)(tile % nxb) * TLT, z = (int)(tile / nxb);
+                const size_t half = tile_elems / 2;
+                for (int h = 0; h < 2; ++h) tma_load_4d(dst + h * half, map, bar + c, h * 16, x0, 0, z);
+            } else if (GEOM == GEOM_XZ) {
+                const long long tile = first / TLT;
+                const int nlb = p.sz / TLT, ngj = p.ny / p.sz;
+                const int l0 = (int)(tile % nlb) * TLT;
+                const int gj = (int)((tile / nlb) % ngj);
+                const int x = (int)(tile / ((long long)nlb * ngj));
+                for (int b = 0; b * A.boxr < rows; ++b)
+                    tma_load_4d(dst + (size_t)b * A.boxr * TLT, map, bar + c, l0, x, gj, b * A.boxr);
+            } else {
+                const int g = (int)(first / p.sz), l0 = (int)(first % p.sz);
+                for (int b = 0; b * A.boxr < rows; ++b)
+                    tma_load_3d(dst + (size_t)b * A.boxr * TLT, map, bar + c, l0, b * A.boxr, g);
+            }
+        }
+    };
+
+    if (t == 0) {
+        for (int c = 0; c < 3; ++c) mbar_init(bar + c, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    long long item = blockIdx.x;
+    if (t == 0 && item < A.items) {
+        issue(ca, item);
+        issue(jd, item);
+        issue(cb, item);
+    }
+    uint32_t phases = 0;   // bit c: parity of the next completion of tile c
+
+    // window offsets (the same in every tile): see k_transport_tma
+    const int xy_half = rows * TLT / 2;
+    auto xy_off = [&](int y) {
+        return ((y >> 4) & 1) * xy_half + (((y >> 5) * TLT + lane) << 4) +
+               ((((y & 15) >> 1) ^ (lane & 7)) << 1) + (y & 1);
+    };
+    const int base = GEOM == GEOM_XY ? xy_off(r0) - ((lane & 7) << 1) : r0 * TLT + lane;
+    const int lo = GEOM == GEOM_XY ? 0 : (chunk == 0 ? rows - 2 : r0 - 2) * TLT + lane;
+    const int hi = GEOM == GEOM_XY ? 0 : (chunk == C - 1 ? 0 : r0 + M) * TLT + lane;
+    const int ylo = chunk == 0 ? rows - 2 : r0 - 2, yhi = chunk == C - 1 ? 0 : r0 + M;
+    const int xh0 = GEOM == GEOM_XY ? xy_off(ylo) : 0, xh1 = GEOM == GEOM_XY ? xy_off(ylo + 1) : 0;
+    const int xh2 = GEOM == GEOM_XY ? xy_off(yhi) : 0, xh3 = GEOM == GEOM_XY ? xy_off(yhi + 1) : 0;
+    auto wrap = [&](int i) {
+        if (GEOM == GEOM_XY) {
+            if (i < 2) return i == 0 ? xh0 : xh1;
+            if (i >= M + 2) return i == M + 2 ? xh2 : xh3;
+            const int l = i - 2;
+            return base + ((((l >> 1) ^ (lane & 7))) << 1) + (l & 1);
+        }
+        return i < 2 ? lo + i * TLT : (i >= M + 2 ? hi + (i - M - 2) * TLT : base + (i - 2) * TLT);
+    };
+    double* Y0 = sY + (size_t)tl * KE * TLT;
+    double* YA = Y0;
+    double* YB = Y0 + ybuf;
+    double* YC = Y0 + 2 * ybuf;
+    auto post = [&](double* Y, double first, double last) {
+        Y[(2 * chunk) * TLT + lane] = first;
+        Y[(2 * chunk + 1) * TLT + lane] = last;
+        if (dup) {
+            Y[(K + 2 * chunk) * TLT + lane] = first;
+            Y[(K + 2 * chunk + 1) * TLT + lane] = last;
+        }
+    };
+    const int yo1 = q1 * TLT + lane, yo2 = q2 * TLT + lane;
+    auto wait_tile = [&](int c) {
+        const uint32_t ph = (phases >> c) & 1u;
+        while (!mbar_try_wait(bar + c, ph)) {
+        }
+        phases ^= 1u << c;
+    };
+
+    for (; item < A.items; item += gridDim.x) {
+        const long long line = (item * tpc + tl) * TLT + lane;
+        const bool valid = line < p.lines;
+        const long long nxt = item + gridDim.x;
+        // this thread's output rows (component offset added per phase)
+        long long orow = 0, ostride = sz;
+        if (GEOM == GEOM_XY) {
+            const long long tile = line / TLT;
+            const int nxb = p.nx / TLT;
+            const long long x = (tile % nxb) * TLT + lane, z = tile / nxb;
+            orow = (((long long)(r0 >> 5) + z * (p.ny / p.sz)) * p.nx + x) * sz + (r0 & 31);
+            ostride = 1;
+        } else if (GEOM == GEOM_XZ) {
+            const long long tile = line / TLT;
+            const int nlb = p.sz / TLT, ngj = p.ny / p.sz;
+            const long long x = tile / ((long long)nlb * ngj);
+            const long long gj = (tile / nlb) % ngj;
+            ostride = (long long)p.nx * p.ny;
+            orow = (gj * p.nx + x) * sz + (tile % nlb) * TLT + lane + r0 * ostride;
+        } else {
+            orow = valid ? line_base_t<SZC>(line, rows, p.sz) + (long long)r0 * sz : 0;
+        }
+        const double* Tj = tiles + jd * field_elems + tl * tile_elems;
+#pragma unroll 1
+        for (int s = 0; s < 3; ++s) {
+            const int c = s == 0 ? ca : (s == 1 ? cb : jd);
+            const double* Tc = tiles + c * field_elems + tl * tile_elems;
+            double* ob = A.out[c] + orow;
+            if (c != jd) wait_tile(c);   // u_j: waited for once per item, below
+            double acc[M], d[M];
+            double F, L;
+
+            // pass 1: d(u_c) and d2(u_c) from one read of the window
+            if (p.has_nu) {
+                double d2[M];
+                dsweeps2<M>(RT, st1, st2, [&](int i) { return Tc[wrap(i)]; }, d, d2);
+                post(YA, d[0], d[M - 1]);
+                post(YC, d2[0], d2[M - 1]);
+                __syncthreads();
+                if (s == 0) wait_tile(jd);
+                double F2, L2;
+                circ_bounds<TLT>(A.hc1, A.nbc1, YA + yo1, F, L);
+                circ_bounds<TLT>(A.hc2, A.nbc2, YC + yo2, F2, L2);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const DirRow& R = RT[i];
+                    acc[i] = fma(-0.5 * Tj[wrap(i + 2)], subst2(R.s1, i, M, F, L, d[i]),
+                                 p.nu * subst2(R.s2, i, M, F2, L2, d2[i]));
+                }
+            } else {
+                dsweeps1<M>(RT, st1, [&](int i) { return Tc[wrap(i)]; }, d);
+                post(YA, d[0], d[M - 1]);
+                __syncthreads();
+                if (s == 0) wait_tile(jd);
+                circ_bounds<TLT>(A.hc1, A.nbc1, YA + yo1, F, L);
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+                    acc[i] = -0.5 * Tj[wrap(i + 2)] * subst2(RT[i].s1, i, M, F, L, d[i]);
+            }
+
+            double old[M];
+            if (ACC) {
+                // old accumulator rows, in flight during the product sweeps
+                if (GEOM == GEOM_XY) {
+                    const double2* o2 = reinterpret_cast<const double2*>(ob);
+#pragma unroll
+                    for (int i = 0; i < M / 2; ++i) {
+                        const double2 o = valid ? __ldcs(o2 + i) : make_double2(0.0, 0.0);
+                        old[2 * i] = o.x;
+                        old[2 * i + 1] = o.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) old[i] = valid ? __ldcs(ob + i * ostride) : 0.0;
+                }
+            }
+            // pass 2: d(u_j u_c); its sweeps are the phase's last tile reads
+            dsweeps1<M>(RT, st1, [&](int i) { const int o = wrap(i); return Tj[o] * Tc[o]; }, d);
+            post(YB, d[0], d[M - 1]);
+            __syncthreads();
+            if (t == 0 && nxt < A.items) {
+                fence_proxy_async();
+                issue(c, nxt);
+            }
+            circ_bounds<TLT>(A.hc1, A.nbc1, YB + yo1, F, L);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                acc[i] = fma(-0.5, subst2(RT[i].s1, i, M, F, L, d[i]), acc[i]);
+                if (ACC) acc[i] = old[i] + acc[i];
+            }
+            if (valid) {
+                if (GEOM == GEOM_XY) {
+                    double2* o2 = reinterpret_cast<double2*>(ob);
+#pragma unroll
+                    for (int i = 0; i < M / 2; ++i)
+                        __stcs(o2 + i, make_double2(acc[2 * i], acc[2 * i + 1]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) __stcs(ob + i * ostride, acc[i]);
+                }
+            }
+        }
+    }
+}
+
+namespace {
+
+template <int TLT, int GEOM, int SZC = 0>
+int launch_transport_dir_t(const TransportDirArgs& a0, cudaStream_t s) {
+    TransportDirArgs A = a0;
+    const TransportArgs& a = A.p;
+    const int per_tile = a.chunks * TLT;
+    A.p.tiles_per_cta = per_tile >= 256 ? 1 : 256 / per_tile;
+    const long long tiles = (a.lines + TLT - 1) / TLT;
+    A.items = (tiles + A.p.tiles_per_cta - 1) / A.p.tiles_per_cta;
+    if (A.items <= 0) return TDS_OK;
+    int rc;
+    for (int c = 0; c < 3; ++c) {
+        if (GEOM == GEOM_XY) {
+            if ((rc = encode_xy_map(A.u[c], a.nx, a.ny, a.nz, a.sz, TLT, &A.map[c]))) return rc;
+            A.boxr = a.rows;
+        } else if (GEOM == GEOM_XZ) {
+            if ((rc = encode_xz_map(A.u[c], a.nx, a.ny, a.nz, a.sz, 16, TLT, &A.map[c], &A.boxr)))
+                return rc;
+        } else {
+            FastArgs f{};
+            f.u = A.u[c];
+            f.rows = a.rows;
+            f.sz = a.sz;
+            f.lines = a.lines;
+            if ((rc = encode_field_map(f, 16, TLT, &A.map[c], &A.boxr))) return rc;
+        }
+    }
+    const int threads = A.p.tiles_per_cta * per_tile;
+    const size_t smem = (size_t)A.p.tiles_per_cta *
+                            (3 * (size_t)a.rows * TLT + 3 * (size_t)(2 * a.chunks + A.ydup) * TLT) *
+                            sizeof(double) + 16 * sizeof(DirRow) + 12 * sizeof(double) +
+                        3 * sizeof(uint64_t);
+    const void* fn = reinterpret_cast<const void*>(k_transport_dir<TLT, GEOM, SZC>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_transport_dir)"))) return rc;
+    const long long grid = persistent_grid(fn, threads, smem, A.items, 0);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_dir does not fit on an SM");
+    k_transport_dir<TLT, GEOM, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_transport_dir launch");
+}
+
+// tile width of k_transport_dir: 16 lines (one CTA of 512 threads per SM at
+// n = 512; measured 9.87 vs 10.05 ms for the 512^3 RHS against 8-line tiles
+// at two CTAs per SM, whose four chunks per warp read the same banks) unless
+// TDS_TRANSPORT_DIR_TL=8; 0 if no width fits
+int transport_dir_tl(const TransportArgs& a, int ydup, const double* const* u, double* const* out) {
+    for (int c = 0; c < 3; ++c)
+        if (reinterpret_cast<uintptr_t>(u[c]) % 16 || reinterpret_cast<uintptr_t>(out[c]) % 16)
+            return 0;
+    if (box_rows(a.rows, 16) == 0) return 0;
+    int pref = 16;
+    if (const char* e = getenv("TDS_TRANSPORT_DIR_TL")) pref = atoi(e) == 8 ? 8 : 16;
+    for (int tl : {pref, 24 - pref}) {
+        if (a.sz % tl) continue;
+        const int per_tile = a.chunks * tl;
+        if (per_tile > 512) continue;
+        const int tpc = per_tile >= 256 ? 1 : 256 / per_tile;
+        const size_t smem =
+            (size_t)tpc * (3 * (size_t)a.rows * tl + 3 * (size_t)(2 * a.chunks + ydup) * tl) * 8 +
+            16 * sizeof(DirRow) + 96 + 24;
+        if (smem <= 227 * 1024) return tl;
+    }
+    return 0;
+}
+
+}  // namespace
+
+int transport_direction_from_plans(const tds_plan* d1, const tds_plan* d2, const double* const* u,
+                                   double* const* out, double nu, int nx, int ny, int nz, int sz,
+                                   int dir, cudaStream_t s) {
+    TransportDirArgs A{};
+    TransportArgs& a = A.p;
+    a.geom = dir == 0 ? GEOM_LINES : (dir == 1 ? GEOM_XY : GEOM_XZ);
+    a.nx = nx;
+    a.ny = ny;
+    a.nz = nz;
+    a.rows = d1->block_rows;
+    a.sz = sz;
+    a.chunks = d1->C;
+    a.lines = dir == 0 ? (long long)ny * nz : (dir == 1 ? (long long)nx * nz : (long long)nx * ny);
+    a.accumulate = dir != 0;
+    a.has_nu = d2 ? 1 : 0;
+    a.nu = nu;
+    a.t1 = d1->ut;
+    a.t2 = d2 ? d2->ut : d1->ut;
+    a.H1 = d1->d_Hp;
+    a.H2 = d2 ? d2->d_Hp : d1->d_Hp;
+    a.Hb1 = d1->d_Hb;
+    a.Hb2 = d2 ? d2->d_Hb : d1->d_Hb;
+    a.bq1 = d1->d_bq0;
+    a.bq2 = d2 ? d2->d_bq0 : d1->d_bq0;
+    a.nb1 = d1->band_n;
+    a.nb2 = d2 ? d2->band_n : d1->band_n;
+    for (int c = 0; c < 3; ++c) {
+        A.u[c] = u[c];
+        A.out[c] = out[c];
+    }
+    A.jdir = dir;
+    if (!d1->band_circ || d1->band_n > NBC_MAX || (d2 && (!d2->band_circ || d2->band_n > NBC_MAX)))
+        return set_err(TDS_ERR_UNSUPPORTED, "direction transport: reduced map not circulant");
+    A.nbc1 = d1->band_n;
+    A.q01 = d1->band_q0;
+    for (int j = 0; j < d1->band_n; ++j) A.hc1[j] = d1->band_row[j];
+    const tds_plan* e2 = d2 ? d2 : d1;
+    A.nbc2 = e2->band_n;
+    A.q02 = e2->band_q0;
+    for (int j = 0; j < e2->band_n; ++j) A.hc2[j] = e2->band_row[j];
+    A.ydup = std::max(A.nbc1, A.nbc2);
+    A.ydup += A.ydup & 1;
+    if (A.ydup > 2 * a.chunks) return set_err(TDS_ERR_UNSUPPORTED, "direction transport: band > K");
+    const int tl = transport_dir_tl(a, A.ydup, u, out);
+    if (a.geom == GEOM_XY) {
+        if (sz != 32 || ny % 32 || (tl != 16 && tl != 8) || nx % tl)
+            return set_err(TDS_ERR_UNSUPPORTED, "xy transport: sz = 32, 32 | ny, tile | nx");
+        if (tl == 16) return launch_transport_dir_t<16, GEOM_XY>(A, s);
+        return launch_transport_dir_t<8, GEOM_XY>(A, s);
+    }
+    if (a.geom == GEOM_XZ) {
+        if (ny % sz) return set_err(TDS_ERR_UNSUPPORTED, "xz transport: sz must divide ny");
+        if (tl == 16) return launch_transport_dir_t<16, GEOM_XZ>(A, s);
+        if (tl == 8) return launch_transport_dir_t<8, GEOM_XZ>(A, s);
+        return set_err(TDS_ERR_UNSUPPORTED, "direction transport: shape not TMA-tileable");
+    }
+    if (tl == 16 && sz == 32) return launch_transport_dir_t<16, GEOM_LINES, 32>(A, s);
+    if (tl == 8 && sz == 32) return launch_transport_dir_t<8, GEOM_LINES, 32>(A, s);
+    if (tl == 16) return launch_transport_dir_t<16, GEOM_LINES>(A, s);
+    if (tl == 8) return launch_transport_dir_t<8, GEOM_LINES>(A, s);
+    return set_err(TDS_ERR_UNSUPPORTED, "direction transport: shape not TMA-tileable");
 }
 
 // ----------------------------------------------------------- re-layout

@@ -184,7 +184,12 @@ def _reorder_tensor(data, n, sz, src, dst, out=None, accumulate=False):
 
 def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     """Full right-hand side of all three components, x-layout results
-    (momentum.py:142-169)."""
+    (momentum.py:142-169).
+
+    Default: one `k_transport_dir` launch per direction (x writes the
+    accumulators, y / z add into them in place), each reading u, v, w once
+    (`tds_transport_direction`). Shapes it cannot tile take the per-term
+    kernels below, direction by direction."""
     torch = _torch()
     if fields.layout.direction != "x":
         raise ValueError("inputs must arrive in x layout")
@@ -193,17 +198,21 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
     if lay.pad:
         raise NotImplementedError("padded layouts are not supported by the GPU transport demo")
     acc = [torch.empty_like(fields.component(i).data) for i in range(3)]
-    for i in range(3):
-        _contribution_into(i, "x", fields, acc[i], False, rank_count)
-    scratch = torch.empty_like(acc[0])
+    done = _direction_passes(fields, acc, (0, 1, 2)) if rank_count == 1 else set()
+    if 0 not in done:
+        for i in range(3):
+            _contribution_into(i, "x", fields, acc[i], False, rank_count)
+    scratch = None
     # y / z contributions read in place from the x layout and added into the
     # accumulators (k_transport_tma GEOM_XY / GEOM_XZ) when the box allows
     for dj in ("y", "z"):
+        if _DIRECTIONS.index(dj) in done:
+            continue
         plans = _in_x_plans(fields, dj) if rank_count == 1 else None
         if plans is not None:
             p1, p2 = plans
             adv = fields.component(_DIRECTIONS.index(dj)).data
-            done = 0
+            ndone = 0
             for i in range(3):
                 rc = N.lib().tds_transport_contribution_in_x(
                     p1.handle, None if p2 is None else p2.handle,
@@ -212,8 +221,8 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
                 if rc == N.TDS_ERR_UNSUPPORTED and i == 0:
                     break                     # shape not tileable: reorder path below
                 N.check(rc)
-                done += 1
-            if done == 3:
+                ndone += 1
+            if ndone == 3:
                 continue
         lay_j = LayoutDescriptor(n, n, n, sz, dj)
         _TRUSTED.on = True
@@ -223,10 +232,74 @@ def evaluate_transport_rhs(fields, rank_count=1, ledger=None, catalog=None):
                                   for c in range(3)), fields.nu, fields.h)
         finally:
             _TRUSTED.on = False
+        if scratch is None:
+            scratch = torch.empty_like(acc[0])
         for i in range(3):
             _contribution_into(i, dj, rot, scratch, False, rank_count)
             _reorder_tensor(scratch, n, sz, dj, "x", out=acc[i], accumulate=True)
     return tuple(GroupedField(lay, a) for a in acc)
+
+
+def _direction_plans(h, nu, rows):
+    """16-row-chunk uniform P=1 plans of the d/dx and (nu != 0) d2/dx2
+    operators of `rows`-long periodic lines, or None."""
+    part = SubdomainPartition((rows,))
+    s1, st1 = _operator(1, h, rows)
+    p1 = get_plan(s1, st1, part, chunk_rows=16)
+    if p1.info.chunk_rows != 16 or p1.info.uniform != 1:
+        return None
+    p2 = None
+    if nu != 0.0:
+        s2, st2 = _operator(2, h, rows)
+        p2 = get_plan(s2, st2, part, chunk_rows=16)
+        if p2.info.chunk_rows != 16 or p2.info.uniform != 1:
+            return None
+    return p1, p2
+
+
+def _direction_pass(u, acc, extents, sz, h, nu, dj):
+    """One `tds_transport_direction` launch (k_transport_dir: the three
+    components' contributions along direction dj, u[0..2] read once) on an
+    x-layout (nx, ny, nz) block; dj = 0 writes `acc`, 1 / 2 add into it.
+    False when the kernel cannot tile the shape (per-term path instead).
+    A/B knob: TDS_TRANSPORT_DIR=0."""
+    import os
+    if os.environ.get("TDS_TRANSPORT_DIR") == "0":
+        return False
+    nx, ny, nz = extents
+    rows = extents[dj]
+    if ny % sz or rows % 16:
+        return False
+    plans = _direction_plans(h, nu, rows)
+    if plans is None:
+        return False
+    p1, p2 = plans
+    rc = N.lib().tds_transport_direction(
+        p1.handle, None if p2 is None else p2.handle, _vp(u[0]), _vp(u[1]), _vp(u[2]),
+        _vp(acc[0]), _vp(acc[1]), _vp(acc[2]), float(nu), nx, ny, nz, sz, dj,
+        _stream_handle())
+    if rc == N.TDS_ERR_UNSUPPORTED:
+        return False
+    N.check(rc)
+    return True
+
+
+def _direction_passes(fields, acc, dirs, extents=None):
+    """`_direction_pass` for the directions in `dirs`, in order, stopping at
+    the first one the kernel cannot tile (the rest then run per term, in the
+    same order, so the accumulation order never changes). Returns the set of
+    directions done."""
+    lay = fields.layout
+    if lay.pad:
+        return set()
+    ext = extents if extents is not None else (lay.nx, lay.ny, lay.nz)
+    u = [fields.component(c).data for c in range(3)]
+    done = set()
+    for dj in dirs:
+        if not _direction_pass(u, acc, ext, lay.sz, fields.h, fields.nu, dj):
+            break
+        done.add(dj)
+    return done
 
 
 def _in_x_plans(fields, dj):
@@ -426,18 +499,24 @@ class SlabTransport:
 
     def rhs(self, u, v, w):
         """Local x-layout slabs of u, v, w -> local x-layout RHS of each
-        component (momentum.py:142-169, same per-direction grouping)."""
+        component (momentum.py:142-169, same per-direction grouping). Local
+        directions (x, y; z too on one rank) run as one k_transport_dir
+        launch each when the shape allows it."""
         torch = _torch()
         vel = (u, v, w)
         acc = [torch.empty_like(u) for _ in range(3)]
+        ext = (self.n, self.n, self.m)
         marks = self._marks
         if marks is not None:
             marks[0].record()
-        for i in range(3):
-            _local_contribution(vel[i], vel[0], acc[i], self.n, self.h, self.nu, False)
+        xdir = _direction_pass(vel, acc, ext, self.sz, self.h, self.nu, 0)
+        if not xdir:
+            for i in range(3):
+                _local_contribution(vel[i], vel[0], acc[i], self.n, self.h, self.nu, False)
         if marks is not None:
             marks[1].record()
-        if not self._y_in_place(vel, acc):
+        ydir = xdir and _direction_pass(vel, acc, ext, self.sz, self.h, self.nu, 1)
+        if not ydir and not self._y_in_place(vel, acc):
             rot = [self._reorder(c, "x", "y") for c in vel]
             scratch = torch.empty_like(rot[0])
             for i in range(3):
@@ -445,11 +524,13 @@ class SlabTransport:
                 self._reorder(scratch, "y", "x", out=acc[i], accumulate=True)
         if marks is not None:
             marks[2].record()
-        rot = [self._reorder(c, "x", "z") for c in vel]
-        scratch = torch.empty_like(rot[0])
-        for i in range(3):
-            self._z_contribution(rot[i], rot[2], scratch)
-            self._reorder(scratch, "z", "x", out=acc[i], accumulate=True)
+        if not (self._rank is None and ydir and
+                _direction_pass(vel, acc, ext, self.sz, self.h, self.nu, 2)):
+            rot = [self._reorder(c, "x", "z") for c in vel]
+            scratch = torch.empty_like(rot[0])
+            for i in range(3):
+                self._z_contribution(rot[i], rot[2], scratch)
+                self._reorder(scratch, "z", "x", out=acc[i], accumulate=True)
         if marks is not None:
             marks[3].record()
         return tuple(acc)
