@@ -669,6 +669,7 @@ struct TransportDirArgs {
     const double* u[3];
     double* out[3];
     CUtensorMap map[3];
+    CUtensorMap omap[3];      // the outputs (y / z passes: TMA reduce-add targets)
     int boxr;
     int jdir;                 // solve direction = the advecting component
     long long items;
@@ -847,6 +848,35 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
         }
     };
 
+    // y / z passes: add tile c (holding the item's contribution, in the
+    // layout its load used) into out[c] with the TMA engine -- the inverse
+    // of issue(c, item)
+    auto reduce_out = [&](int c, long long item) {
+        const double* src0 = tiles + c * field_elems;
+        const CUtensorMap* map = &A.omap[c];
+        for (int q = 0; q < tpc; ++q) {
+            const long long first = (item * tpc + q) * TLT;
+            if (first >= p.lines) break;
+            const double* src = src0 + q * tile_elems;
+            if (GEOM == GEOM_XY) {
+                const long long tile = first / TLT;
+                const int nxb = p.nx / TLT;
+                const int x0 = (int)(tile % nxb) * TLT, z = (int)(tile / nxb);
+                const size_t half = tile_elems / 2;
+                for (int h = 0; h < 2; ++h) tma_reduce_add_4d(map, src + h * half, h * 16, x0, 0, z);
+            } else if (GEOM == GEOM_XZ) {
+                const long long tile = first / TLT;
+                const int nlb = p.sz / TLT, ngj = p.ny / p.sz;
+                const int l0 = (int)(tile % nlb) * TLT;
+                const int gj = (int)((tile / nlb) % ngj);
+                const int x = (int)(tile / ((long long)nlb * ngj));
+                for (int b = 0; b * A.boxr < rows; ++b)
+                    tma_reduce_add_4d(map, src + (size_t)b * A.boxr * TLT, l0, x, gj, b * A.boxr);
+            }
+        }
+        bulk_commit();
+    };
+
     if (t == 0) {
         for (int c = 0; c < 3; ++c) mbar_init(bar + c, 1);
         fence_mbar_init();
@@ -880,6 +910,16 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
             return base + ((((l >> 1) ^ (lane & 7))) << 1) + (l & 1);
         }
         return i < 2 ? lo + i * TLT : (i >= M + 2 ? hi + (i - M - 2) * TLT : base + (i - 2) * TLT);
+    };
+    // window row i of a tile; the y-line tiles (GEOM_XY) hold rows 2k, 2k+1
+    // of a line in one 16-byte unit: read it whole (LDS.128, the two calls of
+    // a pair are one load), 4 wavefronts per warp instead of 4 per 8 bytes
+    auto rd = [&](const double* T, int i) -> double {
+        if (GEOM == GEOM_XY) {
+            const double2 q = *reinterpret_cast<const double2*>(T + wrap(i & ~1));
+            return (i & 1) ? q.y : q.x;
+        }
+        return T[wrap(i)];
     };
     double* Y0 = sY + (size_t)tl * KE * TLT;
     double* YA = Y0;
@@ -936,7 +976,7 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
             // pass 1: d(u_c) and d2(u_c) from one read of the window
             if (p.has_nu) {
                 double d2[M];
-                dsweeps2<M>(RT, st1, st2, [&](int i) { return Tc[wrap(i)]; }, d, d2);
+                dsweeps2<M>(RT, st1, st2, [&](int i) { return rd(Tc, i); }, d, d2);
                 post(YA, d[0], d[M - 1]);
                 post(YC, d2[0], d2[M - 1]);
                 __syncthreads();
@@ -947,63 +987,64 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
                     const DirRow& R = RT[i];
-                    acc[i] = fma(-0.5 * Tj[wrap(i + 2)], subst2(R.s1, i, M, F, L, d[i]),
+                    acc[i] = fma(-0.5 * rd(Tj, i + 2), subst2(R.s1, i, M, F, L, d[i]),
                                  p.nu * subst2(R.s2, i, M, F2, L2, d2[i]));
                 }
             } else {
-                dsweeps1<M>(RT, st1, [&](int i) { return Tc[wrap(i)]; }, d);
+                dsweeps1<M>(RT, st1, [&](int i) { return rd(Tc, i); }, d);
                 post(YA, d[0], d[M - 1]);
                 __syncthreads();
                 if (s == 0) wait_tile(jd);
                 circ_bounds<TLT>(A.hc1, A.nbc1, YA + yo1, F, L);
 #pragma unroll
                 for (int i = 0; i < M; ++i)
-                    acc[i] = -0.5 * Tj[wrap(i + 2)] * subst2(RT[i].s1, i, M, F, L, d[i]);
+                    acc[i] = -0.5 * rd(Tj, i + 2) * subst2(RT[i].s1, i, M, F, L, d[i]);
             }
 
-            double old[M];
-            if (ACC) {
-                // old accumulator rows, in flight during the product sweeps
-                if (GEOM == GEOM_XY) {
-                    const double2* o2 = reinterpret_cast<const double2*>(ob);
-#pragma unroll
-                    for (int i = 0; i < M / 2; ++i) {
-                        const double2 o = valid ? __ldcs(o2 + i) : make_double2(0.0, 0.0);
-                        old[2 * i] = o.x;
-                        old[2 * i + 1] = o.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < M; ++i) old[i] = valid ? __ldcs(ob + i * ostride) : 0.0;
-                }
-            }
             // pass 2: d(u_j u_c); its sweeps are the phase's last tile reads
-            dsweeps1<M>(RT, st1, [&](int i) { const int o = wrap(i); return Tj[o] * Tc[o]; }, d);
+            dsweeps1<M>(RT, st1, [&](int i) { return rd(Tj, i) * rd(Tc, i); }, d);
             post(YB, d[0], d[M - 1]);
             __syncthreads();
-            if (t == 0 && nxt < A.items) {
+            if (!ACC && t == 0 && nxt < A.items) {
                 fence_proxy_async();
                 issue(c, nxt);
             }
             circ_bounds<TLT>(A.hc1, A.nbc1, YB + yo1, F, L);
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                acc[i] = fma(-0.5, subst2(RT[i].s1, i, M, F, L, d[i]), acc[i]);
-                if (ACC) acc[i] = old[i] + acc[i];
-            }
-            if (valid) {
-                if (GEOM == GEOM_XY) {
-                    double2* o2 = reinterpret_cast<double2*>(ob);
-#pragma unroll
-                    for (int i = 0; i < M / 2; ++i)
-                        __stcs(o2 + i, make_double2(acc[2 * i], acc[2 * i + 1]));
-                } else {
+            for (int i = 0; i < M; ++i) acc[i] = fma(-0.5, subst2(RT[i].s1, i, M, F, L, d[i]), acc[i]);
+            if (!ACC) {
+                if (valid) {
 #pragma unroll
                     for (int i = 0; i < M; ++i) __stcs(ob + i * ostride, acc[i]);
+                }
+            } else {
+                // the contribution goes into tile c (free since the barrier)
+                // in its load layout, and the TMA engine adds it into out[c]
+                // in L2: no accumulator reads by the SM, and the per-thread
+                // 128-byte rows of a y line never go through the LSU
+                double* Tw = tiles + c * field_elems + tl * tile_elems;
+                if (GEOM == GEOM_XY) {
+#pragma unroll
+                    for (int u = 0; u < M / 2; ++u)
+                        *reinterpret_cast<double2*>(Tw + wrap(2 * u + 2)) =
+                            make_double2(acc[2 * u], acc[2 * u + 1]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) Tw[wrap(i + 2)] = acc[i];
+                }
+                fence_proxy_async();
+                __syncthreads();
+                if (t == 0) {
+                    reduce_out(c, item);
+                    if (nxt < A.items) {
+                        bulk_wait_read<0>();   // the reduce has read the tile
+                        issue(c, nxt);
+                    }
                 }
             }
         }
     }
+    if (ACC && t == 0) bulk_wait_all();   // the last reduces complete before exit
 }
 
 namespace {
@@ -1021,9 +1062,13 @@ int launch_transport_dir_t(const TransportDirArgs& a0, cudaStream_t s) {
     for (int c = 0; c < 3; ++c) {
         if (GEOM == GEOM_XY) {
             if ((rc = encode_xy_map(A.u[c], a.nx, a.ny, a.nz, a.sz, TLT, &A.map[c]))) return rc;
+            if ((rc = encode_xy_map(A.out[c], a.nx, a.ny, a.nz, a.sz, TLT, &A.omap[c]))) return rc;
             A.boxr = a.rows;
         } else if (GEOM == GEOM_XZ) {
             if ((rc = encode_xz_map(A.u[c], a.nx, a.ny, a.nz, a.sz, 16, TLT, &A.map[c], &A.boxr)))
+                return rc;
+            if ((rc = encode_xz_map(A.out[c], a.nx, a.ny, a.nz, a.sz, 16, TLT, &A.omap[c],
+                                    &A.boxr)))
                 return rc;
         } else {
             FastArgs f{};
