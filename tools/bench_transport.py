@@ -7,13 +7,13 @@ Multi-GPU (under torchrun): SlabTransport, rank r owning the z-slab
 rank ring (fused k_dd/k_dd2), x/y contributions are local.
 CUDA events, best of `--reps`, max over ranks.
 
-Logical traffic of the single-GPU fused pipeline per grid point (fp64, 8 B
-per access):
-  x:      3 contributions, fused (diagonal 16 B, off-diagonal 24 B)  =  64 B
-  y, z:   3 one-pass input reorders (16 B each)                       =  48 B
-          3 contributions into scratch                                =  64 B
-          3 reorder-accumulates into x (24 B each)                    =  72 B
-  total   64 + 2 * 184                                                = 432 B
+Algorithmic traffic of the default pipeline (k_transport_dir, one launch
+per direction) per grid point, fp64:
+  x:      read u, v, w + write 3 accumulators                         =  48 B
+  y, z:   read u, v, w + read-modify-write 3 accumulators             =  72 B
+  total                                                               = 192 B
+("logical_gbs_432B" keeps the round-1 figure: the reference-shaped pipeline
+of reorders + per-term kernels moves 432 B/pt.)
 
     python tools/bench_transport.py [--grid 512] [--sz 32] [--nu 0.01]
     python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
@@ -31,6 +31,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_13532_b200 as T  # noqa: E402
 
 BYTES_PER_POINT = 432
+ALGO_BYTES_PER_POINT = 192
 
 
 def main():
@@ -112,6 +113,8 @@ def main():
                           "gdof_per_s": round(pts / (best * 1e-3) / 1e9, 2),
                           "gdof_per_s_per_gpu": round(pts_local / (best * 1e-3) / 1e9, 2),
                           "logical_gbs_432B": round(BYTES_PER_POINT * pts / (best * 1e-3) / 1e9, 1),
+                          "algorithmic_gbs_192B": round(
+                              ALGO_BYTES_PER_POINT * pts_local / (best * 1e-3) / 1e9, 1),
                           "rank0_phase_ms": phases}),
               flush=True)
     if world > 1:
