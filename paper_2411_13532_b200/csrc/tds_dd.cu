@@ -346,6 +346,12 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     const FastArgs& p = A.t.f;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int CW = 32 / TLT;                       // chunks per warp
+    // edge region: the first / last ECH chunks of a tile (plan.cpp dd_defer:
+    // 2 chunks for 16- and 32-line tiles, 4 for 8-line tiles), EW warps per
+    // side, NE stash slots per tile
+    constexpr int ECH = TLT == 8 ? 4 : 2;
+    constexpr int EW = ECH / CW;
+    constexpr int NE = 2 * EW;
     const int C = p.chunks;
     const int K = 2 * C;
     const int rows = p.rows;
@@ -357,17 +363,26 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     const int tl = t / (TLT * C);
     const int wc0 = chunk - (wl / TLT);                // first chunk of my warp
     const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
-    const bool has_first = wc0 == 0, has_last = wc0 + CW - 1 >= C - 1;
+    const bool has_first = wc0 < ECH, has_last = wc0 + CW - 1 >= C - ECH;
     const bool edge_warp = has_first || has_last;
-    // helper roles of two interior warps (k_dd2 runs only with >= 4 warps per
-    // tile): warp 1 forms and posts g0.Y / g1.Y, warp 2 posts the halo rows
-    const int wt = (t >> 5) % (C * TLT / 32);
+    // helper roles of interior warps: form and post g0.Y / g1.Y (gy_role 0 /
+    // 1), post the halo rows. 8- / 16-line tiles (>= 4 warps per tile): warp 1
+    // holds both g.Y roles (one per chunk), warp 2 both halo roles. 32-line
+    // tiles (one chunk per warp, >= 2 EW + 4 warps): one warp per role after
+    // the first-side edge warps.
+    const int NW = C * TLT / 32;
+    const int wt = (t >> 5) % NW;
     const int role = wl / TLT;
-    // with fewer than 4 warps per tile there are no helpers: the first / last
-    // chunk threads post their own halos and ROUND 2
-    const bool helpers = C * TLT / 32 >= 4;
-    const bool halo_lo_poster = helpers ? (wt == 2 && role == 0) : first_chunk;
-    const bool halo_hi_poster = helpers ? (wt == 2 && role == 1) : last_chunk;
+    // without enough warps there are no helpers: the first / last chunk
+    // threads post their own halos and ROUND 2
+    const bool helpers = CW == 1 ? NW >= 2 * EW + 4 : NW >= 4;
+    const int gy_role = !helpers || edge_warp ? -1
+                        : CW == 1 ? (wt == EW ? 0 : (wt == EW + 1 ? 1 : -1))
+                                  : (wt == 1 && role < 2 ? role : -1);
+    const bool halo_lo_poster =
+        helpers ? (CW == 1 ? wt == EW + 2 : (wt == 2 && role == 0)) : first_chunk;
+    const bool halo_hi_poster =
+        helpers ? (CW == 1 ? wt == EW + 3 : (wt == 2 && role == 1)) : last_chunk;
     const long long sz = SZC ? SZC : p.sz;
     const int r0 = chunk * M;
     const Mail mb{p.lines};
@@ -377,10 +392,12 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     const size_t tile_elems = (size_t)rows * TLT;
     double* sY = tiles + (size_t)tpc * tile_elems;
     const size_t ybuf = (size_t)tpc * K * TLT;
-    double* sS = sY + 2 * ybuf;                        // stash: [tpc][2][M+1][32]
-    double* sGY = sS + (size_t)tpc * 2 * (M + 1) * 32; // rank d[0], d[m-1]: [2][tpc][2][TLT]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sGY + (size_t)2 * tpc * 2 * TLT);
-    double* stash = sS + ((size_t)(2 * tl + (has_first ? 0 : 1)) * (M + 1)) * 32 + wl;
+    double* sS = sY + 2 * ybuf;                        // stash: [tpc][NE][M+1][32]
+    double* sGY = sS + (size_t)tpc * NE * (M + 1) * 32; // rank d[0], d[m-1]: [2][tpc][2][TLT]
+    double* sPin = sGY + (size_t)2 * tpc * 2 * TLT;    // pins (32-line tiles): [tpc][2][TLT]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sPin + (CW == 1 ? (size_t)tpc * 2 * TLT : 0));
+    const int es = CW == 1 ? (has_first ? wt : EW + wt - (NW - EW)) : (has_first ? 0 : 1);
+    double* stash = sS + ((size_t)(NE * tl + es) * (M + 1)) * 32 + wl;
     const double* __restrict__ tb = p.tab + (size_t)r0 * NCOEF;
 
     auto issue = [&](long long item) {
@@ -443,9 +460,20 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                 ue = (ue - p.sc_last * next_first) / p.det_next;
             }
         }
-        // broadcast the pins of each line to every chunk of this warp
-        us = __shfl_sync(0xffffffffu, us, lane);
-        ue = __shfl_sync(0xffffffffu, ue, (C - 1 - wc0) * TLT + lane);
+        if (CW == 1) {
+            // 32-line tiles: the pins reach the other edge warp of each side
+            // through shared memory (named barrier of the edge warps)
+            double* PP = sPin + (size_t)tl * 2 * TLT;
+            if (first_chunk) PP[lane] = us;
+            if (last_chunk) PP[TLT + lane] = ue;
+            asm volatile("bar.sync 1, %0;" ::"r"(tpc * NE * 32) : "memory");
+            us = PP[lane];
+            ue = PP[TLT + lane];
+        } else {
+            // broadcast the pins of each line to every chunk of this warp
+            us = __shfl_sync(0xffffffffu, us, lane);
+            ue = __shfl_sync(0xffffffffu, ue, (C - 1 - wc0) * TLT + lane);
+        }
         const double2 h0 = __ldg(p.Hp + (size_t)chunk * K);
         const double2 hl = __ldg(p.Hp + (size_t)chunk * K + K - 1);
         double F = stash[0], L = stash[(M - 1) * 32];
@@ -550,15 +578,15 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
 
         // ROUND 2 posts of this item first (helper warp): the rank's d[0] /
         // d[m-1], on their way while the chunk boundary values are formed
-        if (!edge_warp && wt == 1 && role < 2 && valid) {
-            const double gy = gdot<TLT>(p, role, Y, K, lane);
-            if (role == 0 && A.mail_prev) {
+        if (gy_role >= 0 && valid) {
+            const double gy = gdot<TLT>(p, gy_role, Y, K, lane);
+            if (gy_role == 0 && A.mail_prev) {
                 post(A.mail_prev + par + mb.d_from_next() + line, gy);
             }
-            if (role == 1 && A.mail_next) {
+            if (gy_role == 1 && A.mail_next) {
                 post(A.mail_next + par + mb.d_from_prev() + line, gy);
             }
-            sGY[(((size_t)(it & 1) * tpc + tl) * 2 + role) * TLT + lane] = gy;
+            sGY[(((size_t)(it & 1) * tpc + tl) * 2 + gy_role) * TLT + lane] = gy;
         }
         // chunk boundary values without the rank pins
         double F, L;
@@ -606,8 +634,8 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                            (halo_hi_poster && A.mail_next ? 2u : 0u);
         unsigned b = 0;
         if (helpers) {
-            if (!edge_warp && wt == 1 && role == 0 && A.mail_prev) b = 1;
-            if (!edge_warp && wt == 1 && role == 1 && A.mail_next) b = 1;
+            if (gy_role == 0 && A.mail_prev) b = 1;
+            if (gy_role == 1 && A.mail_next) b = 1;
         } else {
             b = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
         }
@@ -656,7 +684,9 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
 }
 
 size_t dd2_smem(const FastArgs& a, TileCfg c, int M) {
-    return tma_smem(a, c) + (size_t)c.tpc * 2 * (M + 1) * 32 * 8 + (size_t)4 * c.tpc * c.tl * 8;
+    const int ne = c.tl == 32 ? 4 : 2;   // stash slots per tile (k_dd2 NE)
+    return tma_smem(a, c) + (size_t)c.tpc * ne * (M + 1) * 32 * 8 +
+           (size_t)4 * c.tpc * c.tl * 8 + (c.tl == 32 ? (size_t)2 * c.tpc * c.tl * 8 : 0);
 }
 
 template <int M, int UNI, int TLT, int SZC = 0>
@@ -704,6 +734,20 @@ int launch_dd_m(const DDArgs& A, cudaStream_t s) {
                        (cfg.tl == 8 ? A.t.f.dd_defer8 : A.t.f.dd_defer16);
     if (cfg.tl == 8)
         return defer ? launch_dd2_t<M, UNI, 8>(A, cfg, s) : launch_dd_t<M, UNI, 8>(A, cfg, s);
+    if constexpr (M == 32) {
+        // k_dd2 with 32-line tiles (one chunk per warp; two edge warps and
+        // four helper warps per tile, so >= 8 chunks: m >= 256) at two CTAs
+        // per SM. Same choice on every rank (plan and sz only). Knob
+        // TDS_DD2_TL32=0.
+        const int C = A.t.f.chunks;
+        if (defer && A.t.f.sz == 32 && C >= 8 && C * 32 <= 512 &&
+            !(getenv("TDS_DD2_TL32") && getenv("TDS_DD2_TL32")[0] == '0') &&
+            !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0')) {
+            const int per_tile = C * 32;
+            const TileCfg c32{32, per_tile >= 256 ? 1 : 256 / per_tile};
+            if (dd2_smem(A.t.f, c32, M) <= 113 * 1024) return launch_dd2_t<M, UNI, 32, 32>(A, c32, s);
+        }
+    }
     if constexpr (M == 32) {
         // k_dd with 32-line tiles (one chunk per warp) when no deferral
         // applies (m = 128: every chunk is an edge chunk). Same choice on

@@ -87,11 +87,16 @@ def test_fused_ranks_match_reference_golden(golden, tag, knobs, env):
         group.close()
 
 
+@pytest.mark.parametrize("knobs", [{}, {"TDS_DD2_TL32": "0"}],
+                         ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
 @pytest.mark.parametrize("p", [2, 4, 8])
 @pytest.mark.parametrize("periodic", [True, False])
-def test_fused_ranks_many_items_vs_oracle(p, periodic):
+def test_fused_ranks_many_items_vs_oracle(p, periodic, knobs, env):
     # 1024-row lines, m = 512 / 256 / 128 (the per-GPU blocks of BASELINE
-    # config 3), enough lines that every CTA runs several persistent items
+    # config 3), enough lines that every CTA runs several persistent items.
+    # Default at m >= 256: k_dd2 with 32-line tiles (two edge warps per
+    # side); TDS_DD2_TL32=0: its 16-line tiles
+    env(knobs)
     n, groups, sz = 1024, 40, 32
     lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, periodic)
     s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
@@ -359,7 +364,8 @@ def test_slab_transport_across_devices():
 
 
 @pytest.mark.parametrize("p,periodic,knobs", [(2, True, {}), (4, False, {"TDS_DEFER": "0"}),
-                                              (8, True, {"TDS_TL": "8"})])
+                                              (8, True, {"TDS_TL": "8"}), (2, False, {}),
+                                              (2, True, {"TDS_DD2_TL32": "0"})])
 def test_fused_protocol_stress_many_epochs(p, periodic, knobs, env):
     # compute-sanitizer is unavailable on the GPU pool: instead hammer the
     # fence-free mailbox protocol (both parity halves, every CTA posting
