@@ -269,6 +269,18 @@ int tds_fused_transport(const tds_plan* d1, const tds_plan* d2, const double* u_
                         double* mail, double* mail_prev, double* mail_next,
                         unsigned long long epoch, int max_ctas, void* stream);
 
+/* The same distributed term read IN PLACE from a rank's x-layout z-slab
+ * (nx, ny, m) -- the z lines of SlabTransport without re-layout passes --
+ * and ADDED into the x-layout accumulator acc by TMA reduce-add. Same plans,
+ * mailboxes (tds_transport_mailbox_words(nx ny / sz, sz) words) and epoch /
+ * max_ctas rules as tds_fused_transport; sz | ny. Replaces reorder(x->z) +
+ * directional_contribution + reorder/accumulate(z->x) of one term
+ * (momentum.py:129-169) on the rank chain. */
+int tds_fused_transport_in_x(const tds_plan* d1, const tds_plan* d2, const double* u_i,
+                             const double* u_j, double* acc, double nu, int nx, int ny, int m,
+                             int sz, double* mail, double* mail_prev, double* mail_next,
+                             unsigned long long epoch, int max_ctas, void* stream);
+
 /* acc += the (i, dir) contribution, dir = 1 (y) or 2 (z), for an
  * (nx, ny, nz) block with everything in the x layout (groups = ny nz/sz, nx,
  * sz): the y / z lines are read in place through 4-D tensor maps and the

@@ -861,6 +861,10 @@ struct TrDDArgs {
     unsigned long long epoch;
     unsigned long long timeout_ns;
     int max_ctas;
+    // in-place mode (XZ): the z lines of an x-layout (nx, ny, rows) slab,
+    // the term added into `out` (x layout) by TMA reduce-add
+    int nx, ny;
+    CUtensorMap omap;
 };
 
 namespace {
@@ -889,7 +893,7 @@ __device__ __forceinline__ double tr_subst(const UniformTable& T, int i, int M, 
 
 }  // namespace
 
-template <int TLT, int SZC>
+template <int TLT, int SZC, int XZ>
 __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__ TrDDArgs A) {
     constexpr int M = 16;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -922,6 +926,23 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
     const UniformTable& T1 = sT[0];
     const UniformTable& T2 = sT[1];
 
+    // XZ: tile = TLT lanes of y-group gj at x (lane blocks fastest), z rows
+    // at stride nx ny; a line's rows start at xz_base(line)
+    const int nlb = XZ ? A.sz / TLT : 1, ngj = XZ ? A.ny / A.sz : 1;
+    const long long rstride = XZ ? (long long)A.nx * A.ny : sz;
+    auto xz_tile = [&](long long tile, int& l0, int& x, int& gj) {
+        l0 = (int)(tile % nlb) * TLT;
+        gj = (int)((tile / nlb) % ngj);
+        x = (int)(tile / ((long long)nlb * ngj));
+    };
+    auto row0 = [&](long long ln) -> long long {
+        if (XZ) {
+            int l0, x, gj;
+            xz_tile(ln / TLT, l0, x, gj);
+            return ((long long)gj * A.nx + x) * sz + l0 + ln % TLT;
+        }
+        return line_base_t<SZC>(ln, rows, A.sz);
+    };
     auto issue = [&](long long item) {
         uint32_t bytes = 0;
         for (int j = 0; j < tpc; ++j)
@@ -931,6 +952,17 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
         for (int j = 0; j < tpc; ++j) {
             const long long first = (item * tpc + j) * TLT;
             if (first >= A.lines) break;
+            if (XZ) {
+                int l0, x, gj;
+                xz_tile(first / TLT, l0, x, gj);
+                for (int b = 0; b * A.boxr < rows; ++b) {
+                    tma_load_4d(ti + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_i, bar, l0,
+                                x, gj, b * A.boxr);
+                    tma_load_4d(tj + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_j, bar, l0,
+                                x, gj, b * A.boxr);
+                }
+                continue;
+            }
             const int g = (int)(first / A.sz), l0 = (int)(first % A.sz);
             for (int b = 0; b * A.boxr < rows; ++b) {
                 tma_load_3d(ti + j * tile_elems + (size_t)b * A.boxr * TLT, &A.map_i, bar, l0,
@@ -940,25 +972,38 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
             }
         }
     };
+    // XZ: add the staged term (tile i, load layout) into out by TMA
+    auto reduce_out = [&](long long item) {
+        for (int j = 0; j < tpc; ++j) {
+            const long long first = (item * tpc + j) * TLT;
+            if (first >= A.lines) break;
+            int l0, x, gj;
+            xz_tile(first / TLT, l0, x, gj);
+            for (int b = 0; b * A.boxr < rows; ++b)
+                tma_reduce_add_4d(&A.omap, ti + j * tile_elems + (size_t)b * A.boxr * TLT, l0, x,
+                                  gj, b * A.boxr);
+        }
+        bulk_commit();
+    };
     // ROUND 1 of `item`: first two rows of u_i, u_j -> prev, last two -> next
     auto publish_halo = [&](long long item) {
         if (!first_chunk && !last_chunk) return;
         const long long ln = (item * tpc + tl) * TLT + lane;
         if (ln >= A.lines) return;
-        const long long lb = line_base_t<SZC>(ln, rows, A.sz);
+        const long long lb = row0(ln);
         const double* bi = A.ui + lb;
         const double* bj = A.uj + lb;
         const long long hb = halo_base_t<SZC>(ln, A.sz);
         if (first_chunk && A.mail_prev) {
             double* m = A.mail_prev + par;
             post(m + mb.hhi_i() + hb, __ldg(bi));
-            post(m + mb.hhi_i() + hb + sz, __ldg(bi + sz));
+            post(m + mb.hhi_i() + hb + sz, __ldg(bi + rstride));
             post(m + mb.hhi_j() + hb, __ldg(bj));
-            post(m + mb.hhi_j() + hb + sz, __ldg(bj + sz));
+            post(m + mb.hhi_j() + hb + sz, __ldg(bj + rstride));
         }
         if (last_chunk && A.mail_next) {
             double* m = A.mail_next + par;
-            const long long a = (long long)(rows - 2) * sz, b = (long long)(rows - 1) * sz;
+            const long long a = (long long)(rows - 2) * rstride, b = (long long)(rows - 1) * rstride;
             post(m + mb.hlo_i() + hb, __ldg(bi + a));
             post(m + mb.hlo_i() + hb + sz, __ldg(bi + b));
             post(m + mb.hlo_j() + hb, __ldg(bj + a));
@@ -1132,13 +1177,32 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
         correct(0, A.f1, T1, -0.5, true);
         correct(1, A.f1, T1, -0.5, false);
         if (A.has_nu) correct(2, A.f2, T2, A.nu, false);
-        release(nxt);             // tiles consumed (u_j rows of the A correction)
-        if (valid) {
-            double* ob = A.out + line_base_t<SZC>(line, rows, A.sz) + (long long)r0 * sz;
+        if (XZ) {
+            // the term goes into tile i (its last reader was the sweeps,
+            // before the pin barrier) and is added into out by the TMA
+            // engine; the tiles are re-armed once it has read them
+            double* Tw = ti + tl * tile_elems;
 #pragma unroll
-            for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
+            for (int i = 0; i < M; ++i) Tw[base + (i + 2) * TLT] = acc[i];
+            fence_proxy_async();
+            __syncthreads();
+            if (t == 0) {
+                reduce_out(item);
+                if (nxt < A.items) {
+                    bulk_wait_read<0>();
+                    issue(nxt);
+                }
+            }
+        } else {
+            release(nxt);         // tiles consumed (u_j rows of the A correction)
+            if (valid) {
+                double* ob = A.out + line_base_t<SZC>(line, rows, A.sz) + (long long)r0 * sz;
+#pragma unroll
+                for (int i = 0; i < M; ++i) __stcs(ob + (long long)i * sz, acc[i]);
+            }
         }
     }
+    if (XZ && t == 0) bulk_wait_all();   // the last reduces complete before exit
     {
         const unsigned n = valid_items(A.items, A.lines, tpc, tl, TLT, lane);
         const unsigned per = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
@@ -1149,7 +1213,7 @@ __global__ void __launch_bounds__(512, 1) k_dd_transport(const __grid_constant__
 
 namespace {
 
-template <int TLT, int SZC>
+template <int TLT, int SZC, int XZ = 0>
 int launch_dd_transport_t(const TrDDArgs& A0, cudaStream_t s) {
     TrDDArgs A = A0;
     const int per_tile = A.chunks * TLT;
@@ -1163,21 +1227,27 @@ int launch_dd_transport_t(const TrDDArgs& A0, cudaStream_t s) {
     fi.rows = fj.rows = A.rows;
     fi.sz = fj.sz = A.sz;
     fi.lines = fj.lines = A.lines;
-    int rc = encode_field_map(fi, 16, TLT, &A.map_i, &A.boxr);
-    if (rc) return rc;
-    rc = encode_field_map(fj, 16, TLT, &A.map_j, &A.boxr);
-    if (rc) return rc;
+    int rc;
+    if (XZ) {
+        if ((rc = encode_xz_map(A.ui, A.nx, A.ny, A.rows, A.sz, 16, TLT, &A.map_i, &A.boxr)) ||
+            (rc = encode_xz_map(A.uj, A.nx, A.ny, A.rows, A.sz, 16, TLT, &A.map_j, &A.boxr)) ||
+            (rc = encode_xz_map(A.out, A.nx, A.ny, A.rows, A.sz, 16, TLT, &A.omap, &A.boxr)))
+            return rc;
+    } else {
+        if ((rc = encode_field_map(fi, 16, TLT, &A.map_i, &A.boxr))) return rc;
+        if ((rc = encode_field_map(fj, 16, TLT, &A.map_j, &A.boxr))) return rc;
+    }
     const int threads = A.tpc * per_tile;
     const size_t smem = (size_t)A.tpc *
                             (2 * (size_t)A.rows * TLT + 3 * (size_t)2 * A.chunks * TLT +
                              3 * 2 * TLT) * sizeof(double) +
                         2 * sizeof(UniformTable) + 16;
-    const void* fn = reinterpret_cast<const void*>(k_dd_transport<TLT, SZC>);
+    const void* fn = reinterpret_cast<const void*>(k_dd_transport<TLT, SZC, XZ>);
     if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd_transport)"))) return rc;
     // co-resident, identical on every rank (max_ctas: ranks sharing a device)
     const long long grid = persistent_grid(fn, threads, smem, A.items, A.max_ctas);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport does not fit on an SM");
-    k_dd_transport<TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_dd_transport<TLT, SZC, XZ><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_dd_transport launch");
 }
 
@@ -1189,9 +1259,11 @@ long long dd_transport_err_word(long long lines) { return TrMail{lines}.err(); }
 int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui,
                         const double* uj, double* out, double nu, long long lines, int sz,
                         double* mail, double* mail_prev, double* mail_next,
-                        unsigned long long epoch, int max_ctas, cudaStream_t s) {
+                        unsigned long long epoch, int max_ctas, cudaStream_t s, int nx, int ny) {
     TrDDArgs A;
     std::memset(&A, 0, sizeof(A));
+    A.nx = nx;
+    A.ny = ny;
     A.max_ctas = max_ctas;
     A.f1 = f1;
     A.f2 = f2;
@@ -1215,6 +1287,15 @@ int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui
         A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
     int tl = 16;
     if (const char* e = getenv("TDS_TRANSPORT_TL")) tl = atoi(e) == 8 ? 8 : 16;
+    if (nx > 0) {
+        // in place from the x layout (the z lines of a slab), added into out
+        if (ny % sz || reinterpret_cast<uintptr_t>(out) % 16)
+            return set_err(TDS_ERR_UNSUPPORTED, "in-place distributed transport: sz | ny");
+        if (tl == 16 && sz % 16 == 0 && A.chunks * 16 <= 512)
+            return launch_dd_transport_t<16, 0, 1>(A, s);
+        if (sz % 8 == 0 && A.chunks * 8 <= 512) return launch_dd_transport_t<8, 0, 1>(A, s);
+        return set_err(TDS_ERR_UNSUPPORTED, "in-place distributed transport: tile");
+    }
     if (tl == 16 && sz % 16 == 0 && A.chunks * 16 <= 512) {
         if (sz == 32) return launch_dd_transport_t<16, 32>(A, s);
         return launch_dd_transport_t<16, 0>(A, s);

@@ -39,6 +39,11 @@ int ensure_smem(const void* fn, size_t smem, const char* what);
 long long persistent_grid(const void* fn, int threads, size_t smem, long long items,
                           int max_ctas);
 
+// 4-D view (lane, x, y-group, z) of an x-layout (nx, ny, nz) block, box tl
+// lanes x 1 x 1 x boxr z-rows: the z lines read in place (tds_transport.cu)
+int encode_xz_map(const double* u, int nx, int ny, int nz, int sz, int M, int tl,
+                  CUtensorMap* map, int* boxr);
+
 // long lines split over a thread-block cluster (tds_cluster.cu)
 bool tmc_eligible(int M, bool uniform, const FastArgs& a);
 int launch_tmc(int M, bool uniform, const FastArgs& a, cudaStream_t s);

@@ -504,8 +504,6 @@ __global__ void __launch_bounds__(512, 1) k_transport_tma(const __grid_constant_
     }
 }
 
-namespace {
-
 // 4-D view of an x-layout (nx, ny, nz) block (G = ny nz/sz, nx, sz):
 // (lane, x, y-group, z) with group = y-group + z * ny/sz; box TLT lanes x
 // 1 x 1 x boxr z-rows.
@@ -524,6 +522,8 @@ int encode_xz_map(const double* u, int nx, int ny, int nz, int sz, int M, int tl
     if (cr != CUDA_SUCCESS) return set_err(TDS_ERR_CUDA, "cuTensorMapEncodeTiled (xz) failed");
     return TDS_OK;
 }
+
+namespace {
 
 // The same 4-D view, box 16 lanes x TLT x-positions x all y-groups x 1 z,
 // 128-byte swizzle (GEOM_XY tiles).

@@ -469,6 +469,41 @@ class SlabTransport:
         self.ctx.exchange_rounds += 6
         return True
 
+    def _z_in_x(self, vel, acc):
+        """The three z terms read in place from the slab's x layout and added
+        into acc (tds_fused_transport_in_x: k_dd_transport on the slab's z
+        lines, TMA reduce-add) -- no re-layout passes. False when the plans /
+        shape do not allow it (the same decision on every rank: plans and
+        shape only). A/B knob: TDS_TRANSPORT_Z=0."""
+        import os
+        if not self._zfused or os.environ.get("TDS_TRANSPORT_Z") == "0":
+            return False
+        if self._zbroken is not None:
+            raise TimeoutError(str(self._zbroken))
+        p1, p2 = self._zfused
+        n, sz, m = self.n, self.sz, self.m
+        groups = n * n // sz
+        key = (groups, sz)
+        mb = self._zmail.get(key)
+        if mb is None:
+            mb = self.ctx.open_mailboxes(N.lib().tds_transport_mailbox_words(groups, sz))
+            self._zmail[key] = mb
+        self._poll_z()
+        stream = _torch().cuda.current_stream()
+        for i in range(3):
+            self._zepoch += 1
+            rc = N.lib().tds_fused_transport_in_x(
+                p1.handle, None if p2 is None else p2.handle, _vp(vel[i]), _vp(vel[2]),
+                _vp(acc[i]), self.nu, n, n, m, sz, mb.own, mb.prev, mb.next, self._zepoch,
+                self.ctx.fused_grid_cap, ctypes.c_void_p(stream.cuda_stream))
+            if rc == N.TDS_ERR_UNSUPPORTED and i == 0:
+                self._zepoch -= 1
+                return False
+            N.check(rc)
+            self.ctx.exchange_rounds += 6
+        mb.post_status(stream)
+        return True
+
     def _poll_z(self, block=False):
         """Fold the fused z kernels' status words into the context (posted
         halo words of u_i and u_j: 4 L per directed edge per term, boundary
@@ -524,8 +559,18 @@ class SlabTransport:
                 self._reorder(scratch, "y", "x", out=acc[i], accumulate=True)
         if marks is not None:
             marks[2].record()
-        if not (self._rank is None and ydir and
-                _direction_pass(vel, acc, ext, self.sz, self.h, self.nu, 2)):
+        if self._rank is None:   # one rank: keep evaluate_transport_rhs's order
+            zdone = ydir and _direction_pass(vel, acc, ext, self.sz, self.h, self.nu, 2)
+        else:
+            if self.ctx.fused_grid_cap < 0:
+                # ranks sharing a device: a rank's fused z kernel waiting for
+                # a neighbour must not hold SMs that the neighbour's
+                # persistent x / y kernels still need -- all ranks finish the
+                # local passes first
+                torch.cuda.current_stream().synchronize()
+                self.ctx.barrier()
+            zdone = self._z_in_x(vel, acc)
+        if not zdone:
             rot = [self._reorder(c, "x", "z") for c in vel]
             scratch = torch.empty_like(rot[0])
             for i in range(3):
