@@ -281,6 +281,19 @@ int tds_fused_transport_in_x(const tds_plan* d1, const tds_plan* d2, const doubl
                              int sz, double* mail, double* mail_prev, double* mail_next,
                              unsigned long long epoch, int max_ctas, void* stream);
 
+/* All three z contributions of a rank's x-layout z-slab (nx, ny, m) in ONE
+ * kernel per rank (k_dd_transport_dir): u0..u2 read once in place, the nine
+ * DistD2 solves with their neighbour rounds over the mailboxes, each
+ * component's term added into acc_i by TMA reduce-add. The distributed
+ * counterpart of tds_transport_direction (dir = 2); plans, mailboxes
+ * (tds_transport_mailbox_words(nx ny / sz, sz) words, shared with the
+ * per-term kernels) and epoch / max_ctas rules as tds_fused_transport. */
+int tds_fused_transport_direction(const tds_plan* d1, const tds_plan* d2, const double* u0,
+                                  const double* u1, const double* u2, double* acc0, double* acc1,
+                                  double* acc2, double nu, int nx, int ny, int m, int sz,
+                                  double* mail, double* mail_prev, double* mail_next,
+                                  unsigned long long epoch, int max_ctas, void* stream);
+
 /* acc += the (i, dir) contribution, dir = 1 (y) or 2 (z), for an
  * (nx, ny, nz) block with everything in the x layout (groups = ny nz/sz, nx,
  * sz): the y / z lines are read in place through 4-D tensor maps and the

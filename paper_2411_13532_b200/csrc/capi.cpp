@@ -400,6 +400,10 @@ int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui
                         double* mail, double* mail_prev, double* mail_next,
                         unsigned long long epoch, int max_ctas, cudaStream_t s, int nx = 0,
                         int ny = 0);
+int launch_dd_transport_dir(const FastArgs& f1, const FastArgs& f2, const double* const* u,
+                            double* const* out, double nu, int nx, int ny, int m, int sz,
+                            double* mail, double* mail_prev, double* mail_next,
+                            unsigned long long epoch, int max_ctas, cudaStream_t s);
 }  // namespace tds
 
 extern "C" long long tds_transport_mailbox_words(long long groups, int sz) {
@@ -470,6 +474,40 @@ extern "C" int tds_fused_transport_in_x(const tds_plan* d1, const tds_plan* d2,
                                     d1->has_prev ? mail_prev : nullptr,
                                     d1->has_next ? mail_next : nullptr, epoch, max_ctas,
                                     S(stream), nx, ny);
+}
+
+extern "C" int tds_fused_transport_direction(const tds_plan* d1, const tds_plan* d2,
+                                             const double* u0, const double* u1,
+                                             const double* u2, double* acc0, double* acc1,
+                                             double* acc2, double nu, int nx, int ny, int m,
+                                             int sz, double* mail, double* mail_prev,
+                                             double* mail_next, unsigned long long epoch,
+                                             int max_ctas, void* stream) {
+    if (!d1 || !u0 || !u1 || !u2 || !acc0 || !acc1 || !acc2 || !mail)
+        return set_err(TDS_ERR_INVALID, "null argument");
+    if (nx < 1 || ny < 1 || sz < 1 || ny % sz || m != d1->block_rows)
+        return set_err(TDS_ERR_INVALID, "bad slab extents (sz | ny, m = the plan's block rows)");
+    auto ok = [&](const tds_plan* p) {
+        return p->rank >= 0 && p->P >= 2 && p->path == TDS_PATH_FAST && p->M == 16 &&
+               p->C >= 2 && p->uniform && !p->special_first && !p->special_last;
+    };
+    if (!ok(d1) || (nu != 0.0 && (!d2 || !ok(d2) || d2->C != d1->C || d2->rank != d1->rank ||
+                                  d2->block_rows != d1->block_rows)))
+        return set_err(TDS_ERR_UNSUPPORTED,
+                       "fused distributed transport needs uniform per-rank 16-row-chunk plans");
+    if ((d1->has_prev && !mail_prev) || (d1->has_next && !mail_next))
+        return set_err(TDS_ERR_INVALID, "missing mailbox");
+    if (tds::box_rows(m, 16) == 0 || !tds::encode_fn())
+        return set_err(TDS_ERR_UNSUPPORTED, "fused distributed transport: not TMA-eligible");
+    const long long lines = (long long)nx * ny;
+    tds::FastArgs f1 = fast_args(d1, lines, sz);
+    tds::FastArgs f2 = nu != 0.0 ? fast_args(d2, lines, sz) : f1;
+    const double* u[3] = {u0, u1, u2};
+    double* acc[3] = {acc0, acc1, acc2};
+    return tds::launch_dd_transport_dir(f1, f2, u, acc, nu, nx, ny, m, sz, mail,
+                                        d1->has_prev ? mail_prev : nullptr,
+                                        d1->has_next ? mail_next : nullptr, epoch, max_ctas,
+                                        S(stream));
 }
 
 extern "C" int tds_ipc_alloc(long long bytes, void** ptr, unsigned char* handle) {

@@ -820,17 +820,19 @@ int launch_dd(int M, bool uniform, const FastArgs& a, double* mail, double* mail
 // rank_count ranks) is three DistD2 solves + products; here the HBM traffic
 // is u_i, u_j read once and the term written once (24 B/point).
 //
-// Mailbox (TrMail, 8-byte sentinel slots, two parity halves of 14 L):
+// Mailbox (TrMail, 8-byte sentinel slots, two parity halves, 14 L used of 30):
 //   DP(s) [L], s = 0..2   prev's d[m-1] of solve s
 //   DN(s) [L]             next's d[0] of solve s
 //   HLO_I, HLO_J [2L]     prev's last two rows of u_i, u_j
 //   HHI_I, HHI_J [2L]     next's first two rows of u_i, u_j
 // Deadlock freedom as k_dd: identical persistent schedule on every rank,
 // posts before waits, waits only on the same CTA index of a neighbour.
+// (The halves are 30 L apart and the status words sit at 60 L: the layout
+// shared with k_dd_transport_dir, TdMail, so one mailbox serves both.)
 struct TrMail {
     long long L;
     __host__ __device__ long long half(unsigned long long epoch) const {
-        return (long long)(epoch & 1ULL) * 14 * L;
+        return (long long)(epoch & 1ULL) * 30 * L;
     }
     __host__ __device__ long long dp(int s) const { return s * L; }
     __host__ __device__ long long dn(int s) const { return (3 + s) * L; }
@@ -838,8 +840,8 @@ struct TrMail {
     __host__ __device__ long long hlo_j() const { return 8 * L; }
     __host__ __device__ long long hhi_i() const { return 10 * L; }
     __host__ __device__ long long hhi_j() const { return 12 * L; }
-    __host__ __device__ long long err() const { return 28 * L; }
-    __host__ __device__ long long words() const { return 28 * L + 3; }   // + status words
+    __host__ __device__ long long err() const { return 60 * L; }
+    __host__ __device__ long long words() const { return 60 * L + 3; }   // + status words
 };
 
 struct TrDDArgs {
@@ -1305,6 +1307,454 @@ int launch_dd_transport(const FastArgs& f1, const FastArgs& f2, const double* ui
         return launch_dd_transport_t<8, 0>(A, s);
     }
     return set_err(TDS_ERR_UNSUPPORTED, "fused distributed transport: sz % 8, tile <= 512 threads");
+}
+
+
+// ===========================================================================
+// k_dd_transport_dir: the three z contributions (components i = 0, 1, 2) of
+// a rank's z-slab in ONE kernel per rank -- k_transport_dir's schedule with
+// k_dd_transport's neighbour rounds. The slab stays in the x layout: u_0..u_2
+// tiles (TLT lanes x m z-rows) arrive by TMA through 4-D tensor maps, each
+// on its own mbarrier, into tiles with two spare rows at each end that the
+// rank-edge threads fill from the neighbours' halo posts; every phase's
+// result is staged in its freed tile and added into the accumulator by TMA
+// reduce-add. HBM: u_0..u_2 read once, three accumulators read-modify-
+// written in L2: 72 B/pt, against 96 for three k_dd_transport launches and
+// 192 for the reorder pipeline.
+//
+// Per item: ROUND 1 posts the first / last two rows of u_0..u_2 one item
+// ahead. Per component phase (order a, b, j as k_transport_dir): pass 1
+// (d/dx and d2/dx2 of u_c, one window read), pass 2 (d/dx of u_j u_c); after
+// each pass's barrier the rank-edge threads post that pass's g0.Y / g1.Y
+// (ROUND 2) and every chunk forms its pin-free (F, L). At the end of the
+// phase the edge threads take the neighbours' three rows (posted a pass or
+// more earlier), form the 2x2 pins, and every chunk applies the affine pin
+// correction before staging. Deadlock freedom as k_dd: identical persistent
+// schedules, posts before waits, waits only on the same CTA index of a
+// neighbour in the same or an earlier iteration.
+//
+// Mailbox (TdMail, sentinel slots, two parity halves of 30 L; the layout of
+// TrMail's status words):
+//   DP(s), DN(s) [L] s = 3 c + k (k: 0 d/dx, 1 d2/dx2, 2 d/dx of u_j u_c)
+//   HLO(c), HHI(c) [2L]   prev's last / next's first two rows of u_c
+struct TdMail {
+    long long L;
+    __host__ __device__ long long half(unsigned long long epoch) const {
+        return (long long)(epoch & 1ULL) * 30 * L;
+    }
+    __host__ __device__ long long dp(int s) const { return s * L; }
+    __host__ __device__ long long dn(int s) const { return (9 + s) * L; }
+    __host__ __device__ long long hlo(int c) const { return (18 + 2 * c) * L; }
+    __host__ __device__ long long hhi(int c) const { return (24 + 2 * c) * L; }
+    __host__ __device__ long long err() const { return 60 * L; }
+    __host__ __device__ long long words() const { return 60 * L + 3; }
+};
+
+struct TdArgs {
+    FastArgs f1, f2;           // rank plans: d/dx (f1), d2/dx2 (f2)
+    CUtensorMap map[3], omap[3];
+    const double* u[3];
+    double* out[3];
+    int boxr;
+    double nu;
+    int has_nu;
+    long long lines;
+    int rows, sz, chunks, tpc, nx, ny;
+    long long items;
+    double* mail;
+    double* mail_prev;
+    double* mail_next;
+    unsigned long long epoch;
+    unsigned long long timeout_ns;
+    int max_ctas;
+};
+
+template <int TLT>
+__global__ void __launch_bounds__(512, 1) k_dd_transport_dir(const __grid_constant__ TdArgs A) {
+    constexpr int M = 16;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int C = A.chunks, K = 2 * C, rows = A.rows, tpc = A.tpc;
+    const int t = threadIdx.x;
+    const int lane = t % TLT;
+    const int chunk = (t / TLT) % C;
+    const int tl = t / (TLT * C);
+    const long long sz = A.sz;
+    const int r0 = chunk * M;
+    const TdMail mb{A.lines};
+    const long long par = mb.half(A.epoch);
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(A.mail + mb.err());
+    const bool first_chunk = chunk == 0, last_chunk = chunk == C - 1;
+    // tiles with two spare rows at each end: [3][tpc][rows + 4][TLT]
+    const size_t tile_elems = (size_t)(rows + 4) * TLT;
+    const size_t field_elems = (size_t)tpc * tile_elems;
+    double* tiles = reinterpret_cast<double*>(smem);
+    double* sY = tiles + 3 * field_elems;                        // [3][tpc][K][TLT]
+    const size_t ybuf = (size_t)tpc * K * TLT;
+    double* sP = sY + 3 * ybuf;                                  // [3][tpc][2][TLT]
+    DirRow* sR = reinterpret_cast<DirRow*>(sP + (size_t)3 * tpc * 2 * TLT);
+    double* sst = reinterpret_cast<double*>(sR + M);             // stencils [2][5] (+ pad)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sst + 12);
+    const FastArgs& p1 = A.f1;
+    const FastArgs& p2 = A.f2;
+    for (int i = t; i < M; i += blockDim.x) {
+        DirRow r;
+        r.rf1 = make_double2(p1.ut.r[i], p1.ut.f[i]);
+        r.rf2 = make_double2(p2.ut.r[i], p2.ut.f[i]);
+        r.w12 = make_double2(p1.ut.w[i], p2.ut.w[i]);
+        r.s1 = make_double2(p1.ut.sa[i], p1.ut.sc[i]);
+        r.s2 = make_double2(p2.ut.sa[i], p2.ut.sc[i]);
+        sR[i] = r;
+    }
+    if (t < 10) sst[t] = t < 5 ? p1.ut.st[t] : p2.ut.st[t - 5];
+    const DirRow (&RT)[16] = *reinterpret_cast<const DirRow(*)[16]>(sR);
+    const double* st1 = sst;
+    const double* st2 = sst + 5;
+    const int jd = 2;                              // the slab's split direction: z
+    const int ca = 0, cb = 1;
+    const int nlb = A.sz / TLT, ngj = A.ny / A.sz;
+    const long long rs = (long long)A.nx * A.ny;   // z-row stride
+    auto xz_tile = [&](long long tile, int& l0, int& x, int& gj) {
+        l0 = (int)(tile % nlb) * TLT;
+        gj = (int)((tile / nlb) % ngj);
+        x = (int)(tile / ((long long)nlb * ngj));
+    };
+    auto row0 = [&](long long ln) -> long long {
+        int l0, x, gj;
+        xz_tile(ln / TLT, l0, x, gj);
+        return ((long long)gj * A.nx + x) * sz + l0 + ln % TLT;
+    };
+    auto issue = [&](int c, long long item) {
+        uint32_t bytes = 0;
+        for (int q = 0; q < tpc; ++q)
+            if ((item * tpc + q) * TLT < A.lines) bytes += (uint32_t)((size_t)rows * TLT * 8);
+        mbar_expect_tx(bar + c, bytes);
+        for (int q = 0; q < tpc; ++q) {
+            const long long first = (item * tpc + q) * TLT;
+            if (first >= A.lines) break;
+            int l0, x, gj;
+            xz_tile(first / TLT, l0, x, gj);
+            double* dst = tiles + c * field_elems + q * tile_elems + 2 * TLT;
+            for (int b = 0; b * A.boxr < rows; ++b)
+                tma_load_4d(dst + (size_t)b * A.boxr * TLT, &A.map[c], bar + c, l0, x, gj,
+                            b * A.boxr);
+        }
+    };
+    auto reduce_out = [&](int c, long long item) {
+        for (int q = 0; q < tpc; ++q) {
+            const long long first = (item * tpc + q) * TLT;
+            if (first >= A.lines) break;
+            int l0, x, gj;
+            xz_tile(first / TLT, l0, x, gj);
+            const double* src = tiles + c * field_elems + q * tile_elems + 2 * TLT;
+            for (int b = 0; b * A.boxr < rows; ++b)
+                tma_reduce_add_4d(&A.omap[c], src + (size_t)b * A.boxr * TLT, l0, x, gj,
+                                  b * A.boxr);
+        }
+        bulk_commit();
+    };
+    // ROUND 1 of `item`: first two rows of u_0..u_2 -> prev, last two -> next
+    auto publish_halo = [&](long long item) {
+        if (!first_chunk && !last_chunk) return;
+        const long long ln = (item * tpc + tl) * TLT + lane;
+        if (ln >= A.lines) return;
+        const long long o = row0(ln);
+        const long long hb = halo_base(ln, A.sz);
+        for (int c = 0; c < 3; ++c) {
+            const double* b = A.u[c] + o;
+            if (first_chunk && A.mail_prev) {
+                double* m = A.mail_prev + par + mb.hhi(c) + hb;
+                post(m, __ldg(b));
+                post(m + sz, __ldg(b + rs));
+            }
+            if (last_chunk && A.mail_next) {
+                double* m = A.mail_next + par + mb.hlo(c) + hb;
+                post(m, __ldg(b + (long long)(rows - 2) * rs));
+                post(m + sz, __ldg(b + (long long)(rows - 1) * rs));
+            }
+        }
+    };
+
+    if (t == 0) {
+        for (int c = 0; c < 3; ++c) mbar_init(bar + c, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    long long item = blockIdx.x;
+    if (item < A.items) {
+        if (t == 0) {
+            issue(ca, item);
+            issue(jd, item);
+            issue(cb, item);
+        }
+        publish_halo(item);
+    }
+    uint32_t phases = 0;
+    int pend = -1;
+    auto wait_tile = [&](int c) {
+        const uint32_t ph = (phases >> c) & 1u;
+        while (!mbar_try_wait(bar + c, ph)) {
+        }
+        phases ^= 1u << c;
+    };
+    // window row i of the chunk (block row r0 - 2 + i) in an extended tile
+    const int wbase = r0 * TLT + lane;
+    double* Y0 = sY + (size_t)tl * K * TLT;
+    double* YA = Y0;
+    double* YB = Y0 + ybuf;
+    double* YC = Y0 + 2 * ybuf;
+    double* P = sP + (size_t)tl * 2 * TLT;        // + k * tpc * 2 * TLT: solve k of the phase
+    const size_t pstride = (size_t)tpc * 2 * TLT;
+    const int bq1 = __ldg(p1.bq0 + chunk), bq2 = __ldg(p2.bq0 + chunk);
+
+    for (; item < A.items; item += gridDim.x) {
+        const long long line = (item * tpc + tl) * TLT + lane;
+        const bool valid = line < A.lines;
+        const long long nxt = item + gridDim.x;
+        if (nxt < A.items) publish_halo(nxt);                 // one item ahead
+        const bool hlo = valid && first_chunk && A.mail_prev;
+        const bool hhi = valid && last_chunk && A.mail_next;
+        const long long hb = valid ? halo_base(line, A.sz) : 0;
+        // rank-edge halos of this item -> the spare rows of the three tiles
+        // (only this thread reads them back: no barrier)
+        if (hlo || hhi) {
+            unsigned long long v[6];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double* hs = A.mail + par + (hlo ? mb.hlo(c) : mb.hhi(c)) + hb;
+                v[2 * c] = ld_sys_u64(hs);
+                v[2 * c + 1] = ld_sys_u64(hs + sz);
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double* hs = A.mail + par + (hlo ? mb.hlo(c) : mb.hhi(c)) + hb;
+                const double a0 = take_v(hs, v[2 * c], A, err);
+                const double a1 = take_v(hs + sz, v[2 * c + 1], A, err);
+                double* T = tiles + c * field_elems + tl * tile_elems;
+                const int o = hlo ? lane : (rows + 2) * TLT + lane;
+                T[o] = a0;
+                T[o + TLT] = a1;
+            }
+        }
+        const double* Tj = tiles + jd * field_elems + tl * tile_elems;
+#pragma unroll 1
+        for (int s = 0; s < 3; ++s) {
+            const int c = s == 0 ? ca : (s == 1 ? cb : jd);
+            double* Tc = tiles + c * field_elems + tl * tile_elems;
+            if (c != jd) wait_tile(c);
+            double acc[M], d[M];
+            double F, L, F2, L2;
+            // ROUND 2 of solve k after its barrier: own boundary rows (g.Y)
+            // to the neighbours, kept in P for the pair solve
+            auto round2 = [&](int k, const FastArgs& p, const double* Y) {
+                if (!valid || (!first_chunk && !last_chunk)) return;
+                const int sid = 3 * c + k;
+                double* Pk = P + k * pstride;
+                if (first_chunk) {
+                    const double g0y = gdot<TLT>(p, 0, Y, K, lane);
+                    if (A.mail_prev) post(A.mail_prev + par + mb.dn(sid) + line, g0y);
+                    Pk[lane] = g0y;
+                }
+                if (last_chunk) {
+                    const double g1y = gdot<TLT>(p, 1, Y, K, lane);
+                    if (A.mail_next) post(A.mail_next + par + mb.dp(sid) + line, g1y);
+                    Pk[TLT + lane] = g1y;
+                }
+            };
+
+            // pass 1: d(u_c) and d2(u_c) from one read of the window
+            if (A.has_nu) {
+                double d2[M];
+                dsweeps2<M>(RT, st1, st2, [&](int i) { return Tc[wbase + i * TLT]; }, d, d2);
+                YA[(2 * chunk) * TLT + lane] = d[0];
+                YA[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+                YC[(2 * chunk) * TLT + lane] = d2[0];
+                YC[(2 * chunk + 1) * TLT + lane] = d2[M - 1];
+                __syncthreads();
+                if (t == 0 && pend >= 0) {
+                    bulk_wait_read<0>();
+                    issue(pend, nxt);
+                    pend = -1;
+                }
+                if (s == 0) wait_tile(jd);
+                round2(0, p1, YA);
+                round2(1, p2, YC);
+                band_bounds_nopins<TLT>(p1.Hb + (size_t)chunk * p1.nb, bq1, p1.nb, YA, K, lane, F,
+                                        L);
+                band_bounds_nopins<TLT>(p2.Hb + (size_t)chunk * p2.nb, bq2, p2.nb, YC, K, lane, F2,
+                                        L2);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const DirRow& R = RT[i];
+                    acc[i] = fma(-0.5 * Tj[wbase + (i + 2) * TLT], subst2(R.s1, i, M, F, L, d[i]),
+                                 A.nu * subst2(R.s2, i, M, F2, L2, d2[i]));
+                }
+            } else {
+                dsweeps1<M>(RT, st1, [&](int i) { return Tc[wbase + i * TLT]; }, d);
+                YA[(2 * chunk) * TLT + lane] = d[0];
+                YA[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+                __syncthreads();
+                if (t == 0 && pend >= 0) {
+                    bulk_wait_read<0>();
+                    issue(pend, nxt);
+                    pend = -1;
+                }
+                if (s == 0) wait_tile(jd);
+                round2(0, p1, YA);
+                band_bounds_nopins<TLT>(p1.Hb + (size_t)chunk * p1.nb, bq1, p1.nb, YA, K, lane, F,
+                                        L);
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+                    acc[i] = -0.5 * Tj[wbase + (i + 2) * TLT] * subst2(RT[i].s1, i, M, F, L, d[i]);
+            }
+            // pass 2: d(u_j u_c)
+            dsweeps1<M>(RT, st1,
+                        [&](int i) { return Tj[wbase + i * TLT] * Tc[wbase + i * TLT]; }, d);
+            YB[(2 * chunk) * TLT + lane] = d[0];
+            YB[(2 * chunk + 1) * TLT + lane] = d[M - 1];
+            __syncthreads();
+            round2(2, p1, YB);
+            band_bounds_nopins<TLT>(p1.Hb + (size_t)chunk * p1.nb, bq1, p1.nb, YB, K, lane, F, L);
+#pragma unroll
+            for (int i = 0; i < M; ++i) acc[i] = fma(-0.5, subst2(RT[i].s1, i, M, F, L, d[i]), acc[i]);
+
+            // the neighbours' rows of the phase's solves -> 2x2 pairs -> pins
+            if (valid && ((first_chunk && p1.has_prev) || (last_chunk && p1.has_next))) {
+                const int nk = A.has_nu ? 3 : 2;
+                unsigned long long v[3] = {SENTINEL, SENTINEL, SENTINEL};
+                double* slot[3];
+                for (int k = 0; k < 3; ++k) {
+                    const int kk = k == 1 ? 2 : (k == 2 ? 1 : 0);   // A, B, C
+                    const int sid = 3 * c + kk;
+                    slot[k] = A.mail + par + (first_chunk ? mb.dp(sid) : mb.dn(sid)) + line;
+                    if (k < nk) v[k] = ld_sys_u64(slot[k]);
+                }
+                for (int k = 0; k < nk; ++k) {
+                    const int kk = k == 1 ? 2 : (k == 2 ? 1 : 0);
+                    const FastArgs& p = kk == 1 ? p2 : p1;
+                    double* Pk = P + kk * pstride;
+                    const double nb_row = take_v(slot[k], v[k], A, err);
+                    if (first_chunk) Pk[lane] = (Pk[lane] - p.sa_first * nb_row) / p.det_prev;
+                    else Pk[TLT + lane] = (Pk[TLT + lane] - p.sc_last * nb_row) / p.det_next;
+                }
+            }
+            __syncthreads();
+            // affine pin corrections: x += dx(dF, dL), dF = h0.x us + hl.x ue
+            auto correct = [&](int k, const FastArgs& p, double w, bool by_uj, bool second) {
+                const double* Pk = P + k * pstride;
+                const double2 h0 = __ldg(p.Hp + (size_t)chunk * K);
+                const double2 hl = __ldg(p.Hp + (size_t)chunk * K + K - 1);
+                const double us = Pk[lane], ue = Pk[TLT + lane];
+                const double dF = fma(h0.x, us, hl.x * ue), dL = fma(h0.y, us, hl.y * ue);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const double2 sc = second ? RT[i].s2 : RT[i].s1;
+                    double dx = i == 0 ? dF : (i == M - 1 ? dL : -fma(sc.y, dL, sc.x * dF));
+                    if (by_uj) dx *= Tj[wbase + (i + 2) * TLT];
+                    acc[i] = fma(w, dx, acc[i]);
+                }
+            };
+            correct(0, p1, -0.5, true, false);
+            correct(2, p1, -0.5, false, false);
+            if (A.has_nu) correct(1, p2, A.nu, false, true);
+            // stage in tile c (every read of it is done: own rows only) and
+            // add into out[c] with the TMA engine
+#pragma unroll
+            for (int i = 0; i < M; ++i) Tc[wbase + (i + 2) * TLT] = acc[i];
+            fence_proxy_async();
+            __syncthreads();
+            if (t == 0) {
+                reduce_out(c, item);
+                if (nxt < A.items) {
+                    if (s == 2) {
+                        bulk_wait_read<0>();
+                        issue(c, nxt);
+                    } else {
+                        pend = c;
+                    }
+                }
+            }
+        }
+    }
+    if (t == 0) bulk_wait_all();
+    {
+        const unsigned n = valid_items(A.items, A.lines, tpc, tl, TLT, lane);
+        const unsigned per = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
+        // halos: 2 rows of 3 fields; boundary rows: one per solve (9 or 6)
+        flush_counts(err, 6 * per * n, (A.has_nu ? 9u : 6u) * per * n);
+    }
+}
+
+namespace {
+
+template <int TLT>
+int launch_dd_transport_dir_t(const TdArgs& A0, cudaStream_t s) {
+    TdArgs A = A0;
+    const int per_tile = A.chunks * TLT;
+    A.tpc = per_tile >= 256 ? 1 : 256 / per_tile;
+    const long long tiles = (A.lines + TLT - 1) / TLT;
+    A.items = (tiles + A.tpc - 1) / A.tpc;
+    if (A.items <= 0) return TDS_OK;
+    int rc;
+    for (int c = 0; c < 3; ++c)
+        if ((rc = encode_xz_map(A.u[c], A.nx, A.ny, A.rows, A.sz, 16, TLT, &A.map[c], &A.boxr)) ||
+            (rc = encode_xz_map(A.out[c], A.nx, A.ny, A.rows, A.sz, 16, TLT, &A.omap[c],
+                                &A.boxr)))
+            return rc;
+    const int threads = A.tpc * per_tile;
+    const size_t smem = (size_t)A.tpc *
+                            (3 * (size_t)(A.rows + 4) * TLT + 3 * (size_t)2 * A.chunks * TLT +
+                             3 * 2 * TLT) * sizeof(double) +
+                        16 * sizeof(DirRow) + 12 * sizeof(double) + 3 * sizeof(uint64_t);
+    const void* fn = reinterpret_cast<const void*>(k_dd_transport_dir<TLT>);
+    if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd_transport_dir)"))) return rc;
+    const long long grid = persistent_grid(fn, threads, smem, A.items, A.max_ctas);
+    if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport_dir does not fit on an SM");
+    k_dd_transport_dir<TLT><<<(unsigned)grid, threads, smem, s>>>(A);
+    return cuda_check(cudaGetLastError(), "k_dd_transport_dir launch");
+}
+
+}  // namespace
+
+int launch_dd_transport_dir(const FastArgs& f1, const FastArgs& f2, const double* const* u,
+                            double* const* out, double nu, int nx, int ny, int m, int sz,
+                            double* mail, double* mail_prev, double* mail_next,
+                            unsigned long long epoch, int max_ctas, cudaStream_t s) {
+    TdArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.f1 = f1;
+    A.f2 = f2;
+    for (int c = 0; c < 3; ++c) {
+        A.u[c] = u[c];
+        A.out[c] = out[c];
+        if (reinterpret_cast<uintptr_t>(u[c]) % 16 || reinterpret_cast<uintptr_t>(out[c]) % 16)
+            return set_err(TDS_ERR_UNSUPPORTED, "direction distributed transport: alignment");
+    }
+    A.nu = nu;
+    A.has_nu = nu != 0.0;
+    A.lines = (long long)nx * ny;
+    A.rows = m;
+    A.sz = sz;
+    A.chunks = f1.chunks;
+    A.nx = nx;
+    A.ny = ny;
+    A.max_ctas = max_ctas;
+    A.mail = mail;
+    A.mail_prev = mail_prev;
+    A.mail_next = mail_next;
+    A.epoch = epoch;
+    A.timeout_ns = 10ULL * 1000 * 1000 * 1000;
+    if (const char* e = getenv("TDS_FUSED_TIMEOUT_MS"))
+        A.timeout_ns = (unsigned long long)atoll(e) * 1000000ULL;
+    if (ny % sz || !f1.Hb || f1.nb <= 0 || (A.has_nu && (!f2.Hb || f2.nb <= 0)))
+        return set_err(TDS_ERR_UNSUPPORTED, "direction distributed transport: shape / band");
+    int tl = 16;
+    if (const char* e = getenv("TDS_TRANSPORT_TL")) tl = atoi(e) == 8 ? 8 : 16;
+    const size_t need16 = (size_t)3 * (m + 4) * 16 * 8;
+    if (tl == 16 && sz % 16 == 0 && A.chunks * 16 <= 512 && need16 <= 200 * 1024)
+        return launch_dd_transport_dir_t<16>(A, s);
+    if (sz % 8 == 0 && A.chunks * 8 <= 512 && (size_t)3 * (m + 4) * 8 * 8 <= 200 * 1024)
+        return launch_dd_transport_dir_t<8>(A, s);
+    return set_err(TDS_ERR_UNSUPPORTED, "direction distributed transport: tile");
 }
 
 }  // namespace tds

@@ -657,12 +657,6 @@ int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
 // constant DFMA operands (no loads), fully unrolled.
 constexpr int NBC_MAX = 24;
 
-// per-row coefficients of the d/dx (1) and d2/dx2 (2) chunk tables
-struct DirRow {
-    double2 rf1, rf2;         // (r, f)
-    double2 w12;              // (w1, w2)
-    double2 s1, s2;           // (sa, sc)
-};
 
 struct TransportDirArgs {
     TransportArgs p;          // geometry, tables and reduced maps (ui/uj/out unused)
@@ -682,66 +676,6 @@ struct TransportDirArgs {
 
 namespace {
 
-// two solves of one window (tables 1 and 2) / one solve (table 1), the
-// arithmetic of sweeps2_src / sweeps_src with the DirRow table
-template <int M, typename Src>
-__device__ __forceinline__ void dsweeps2(const DirRow (&R)[16], const double* st1,
-                                         const double* st2, Src v, double (&d1)[M],
-                                         double (&d2)[M]) {
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        const double v0 = v(i), v1 = v(i + 1), v2 = v(i + 2), v3 = v(i + 3), v4 = v(i + 4);
-        double a = st1[0] * v0, b = st2[0] * v0;
-        a = fma(st1[1], v1, a);
-        b = fma(st2[1], v1, b);
-        a = fma(st1[2], v2, a);
-        b = fma(st2[2], v2, b);
-        a = fma(st1[3], v3, a);
-        b = fma(st2[3], v3, b);
-        a = fma(st1[4], v4, a);
-        b = fma(st2[4], v4, b);
-        const double2 rf1 = R[i].rf1, rf2 = R[i].rf2;
-        if (i < 2) {
-            d1[i] = a * rf1.x;
-            d2[i] = b * rf2.x;
-        } else {
-            d1[i] = fma(-rf1.x, d1[i - 1], a) * rf1.y;
-            d2[i] = fma(-rf2.x, d2[i - 1], b) * rf2.y;
-        }
-    }
-#pragma unroll
-    for (int i = M - 3; i >= 1; --i) {
-        const double2 w = R[i].w12;
-        d1[i] = fma(-w.x, d1[i + 1], d1[i]);
-        d2[i] = fma(-w.y, d2[i + 1], d2[i]);
-    }
-    const double2 w = R[0].w12;
-    d1[0] = fma(-w.x, d1[1], d1[0]) * R[0].rf1.y;
-    d2[0] = fma(-w.y, d2[1], d2[0]) * R[0].rf2.y;
-}
-
-template <int M, typename Src>
-__device__ __forceinline__ void dsweeps1(const DirRow (&R)[16], const double* st, Src v,
-                                         double (&d)[M]) {
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        double rhs = st[0] * v(i);
-        rhs = fma(st[1], v(i + 1), rhs);
-        rhs = fma(st[2], v(i + 2), rhs);
-        rhs = fma(st[3], v(i + 3), rhs);
-        rhs = fma(st[4], v(i + 4), rhs);
-        const double2 rf = R[i].rf1;
-        if (i < 2) d[i] = rhs * rf.x;
-        else d[i] = fma(-rf.x, d[i - 1], rhs) * rf.y;
-    }
-#pragma unroll
-    for (int i = M - 3; i >= 1; --i) d[i] = fma(-R[i].w12.x, d[i + 1], d[i]);
-    d[0] = fma(-R[0].w12.x, d[1], d[0]) * R[0].rf1.y;
-}
-
-__device__ __forceinline__ double subst2(double2 s, int i, int M, double F, double L, double di) {
-    return i == 0 ? F : (i == M - 1 ? L : fma(-s.y, L, fma(-s.x, F, di)));
-}
 
 // (F, L) of a chunk from a circulant band row held in the parameter bank:
 // the same terms and association as band_bounds (even columns into F0 / L0,

@@ -399,6 +399,7 @@ class SlabTransport:
             self._zmail = {}
             self._zepoch = 0
             self._zbroken = None
+            self._zdir = None          # k_dd_transport_dir usable (None: not tried yet)
 
     def local_slab(self, u3):
         """Pack this rank's slab of a global Cartesian (n, n, n) array for x."""
@@ -490,6 +491,23 @@ class SlabTransport:
             self._zmail[key] = mb
         self._poll_z()
         stream = _torch().cuda.current_stream()
+        if os.environ.get("TDS_TRANSPORT_DIR") != "0" and self._zdir is not False:
+            # all three components in one kernel per rank (k_dd_transport_dir)
+            self._zepoch += 1
+            rc = N.lib().tds_fused_transport_direction(
+                p1.handle, None if p2 is None else p2.handle, _vp(vel[0]), _vp(vel[1]),
+                _vp(vel[2]), _vp(acc[0]), _vp(acc[1]), _vp(acc[2]), self.nu, n, n, m, sz,
+                mb.own, mb.prev, mb.next, self._zepoch, self.ctx.fused_grid_cap,
+                ctypes.c_void_p(stream.cuda_stream))
+            if rc == N.TDS_OK:
+                self._zdir = True
+                self.ctx.exchange_rounds += 18       # 9 solves x 2 rounds, as 3 terms
+                mb.post_status(stream)
+                return True
+            if rc != N.TDS_ERR_UNSUPPORTED or self._zdir:
+                N.check(rc)
+            self._zepoch -= 1
+            self._zdir = False             # same decision on every rank: plans / shape only
         for i in range(3):
             self._zepoch += 1
             rc = N.lib().tds_fused_transport_in_x(
@@ -505,14 +523,15 @@ class SlabTransport:
         return True
 
     def _poll_z(self, block=False):
-        """Fold the fused z kernels' status words into the context (posted
-        halo words of u_i and u_j: 4 L per directed edge per term, boundary
-        rows: one L per solve); TimeoutError if a wait timed out."""
+        """Fold the fused z kernels' status words into the context: one
+        message per field halo (2 L posted words per directed edge: u_i and
+        u_j per term, u_0..u_2 per direction kernel) and per boundary row
+        (L words per solve); TimeoutError if a wait timed out."""
         from .rank import account_status
         for (groups, sz), mb in self._zmail.items():
             lines = groups * sz
             try:
-                account_status(self.ctx, mb, 4 * lines, lines, block)
+                account_status(self.ctx, mb, 2 * lines, lines, block)
             except TimeoutError as exc:
                 self._zbroken = exc
                 raise

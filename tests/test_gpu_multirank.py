@@ -251,16 +251,21 @@ def test_fused_timeout_raises_and_poisons(env):
         group.close()
 
 
-@pytest.mark.parametrize("p,nu,sz,tl,zin", [(2, 0.02, 16, "16", "1"), (2, 0.0, 32, "16", "1"),
-                                             (4, 0.01, 32, "16", "1"), (2, 0.02, 32, "8", "1"),
-                                             (2, 0.02, 32, "16", "0"), (4, 0.0, 16, "8", "0")])
-def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz, tl, zin, env):
-    # BASELINE config 5's distributed RHS: z-slabs on P in-process ranks, the
-    # z terms as one k_dd_transport per rank (in-kernel neighbour rounds),
-    # read in place from the x-layout slab and added by TMA reduce-add
-    # (TDS_TRANSPORT_Z=0: on re-laid-out z fields); TDS_TRANSPORT_TL=8: the
-    # kernel's 8-line tiles
-    env({"TDS_TRANSPORT_TL": tl, "TDS_TRANSPORT_Z": zin})
+@pytest.mark.parametrize("p,nu,sz,tl,zmode", [(2, 0.02, 16, "16", "dir"), (2, 0.0, 32, "16", "dir"),
+                                               (4, 0.01, 32, "16", "dir"), (2, 0.02, 32, "8", "dir"),
+                                               (4, 0.0, 16, "8", "dir"), (2, 0.02, 32, "16", "term"),
+                                               (4, 0.01, 16, "16", "term"),
+                                               (2, 0.02, 32, "16", "relayout"),
+                                               (4, 0.0, 16, "8", "relayout")])
+def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz, tl, zmode, env):
+    # BASELINE config 5's distributed RHS: z-slabs on P in-process ranks.
+    # dir: the three z terms in ONE k_dd_transport_dir per rank, read in
+    # place from the x-layout slab, added by TMA reduce-add; term: one
+    # in-place k_dd_transport per term (TDS_TRANSPORT_DIR=0); relayout: on
+    # re-laid-out z fields (TDS_TRANSPORT_Z=0). TDS_TRANSPORT_TL=8: the
+    # kernels' 8-line tiles
+    env({"TDS_TRANSPORT_TL": tl, "TDS_TRANSPORT_Z": "0" if zmode == "relayout" else "1",
+         "TDS_TRANSPORT_DIR": "0" if zmode == "term" else "1"})
     n = 128
     h = 2 * np.pi / n
     rng = np.random.default_rng(77)
