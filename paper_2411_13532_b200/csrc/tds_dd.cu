@@ -441,7 +441,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         __stcs(ob + (long long)(r0 + M - 1) * sz, L);
     };
     // finish the stashed item `fi` (edge warps only; warp-synchronous)
-    auto finish = [&](long long fi, int fslot) {
+    // the neighbour's row slot finish() takes for item fi (edge threads)
+    auto pin_slot = [&](long long fi) -> double* {
+        const long long fl = (fi * tpc + tl) * TLT + lane;
+        return A.mail + par + (first_chunk ? mb.d_from_prev() : mb.d_from_next()) + fl;
+    };
+    // pv: the slot's value if loaded early (at the top of the iteration, so
+    // the L2 round trip overlaps the tile wait), else SENTINEL
+    auto finish = [&](long long fi, int fslot, unsigned long long pv) {
         const double* GY = sGY + ((size_t)fslot * tpc + tl) * 2 * TLT;
         const long long fl = (fi * tpc + tl) * TLT + lane;
         const bool fv = fl < p.lines;
@@ -449,14 +456,14 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         if (first_chunk) {
             us = GY[lane];
             if (fv && p.has_prev) {
-                const double prev_last = take(A.mail + par + mb.d_from_prev() + fl, A, err);
+                const double prev_last = take_v(pin_slot(fi), pv, A, err);
                 us = (us - p.sa_first * prev_last) / p.det_prev;
             }
         }
         if (last_chunk) {
             ue = GY[TLT + lane];
             if (fv && p.has_next) {
-                const double next_first = take(A.mail + par + mb.d_from_next() + fl, A, err);
+                const double next_first = take_v(pin_slot(fi), pv, A, err);
                 ue = (ue - p.sc_last * next_first) / p.det_next;
             }
         }
@@ -536,6 +543,10 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             b0 = ld_sys_u64(hhi);
             b1 = ld_sys_u64(hhi + sz);
         }
+        unsigned long long pin_pre = SENTINEL;
+        if (prev_item >= 0 && ((first_chunk && p.has_prev) || (last_chunk && p.has_next)) &&
+            (prev_item * tpc + tl) * TLT + lane < p.lines)
+            pin_pre = ld_sys_u64(pin_slot(prev_item));
 
         while (!mbar_try_wait(bar, phase)) {
         }
@@ -614,7 +625,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
                     sGY[(((size_t)(it & 1) * tpc + tl) * 2 + r) * TLT + lane] = gy;
                 }
             }
-            if (prev_item >= 0) finish(prev_item, (it & 1) ^ 1);
+            if (prev_item >= 0) finish(prev_item, (it & 1) ^ 1, pin_pre);
             __syncwarp();
             stash[0] = F;
 #pragma unroll
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     }
     if (prev_item >= 0) {
         __syncthreads();   // the helper warp's g.Y of the last item
-        if (edge_warp) finish(prev_item, (it - 1) & 1);
+        if (edge_warp) finish(prev_item, (it - 1) & 1, SENTINEL);
     }
     {
         const unsigned n = valid_items(p.items, p.lines, tpc, tl, TLT, lane);
