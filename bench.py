@@ -207,6 +207,7 @@ def run_single(args, torch):
     del fields, outs
     torch.cuda.empty_cache()
     t1 = t1_anchor(args, torch) if not args.no_t1 else None
+    tr = transport_rhs(args, torch) if not args.no_transport else None
     res = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -233,6 +234,7 @@ def run_single(args, torch):
         "gpu_launches": 3 * args.steps,
         "clocks": clocks,
         "t1_1024": t1,
+        "transport_rhs": tr,
     }
     res["cpu_baseline"] = cpu_baseline(args, n)
     return res
@@ -265,6 +267,78 @@ def t1_anchor(args, torch, n=1024, steps=10):
     return {"n": n, "ms_per_step": round(ms, 4),
             "gbs": round(3 * BYTES_PER_POINT * n ** 3 / (ms * 1e-3) / 1e9, 1),
             "steps": steps, "path": T.get_plan(sys_, st, part).path}
+
+
+def transport_rhs(args, torch, ctx=None, dist=None):
+    """BASELINE config 5 (the DistD2 path's consumer): the momentum-transport
+    RHS, nu = 0.01, sz = 32, synthetic randn velocity -- 512^3 through
+    evaluate_transport_rhs on one GPU, 1024^3 through SlabTransport (z-slabs,
+    one rank per GPU) at N > 1. Best of `reps` CUDA-event timings (max over
+    ranks). Algorithmic bytes: 192 B/pt (k_transport_dir x / y / z passes:
+    u, v, w read once per direction, 3 writes / 3 read-modify-writes). Never
+    fails the bench line: an error is reported in the key."""
+    import numpy as np
+    import paper_2411_13532_b200 as T
+    try:
+        reps, nu = 3, 0.01
+        world = 1 if ctx is None else ctx.rank_count
+        n = 512 if ctx is None else 1024
+        h = 2 * np.pi / n
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5 + (0 if ctx is None else ctx.rank_id))
+        if ctx is None:
+            u3, v3, w3 = (torch.randn((n, n, n), dtype=torch.float64, device="cuda",
+                                      generator=g) for _ in range(3))
+            f = T.VelocityField.from_arrays(u3, v3, w3, nu, h, sz=SZ)
+            del u3, v3, w3
+
+            def step():
+                return T.evaluate_transport_rhs(f)
+            tr = None
+            what = "evaluate_transport_rhs: k_transport_dir per direction"
+        else:
+            tr = T.SlabTransport(n, SZ, nu, h, ctx)
+            lay = tr.lay["x"]
+            vel = [torch.randn((lay.n_groups, lay.n, lay.sz), dtype=torch.float64,
+                               device="cuda", generator=g) for _ in range(3)]
+
+            def step():
+                return tr.rhs(*vel)
+            what = ("SlabTransport: x / y k_transport_dir on the slab, z k_dd_transport_dir "
+                    "(in-kernel NVLink rounds)" if tr.fused_z else "SlabTransport")
+        step()
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a.record()
+            step()
+            b.record()
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b)
+            if dist is not None:
+                tt = torch.tensor([t], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            best = min(best, t)
+        if tr is not None:
+            tr.check()
+            tr.close()
+        torch.cuda.empty_cache()
+        pts = n ** 3
+        gbs = 192 * pts / (best * 1e-3) / 1e9
+        peak, _ = peaks()
+        return {"config": f"BASELINE configs[4]: transport RHS {n}^3 on {world} GPU(s), "
+                          f"nu={nu}, sz={SZ}", "path": what, "ms_per_rhs": round(best, 3),
+                "gdof_per_s": round(pts / (best * 1e-3) / 1e9, 2),
+                "algorithmic_gbs_192B": round(gbs, 1),
+                "frac_of_peak": round(gbs / (world * peak), 4), "reps": reps}
+    except Exception as exc:   # noqa: BLE001 -- reported, never fatal
+        torch.cuda.empty_cache()
+        return {"error": repr(exc)[:300]}
 
 
 def run_e2e(args, torch, T, sys_, st, part, fields, n):
@@ -358,6 +432,12 @@ def run_multi(args, torch):
     local_points = groups * m * SZ
     achieved = BYTES_PER_POINT * local_points / (solve_ms * 1e-3) / 1e9
     e2e = run_multi_e2e(args, torch, dist, solver, fields, n, world, dev)
+    del fields, outs
+    torch.cuda.empty_cache()
+    tr = None
+    if not args.no_transport and n == 1024:
+        tctx = RankContext.from_process_group(cyclic=True)
+        tr = transport_rhs(args, torch, tctx, dist)
     res = None
     if rank == 0:
         res = {
@@ -388,6 +468,7 @@ def run_multi(args, torch):
             # north star: E(N) = T1(1024^3) / (N * T_N), same box, same operator
             "efficiency_vs_t1": (round(anchor["ms_per_step"] / (world * ms_step), 4)
                                  if anchor else None),
+            "transport_rhs": tr,
         }
     dist.barrier()
     solver.close()
@@ -567,6 +648,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--cpu-groups", type=int, default=256, help="max SZ-groups per CPU worker")
     ap.add_argument("--no-t1", action="store_true", help="skip the T1(1024^3) anchor")
+    ap.add_argument("--no-transport", action="store_true",
+                    help="skip the config-5 transport RHS measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
