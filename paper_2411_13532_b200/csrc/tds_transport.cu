@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "tds_device.cuh"
@@ -682,13 +683,15 @@ namespace {
 // odd into F1 / L1). Yb = this chunk's first band column in the extended Y
 // buffer (K entries plus a copy of the first NBC_MAX: no wrap), so every
 // read is an immediate offset from one address.
-template <int TLT>
+template <int TLT, int NB = 0>
 __device__ __forceinline__ void circ_bounds(const double2 (&h)[NBC_MAX], int nb,
                                             const double* Yb, double& F, double& L) {
     double F0 = 0.0, F1 = 0.0, L0 = 0.0, L1 = 0.0;
+    // NB > 0: the band length known at compile time (no per-column
+    // predicates: the band row can stay constant-bank operands)
 #pragma unroll
-    for (int j = 0; j < NBC_MAX; ++j) {
-        if (j < nb) {
+    for (int j = 0; j < (NB ? NB : NBC_MAX); ++j) {
+        if (NB || j < nb) {
             const double y = Yb[j * TLT];
             if (j & 1) {
                 F1 = fma(h[j].x, y, F1);
@@ -705,7 +708,7 @@ __device__ __forceinline__ void circ_bounds(const double2 (&h)[NBC_MAX], int nb,
 
 }  // namespace
 
-template <int TLT, int GEOM, int SZC>
+template <int TLT, int GEOM, int SZC, int NB1, int NB2>
 __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ TransportDirArgs A) {
     constexpr int M = 16;
     constexpr bool ACC = GEOM != GEOM_LINES;   // x pass writes, y / z passes add
@@ -926,8 +929,8 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
                 }
                 if (s == 0) wait_tile(jd);
                 double F2, L2;
-                circ_bounds<TLT>(A.hc1, A.nbc1, YA + yo1, F, L);
-                circ_bounds<TLT>(A.hc2, A.nbc2, YC + yo2, F2, L2);
+                circ_bounds<TLT, NB1>(A.hc1, A.nbc1, YA + yo1, F, L);
+                circ_bounds<TLT, NB2>(A.hc2, A.nbc2, YC + yo2, F2, L2);
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
                     const DirRow& R = RT[i];
@@ -944,7 +947,7 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
                     pend = -1;
                 }
                 if (s == 0) wait_tile(jd);
-                circ_bounds<TLT>(A.hc1, A.nbc1, YA + yo1, F, L);
+                circ_bounds<TLT, NB1>(A.hc1, A.nbc1, YA + yo1, F, L);
 #pragma unroll
                 for (int i = 0; i < M; ++i)
                     acc[i] = -0.5 * rd(Tj, i + 2) * subst2(RT[i].s1, i, M, F, L, d[i]);
@@ -958,7 +961,7 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
                 fence_proxy_async();
                 issue(c, nxt);
             }
-            circ_bounds<TLT>(A.hc1, A.nbc1, YB + yo1, F, L);
+            circ_bounds<TLT, NB1>(A.hc1, A.nbc1, YB + yo1, F, L);
 #pragma unroll
             for (int i = 0; i < M; ++i) acc[i] = fma(-0.5, subst2(RT[i].s1, i, M, F, L, d[i]), acc[i]);
             if (!STAGE) {
@@ -1004,8 +1007,8 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
 
 namespace {
 
-template <int TLT, int GEOM, int SZC = 0>
-int launch_transport_dir_t(const TransportDirArgs& a0, cudaStream_t s) {
+template <int TLT, int GEOM, int SZC, int NB1, int NB2>
+int launch_transport_dir_nb(const TransportDirArgs& a0, cudaStream_t s) {
     TransportDirArgs A = a0;
     const TransportArgs& a = A.p;
     const int per_tile = a.chunks * TLT;
@@ -1039,12 +1042,23 @@ int launch_transport_dir_t(const TransportDirArgs& a0, cudaStream_t s) {
                             (3 * (size_t)a.rows * TLT + 3 * (size_t)(2 * a.chunks + A.ydup) * TLT) *
                             sizeof(double) + 16 * sizeof(DirRow) + 12 * sizeof(double) +
                         3 * sizeof(uint64_t);
-    const void* fn = reinterpret_cast<const void*>(k_transport_dir<TLT, GEOM, SZC>);
+    const void* fn = reinterpret_cast<const void*>(k_transport_dir<TLT, GEOM, SZC, NB1, NB2>);
     if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_transport_dir)"))) return rc;
     const long long grid = persistent_grid(fn, threads, smem, A.items, 0);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_transport_dir does not fit on an SM");
-    k_transport_dir<TLT, GEOM, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
+    k_transport_dir<TLT, GEOM, SZC, NB1, NB2><<<(unsigned)grid, threads, smem, s>>>(A);
     return cuda_check(cudaGetLastError(), "k_transport_dir launch");
+}
+
+// the band lengths of the 6th-order d/dx and d2/dx2 operators with 16-row
+// chunks (16 / 8 columns at 2^-70) as compile-time constants; others (or
+// nu = 0, TDS_TRANSPORT_DIR_NB=0) take the predicated runtime loop
+template <int TLT, int GEOM, int SZC = 0>
+int launch_transport_dir_t(const TransportDirArgs& a, cudaStream_t s) {
+    const char* e = getenv("TDS_TRANSPORT_DIR_NB");
+    if (!(e && e[0] == '0') && a.nbc1 == 16 && a.nbc2 == 8 && a.p.has_nu)
+        return launch_transport_dir_nb<TLT, GEOM, SZC, 16, 8>(a, s);
+    return launch_transport_dir_nb<TLT, GEOM, SZC, 0, 0>(a, s);
 }
 
 // tile width of k_transport_dir: 16 lines (one CTA of 512 threads per SM at
@@ -1113,6 +1127,9 @@ int transport_direction_from_plans(const tds_plan* d1, const tds_plan* d2, const
     A.nbc2 = e2->band_n;
     A.q02 = e2->band_q0;
     for (int j = 0; j < e2->band_n; ++j) A.hc2[j] = e2->band_row[j];
+    if (getenv("TDS_DEBUG_BAND"))
+        fprintf(stderr, "k_transport_dir: rows %d band %d / %d (q0 %d / %d)\n", a.rows, A.nbc1,
+                A.nbc2, A.q01, A.q02);
     A.ydup = std::max(A.nbc1, A.nbc2);
     A.ydup += A.ydup & 1;
     if (A.ydup > 2 * a.chunks) return set_err(TDS_ERR_UNSUPPORTED, "direction transport: band > K");
