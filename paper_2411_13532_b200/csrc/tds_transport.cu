@@ -747,8 +747,11 @@ __global__ void __launch_bounds__(512) k_transport_dir(const __grid_constant__ T
     // (a kernel-parameter copy of the table is hoisted into registers and
     // spills: measured 10.6 vs 9.87 ms for the 512^3 RHS)
     const DirRow (&RT)[16] = *reinterpret_cast<const DirRow(*)[16]>(sR);
-    const double* st1 = sst;
-    const double* st2 = sst + 5;
+    // stencil weights: kernel-parameter bank (uniform-register operands;
+    // measured x 1.88 -> 1.75, y 2.14 -> 1.93 ms at 512^3) except in the z
+    // pass, where they cost registers and spills (2.08 -> 2.35 ms)
+    const double* st1 = GEOM == GEOM_XZ ? sst : p.t1.st;
+    const double* st2 = GEOM == GEOM_XZ ? sst + 5 : p.t2.st;
     // circulant band: chunk k's window starts at (q0 + 2k) mod K
     const int q1 = (A.q01 + 2 * chunk) % K, q2 = (A.q02 + 2 * chunk) % K;
     const bool dup = 2 * chunk < A.ydup;   // this chunk's Y entries also go to K + 2k
