@@ -251,13 +251,17 @@ def test_fused_timeout_raises_and_poisons(env):
         group.close()
 
 
-@pytest.mark.parametrize("p,nu,sz,tl,zmode", [(2, 0.02, 16, "16", "dir"), (2, 0.0, 32, "16", "dir"),
-                                               (4, 0.01, 32, "16", "dir"), (2, 0.02, 32, "8", "dir"),
-                                               (4, 0.0, 16, "8", "dir"), (2, 0.02, 32, "16", "term"),
-                                               (4, 0.01, 16, "16", "term"),
-                                               (2, 0.02, 32, "16", "relayout"),
-                                               (4, 0.0, 16, "8", "relayout")])
-def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz, tl, zmode, env):
+@pytest.mark.parametrize("p,nu,sz,tl,zmode,n", [(2, 0.02, 16, "16", "dir", 128),
+                                                 (2, 0.0, 32, "16", "dir", 128),
+                                                 (4, 0.01, 32, "16", "dir", 128),
+                                                 (2, 0.02, 32, "8", "dir", 128),
+                                                 (4, 0.0, 16, "8", "dir", 128),
+                                                 (8, 0.01, 32, "16", "dir", 256),
+                                                 (2, 0.02, 32, "16", "term", 128),
+                                                 (4, 0.01, 16, "16", "term", 128),
+                                                 (2, 0.02, 32, "16", "relayout", 128),
+                                                 (4, 0.0, 16, "8", "relayout", 128)])
+def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz, tl, zmode, n, env):
     # BASELINE config 5's distributed RHS: z-slabs on P in-process ranks.
     # dir: the three z terms in ONE k_dd_transport_dir per rank, read in
     # place from the x-layout slab, added by TMA reduce-add; term: one
@@ -266,7 +270,6 @@ def test_slab_transport_ranks_one_device_vs_oracle(p, nu, sz, tl, zmode, env):
     # kernels' 8-line tiles
     env({"TDS_TRANSPORT_TL": tl, "TDS_TRANSPORT_Z": "0" if zmode == "relayout" else "1",
          "TDS_TRANSPORT_DIR": "0" if zmode == "term" else "1"})
-    n = 128
     h = 2 * np.pi / n
     rng = np.random.default_rng(77)
     u3, v3, w3 = (rng.standard_normal((n, n, n)) for _ in range(3))
