@@ -111,9 +111,17 @@ extern "C" int tds_solve(const tds_plan* p, const double* u, double* out, long l
         a.u = u;
         a.out = out;
         a.edge_mode = p->periodic ? tds::EDGE_WRAP : tds::EDGE_ZERO;
+        // dynamic item schedule (SMs stream HBM at different rates: a static
+        // round-robin leaves the fastest idle for the slowest). Knob
+        // TDS_DYN=0: static.
+        if (p->d_ctr && !(getenv("TDS_DYN") && getenv("TDS_DYN")[0] == '0')) {
+            const unsigned slot = __atomic_fetch_add(&p->ctr_next, 1u, __ATOMIC_RELAXED);
+            a.ctr = p->d_ctr + 2 * (slot % tds::CTR_SLOTS);
+        }
         if (p->C <= tds::MAX_CHUNKS)
             return tds::launch_fast(p->M, tds::MODE_SOLVE, p->uniform, a, tiles_of(lines),
                                     S(stream));
+        a.ctr = nullptr;
         // a line longer than one CTA holds: split over a thread-block cluster
         // (k_tmc), else the plan's staged tables
         if (tds::tmc_eligible(p->M, p->uniform, a)) return tds::launch_tmc(p->M, p->uniform, a, S(stream));

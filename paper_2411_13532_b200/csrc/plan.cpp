@@ -922,6 +922,10 @@ int plan_create_impl(const double* lower, const double* diag, const double* uppe
             }
         }
         if ((rc = upload_H(p, H, gv))) return fail(rc);
+        {
+            const std::vector<unsigned long long> zero(2 * tds::CTR_SLOTS, 0ULL);
+            if ((rc = upload(p, &p->d_ctr, zero.data(), zero.size()))) return fail(rc);
+        }
         if (cs.C > tds::MAX_CHUNKS) {   // cluster kernel (k_tmc) or the staged fallback
             if ((rc = build_staged())) return fail(rc);
             p->has_staged = 1;

@@ -16,6 +16,7 @@ constexpr int TL = 16;                     // lines per tile: 16 x fp64 = 128 B 
 constexpr int NCOEF = 10;                  // per-row table: st0..st4, f, r, w, sa, sc
 constexpr int MMAX_UNIFORM = 32;
 constexpr int MAX_CHUNKS = 32;             // C*TL <= 512 threads per tile
+constexpr int CTR_SLOTS = 16;              // k_tma schedule counters per plan
 
 enum FastMode { MODE_SOLVE = 0, MODE_PASS_A = 1, MODE_PASS_B = 2 };
 enum EdgeMode { EDGE_ZERO = 0, EDGE_WRAP = 1, EDGE_HALO = 2 };
@@ -79,6 +80,10 @@ struct FastArgs {
     double sa_first, sc_last, prev_sc_last, next_sa_first, det_prev, det_next;
     UniformTable ut;
     EdgeTable e_first, e_last;
+    // dynamic item schedule of the single-GPU persistent kernels (k_tma):
+    // ctr[0] hands out items past the grid's first, ctr[1] counts CTAs out
+    // (the last one resets both); nullptr = static round-robin
+    unsigned long long* ctr;
 };
 
 // Staged (reference-arithmetic) kernels: one thread per (line, block).
@@ -179,6 +184,10 @@ struct tds_plan {
     double2* d_Hb = nullptr;   // banded H: C x band_n, columns d_bq0[k] + j (mod K)
     int* d_bq0 = nullptr;
     int band_n = 0;
+    // k_tma dynamic-schedule counters: CTR_SLOTS pairs, one per launch in
+    // flight (round-robin; a slot is reset by its launch's last CTA)
+    unsigned long long* d_ctr = nullptr;
+    mutable unsigned ctr_next = 0;
     int g_n0 = 0, g_n1 = 0;   // significant leading / trailing terms of g0 / g1
     double* d_g = nullptr;
     double sa_first = 0, sc_last = 0, prev_sc_last = 0, next_sa_first = 0;

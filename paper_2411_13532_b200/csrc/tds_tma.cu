@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         }
     };
 
+    __shared__ long long s_next[2];   // next item (dynamic schedule), by iteration parity
     if (t == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -113,7 +114,10 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     if (t == 0 && item < p.items) issue(item);
     uint32_t phase = 0;
 
-    for (int it = 0; item < p.items; item += gridDim.x, ++it) {
+    // items past the first: round-robin, or (p.ctr) handed out in order of
+    // request -- thread 0 takes the next when it issues its TMA, everyone
+    // reads it after the iteration's second barrier
+    for (int it = 0; item < p.items; item = s_next[it & 1], ++it) {
         const long long line = (item * tpc + tl) * TLT + lane;
         const bool valid = line < p.lines;
 
@@ -147,7 +151,9 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
         }
         __syncthreads();   // every thread holds its rows: the tile buffer is free
         if (t == 0) {
-            const long long nxt = item + gridDim.x;
+            const long long nxt =
+                p.ctr ? (long long)gridDim.x + (long long)atomicAdd(p.ctr, 1ULL) : item + gridDim.x;
+            s_next[it & 1] = nxt;
             if (nxt < p.items) {
                 fence_proxy_async();
                 issue(nxt);
@@ -214,6 +220,16 @@ __global__ void __launch_bounds__(512) k_tma(const __grid_constant__ TmaArgs A) 
     }
     if constexpr (BST != 0)
         if (lane == 0) bulk_wait_all();                // staging reads done before exit
+    if (p.ctr && t == 0) {
+        // every CTA has taken its last item once all have come here: the last
+        // one out resets the slot for the next launch that uses it
+        __threadfence();
+        if (atomicAdd(p.ctr + 1, 1ULL) == gridDim.x - 1) {
+            p.ctr[0] = 0;
+            p.ctr[1] = 0;
+            __threadfence();
+        }
+    }
 }
 
 namespace {

@@ -372,3 +372,39 @@ def test_long_lines_cluster_kernel_vs_oracle(n, p, periodic, kind, sz):
         np.testing.assert_array_equal(got, want)
     else:
         assert O.rel_linf(got, want) <= TOL
+
+
+@pytest.mark.parametrize("n,periodic", [(512, True), (512, False), (256, True)])
+def test_dynamic_item_schedule_bitwise_and_concurrent(monkeypatch, n, periodic):
+    """k_tma hands items past the grid's first out through a per-plan counter
+    (TDS_DYN, default): on a field with dozens of items per CTA the result is
+    bit-identical to the static round-robin schedule and to the oracle's
+    bound, repeated launches reuse the counter slots (last CTA resets them),
+    and launches of ONE plan on several streams at once use different slots."""
+    groups, sz = 2048, 32                              # 65536 lines, >> 148 CTAs x 1 tile
+    lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, periodic)
+    s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
+    st = T.StencilCoeffs(stc)
+    u = torch.randn((groups, n, sz), dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(n))
+    monkeypatch.setenv("TDS_DYN", "0")
+    ref = T.run_distd2(s, u, stencil=st)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("TDS_DYN", "1")
+    for _ in range(20):                                # > the 16 counter slots
+        got = T.run_distd2(s, u, stencil=st)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [torch.empty_like(u) for _ in streams]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for st_, o in zip(streams, outs):
+            with torch.cuda.stream(st_):
+                T.run_distd2(s, u, stencil=st, out=o)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
+    sub = u[:64].cpu().numpy()
+    want = O.run_distd2(lo, di, up, periodic, sub, stc)
+    assert O.rel_linf(ref[:64].cpu().numpy(), want) <= 1e-12
