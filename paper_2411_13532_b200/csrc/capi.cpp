@@ -349,6 +349,12 @@ extern "C" int tds_fused_solve(const tds_plan* p, const double* u, double* out, 
     a.edge_mode = tds::EDGE_HALO;
     if (!tds::dd_eligible(p->M, a))
         return set_err(TDS_ERR_UNSUPPORTED, "field not eligible for the fused kernel");
+    // dynamic item schedule (k_dd / k_dd2; deadlock-free with one counter per
+    // rank, see k_dd). Knob TDS_DYN=0: round-robin.
+    if (p->d_ctr && !(getenv("TDS_DYN") && getenv("TDS_DYN")[0] == '0')) {
+        const unsigned slot = __atomic_fetch_add(&p->ctr_next, 1u, __ATOMIC_RELAXED);
+        a.ctr = p->d_ctr + 2 * (slot % tds::CTR_SLOTS);
+    }
     return tds::launch_dd(p->M, p->uniform, a, mail, p->has_prev ? mail_prev : nullptr,
                           p->has_next ? mail_next : nullptr, epoch, max_ctas, S(stream));
 }

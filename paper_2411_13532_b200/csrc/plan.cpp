@@ -652,6 +652,10 @@ int build_local(tds_plan* p, const Global& loc, int has_prev, int has_next, doub
             }
             p->dd_defer[v] = ok ? 1 : 0;
         }
+        {
+            const std::vector<unsigned long long> zero(2 * tds::CTR_SLOTS, 0ULL);
+            if ((rc = upload(p, &p->d_ctr, zero.data(), zero.size()))) return rc;
+        }
         return upload_H(p, rm.Hpin, gv);
     }
     p->path = TDS_PATH_STAGED;

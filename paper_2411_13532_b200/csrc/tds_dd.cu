@@ -200,22 +200,35 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         }
     };
 
+    // item schedule: round-robin, or (p.ctr) handed out by a per-plan
+    // counter in increasing order (the SMs stream HBM at different rates).
+    // Thread 0 claims two items ahead (the halo rows of the next item are
+    // posted at the top of an iteration); s_q[k % 3] = the CTA's k-th item.
+    // Deadlock freedom with independent counters per rank: the smallest
+    // item claimed but not finished on either rank always progresses -- its
+    // partner on the other rank is claimed (counters are monotonic) and, as
+    // every CTA posts before it waits, already posted.
+    __shared__ long long s_q[3];
     if (t == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
+        s_q[1] = p.ctr ? (long long)gridDim.x + (long long)atomicAdd(p.ctr, 1ULL)
+                       : (long long)blockIdx.x + gridDim.x;
     }
     __syncthreads();
     long long item = blockIdx.x;
+    unsigned nvalid = 0;     // items with a valid line for this thread (message accounting)
     if (item < p.items) {
         if (t == 0) issue(item);
         publish_halo(item);
     }
     uint32_t phase = 0;
 
-    for (int it = 0; item < p.items; item += gridDim.x, ++it) {
+    for (int it = 0; item < p.items; item = s_q[(it + 1) % 3], ++it) {
         const long long line = (item * tpc + tl) * TLT + lane;
         const bool valid = line < p.lines;
-        const long long nxt = item + gridDim.x;
+        nvalid += valid ? 1u : 0u;
+        const long long nxt = s_q[(it + 1) % 3];
         if (nxt < p.items) publish_halo(nxt);          // one item ahead
         // halo slots of this item: loads in flight across the TMA wait
         const long long hb = valid ? halo_base_t<SZC>(line, p.sz) : 0;
@@ -258,9 +271,16 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             v[i] = x;
         }
         __syncthreads();   // tile buffer free
-        if (t == 0 && nxt < p.items) {
-            fence_proxy_async();
-            issue(nxt);
+        if (t == 0) {
+            if (nxt < p.items) {
+                fence_proxy_async();
+                issue(nxt);
+            }
+            // the item after next (read at the top of the next iteration,
+            // after this iteration's second barrier)
+            s_q[(it + 2) % 3] = nxt >= p.items ? p.items
+                                : p.ctr ? (long long)gridDim.x + (long long)atomicAdd(p.ctr, 1ULL)
+                                        : nxt + gridDim.x;
         }
 
         double d[M];
@@ -325,9 +345,18 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
                                         A.t.store_cs != 0, chunk);
     }
     {
-        const unsigned n = valid_items(p.items, p.lines, tpc, tl, TLT, lane);
+        const unsigned n = nvalid;
         const unsigned per = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
         flush_counts(err, 2 * per * n, per * n);   // 2 halo rows + 1 boundary row per edge
+    }
+    if (p.ctr && t == 0) {
+        // the last CTA out resets the counter slot for its next launch
+        __threadfence();
+        if (atomicAdd(p.ctr + 1, 1ULL) == gridDim.x - 1) {
+            p.ctr[0] = 0;
+            p.ctr[1] = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -512,12 +541,24 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         __stcs(ob + (long long)(r0 + M - 1) * sz, L);
     };
 
+    // item schedule: round-robin, or (p.ctr) handed out by a per-plan
+    // counter in increasing order (the SMs stream HBM at different rates).
+    // Thread 0 claims two items ahead (the halo rows of the next item are
+    // posted at the top of an iteration); s_q[k % 3] = the CTA's k-th item.
+    // Deadlock freedom with independent counters per rank: the smallest
+    // item claimed but not finished on either rank always progresses -- its
+    // partner on the other rank is claimed (counters are monotonic) and, as
+    // every CTA posts before it waits, already posted.
+    __shared__ long long s_q[3];
     if (t == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
+        s_q[1] = p.ctr ? (long long)gridDim.x + (long long)atomicAdd(p.ctr, 1ULL)
+                       : (long long)blockIdx.x + gridDim.x;
     }
     __syncthreads();
     long long item = blockIdx.x;
+    unsigned nvalid = 0;     // items with a valid line for this thread (message accounting)
     if (item < p.items) {
         if (t == 0) issue(item);
         publish_halo(item);
@@ -526,10 +567,11 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
     long long prev_item = -1;
 
     int it = 0;
-    for (; item < p.items; item += gridDim.x, ++it) {
+    for (; item < p.items; item = s_q[(it + 1) % 3], ++it) {
         const long long line = (item * tpc + tl) * TLT + lane;
         const bool valid = line < p.lines;
-        const long long nxt = item + gridDim.x;
+        nvalid += valid ? 1u : 0u;
+        const long long nxt = s_q[(it + 1) % 3];
         if (nxt < p.items) publish_halo(nxt);          // one item ahead
         const long long hb = valid ? halo_base_t<SZC>(line, p.sz) : 0;
         double* hlo = (valid && first_chunk && A.mail_prev) ? A.mail + par + mb.h_lo() + hb : nullptr;
@@ -574,9 +616,16 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             v[i] = x;
         }
         __syncthreads();   // tile buffer free
-        if (t == 0 && nxt < p.items) {
-            fence_proxy_async();
-            issue(nxt);
+        if (t == 0) {
+            if (nxt < p.items) {
+                fence_proxy_async();
+                issue(nxt);
+            }
+            // the item after next (read at the top of the next iteration,
+            // after this iteration's second barrier)
+            s_q[(it + 2) % 3] = nxt >= p.items ? p.items
+                                : p.ctr ? (long long)gridDim.x + (long long)atomicAdd(p.ctr, 1ULL)
+                                        : nxt + gridDim.x;
         }
 
         double d[M];
@@ -640,7 +689,7 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         if (edge_warp) finish(prev_item, (it - 1) & 1, SENTINEL);
     }
     {
-        const unsigned n = valid_items(p.items, p.lines, tpc, tl, TLT, lane);
+        const unsigned n = nvalid;
         const unsigned h = (halo_lo_poster && A.mail_prev ? 2u : 0u) +
                            (halo_hi_poster && A.mail_next ? 2u : 0u);
         unsigned b = 0;
@@ -651,6 +700,15 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
             b = (first_chunk && A.mail_prev ? 1u : 0u) + (last_chunk && A.mail_next ? 1u : 0u);
         }
         flush_counts(err, h * n, b * n);
+    }
+    if (p.ctr && t == 0) {
+        // the last CTA out resets the counter slot for its next launch
+        __threadfence();
+        if (atomicAdd(p.ctr + 1, 1ULL) == gridDim.x - 1) {
+            p.ctr[0] = 0;
+            p.ctr[1] = 0;
+            __threadfence();
+        }
     }
 }
 
