@@ -121,7 +121,6 @@ extern "C" int tds_solve(const tds_plan* p, const double* u, double* out, long l
         if (p->C <= tds::MAX_CHUNKS)
             return tds::launch_fast(p->M, tds::MODE_SOLVE, p->uniform, a, tiles_of(lines),
                                     S(stream));
-        a.ctr = nullptr;
         // a line longer than one CTA holds: split over a thread-block cluster
         // (k_tmc), else the plan's staged tables
         if (tds::tmc_eligible(p->M, p->uniform, a)) return tds::launch_tmc(p->M, p->uniform, a, S(stream));

@@ -374,14 +374,16 @@ def test_long_lines_cluster_kernel_vs_oracle(n, p, periodic, kind, sz):
         assert O.rel_linf(got, want) <= TOL
 
 
-@pytest.mark.parametrize("n,periodic", [(512, True), (512, False), (256, True)])
+@pytest.mark.parametrize("n,periodic", [(512, True), (512, False), (256, True), (2048, True),
+                                        (4096, False)])
 def test_dynamic_item_schedule_bitwise_and_concurrent(monkeypatch, n, periodic):
     """k_tma hands items past the grid's first out through a per-plan counter
     (TDS_DYN, default): on a field with dozens of items per CTA the result is
     bit-identical to the static round-robin schedule and to the oracle's
     bound, repeated launches reuse the counter slots (last CTA resets them),
-    and launches of ONE plan on several streams at once use different slots."""
-    groups, sz = 2048, 32                              # 65536 lines, >> 148 CTAs x 1 tile
+    and launches of ONE plan on several streams at once use different slots.
+    n >= 2048: the cluster kernel k_tmc (the cluster's CTA 0 claims items)."""
+    groups, sz = (2048 if n <= 512 else 256), 32       # >> the persistent grid's items
     lo, di, up, stc = O.assemble("d1", n, 2 * np.pi / n, periodic)
     s = T.TridiagonalSystem(lo, di, up, periodic=periodic)
     st = T.StencilCoeffs(stc)
