@@ -800,7 +800,8 @@ bool defer_policy() {
 
 template <int M, int UNI>
 int launch_dd_m(const DDArgs& A, cudaStream_t s) {
-    const TileCfg cfg = tile_cfg(A.t.f);
+    TileCfg cfg = tile_cfg(A.t.f);
+    if (const char* e = getenv("TDS_DD_TPC")) cfg.tpc = std::max(1, atoi(e));
     // deferral pays only if some warps are interior (chunks > 2 warps' worth)
     const int cw = 32 / (cfg.tl ? cfg.tl : 16);
     const char* ev = getenv("TDS_DEFER");
@@ -825,17 +826,27 @@ int launch_dd_m(const DDArgs& A, cudaStream_t s) {
     }
     if constexpr (M == 32) {
         // k_dd with 32-line tiles (one chunk per warp) when no deferral
-        // applies (m = 128: every chunk is an edge chunk). Same choice on
-        // every rank: it depends on the plan and sz only. Knob TDS_DD_TL32=0.
+        // applies and the block has more than 4 chunks. Same choice on every
+        // rank: it depends on the plan and sz only. Knob TDS_DD_TL32=0.
         const bool tl32 = !defer && A.t.f.sz == 32 && A.t.f.chunks * 32 <= 512 &&
+                          A.t.f.chunks > 4 &&
                           !(getenv("TDS_DD_TL32") && getenv("TDS_DD_TL32")[0] == '0') &&
                           !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0');
         if (tl32) {
             const int per_tile = A.t.f.chunks * 32;
-            const TileCfg c32{32, per_tile >= 256 ? 1 : 256 / per_tile};
+            TileCfg c32{32, per_tile >= 256 ? 1 : 256 / per_tile};
+            // TDS_DD_TPC: tiles per CTA (fewer, smaller CTAs keep more items
+            // in flight per SM against the neighbour round trip)
+            if (const char* e = getenv("TDS_DD_TPC")) c32.tpc = std::max(1, atoi(e));
             if (dd_smem(A.t.f, c32) <= 200 * 1024) return launch_dd_t<M, UNI, 32, 32>(A, c32, s);
         }
     }
+    // k_dd on a short block (<= 4 chunks, m = 128 at N = 8: every chunk waits
+    // for the neighbours' rows in its own iteration): one 16-line tile per
+    // CTA, so 8 small CTAs per SM keep items in flight across the round
+    // trip. Measured at m = 128 on 4 GPUs (512^3): per-rank 0.694 vs 0.619
+    // for two 32-line tiles per CTA.
+    if (!defer && A.t.f.chunks <= 4 && !getenv("TDS_DD_TPC")) cfg.tpc = 1;
     if constexpr (M == 32)
         if (A.t.f.sz == 32 && !(getenv("TDS_SZC") && getenv("TDS_SZC")[0] == '0'))
             return defer ? launch_dd2_t<M, UNI, 16, 32>(A, cfg, s)
