@@ -16,7 +16,7 @@ constexpr int TL = 16;                     // lines per tile: 16 x fp64 = 128 B 
 constexpr int NCOEF = 10;                  // per-row table: st0..st4, f, r, w, sa, sc
 constexpr int MMAX_UNIFORM = 32;
 constexpr int MAX_CHUNKS = 32;             // C*TL <= 512 threads per tile
-constexpr int CTR_SLOTS = 16;              // k_tma schedule counters per plan
+constexpr int CTR_SLOTS = 64;              // schedule counters per plan (launches in flight)
 
 enum FastMode { MODE_SOLVE = 0, MODE_PASS_A = 1, MODE_PASS_B = 2 };
 enum EdgeMode { EDGE_ZERO = 0, EDGE_WRAP = 1, EDGE_HALO = 2 };

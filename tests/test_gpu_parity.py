@@ -393,7 +393,7 @@ def test_dynamic_item_schedule_bitwise_and_concurrent(monkeypatch, n, periodic):
     ref = T.run_distd2(s, u, stencil=st)
     torch.cuda.synchronize()
     monkeypatch.setenv("TDS_DYN", "1")
-    for _ in range(20):                                # > the 16 counter slots
+    for _ in range(70):                                # > the 64 counter slots
         got = T.run_distd2(s, u, stencil=st)
     torch.cuda.synchronize()
     assert torch.equal(got, ref)
