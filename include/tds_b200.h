@@ -318,6 +318,13 @@ int tds_transport_direction(const tds_plan* d1, const tds_plan* d2, const double
                             const double* u1, const double* u2, double* out0, double* out1,
                             double* out2, double nu, int nx, int ny, int nz, int sz, int dir,
                             void* stream);
+/* elementwise helpers of the transport demo: out = u + dt * rhs (the Euler
+ * step, momentum.py:216-222) and out = a * b (the u_j u_i product of the
+ * 3-solve fallback contribution, momentum.py:118) */
+int tds_euler_update(const double* u, const double* rhs, double dt, double* out,
+                     long long count, void* stream);
+int tds_multiply(const double* a, const double* b, double* out, long long count, void* stream);
+
 /* cubic n^3 field: SZ-blocked layout of src_dir -> dst_dir in one pass
  * (reorder, layout.py:144-152); accumulate = 1 adds into dst */
 int tds_reorder(const double* src, double* dst, int n, int sz, int src_dir,

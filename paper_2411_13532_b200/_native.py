@@ -95,6 +95,8 @@ SIGNATURES = {
                                       ctypes.c_ulonglong, _I, _P]),
     "tds_fused_transport_direction": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _D, _I, _I, _I, _I,
                                            _P, _P, _P, ctypes.c_ulonglong, _I, _P]),
+    "tds_euler_update": (_I, [_P, _P, _D, _P, _LL, _P]),
+    "tds_multiply": (_I, [_P, _P, _P, _LL, _P]),
     "tds_reorder3": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "tds_pack": (_I, [_P, _P, _I, _I, _I, _I, _I, _LL, _P]),
     "tds_unpack": (_I, [_P, _P, _I, _I, _I, _I, _I, _LL, _P]),

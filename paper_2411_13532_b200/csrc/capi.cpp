@@ -560,6 +560,8 @@ int launch_reorder(const double* src, double* dst, int nx, int ny, int nz, int s
 int launch_transport_combine(const double* uj, const double* du, const double* dp,
                              const double* d2u, double nu, double* out, long long count,
                              int accumulate, cudaStream_t s);
+int launch_axpy_mul(const double* a, const double* b, double w, int mul, double* out,
+                    long long count, cudaStream_t s);
 int transport_launch_from_plans(const tds_plan* d1, const tds_plan* d2, const double* ui,
                                 const double* uj, double* out, double nu, int accumulate,
                                 long long lines, int sz, cudaStream_t s, int geom, int nx = 0,
@@ -632,6 +634,18 @@ extern "C" int tds_transport_direction(const tds_plan* d1, const tds_plan* d2, c
     double* out[3] = {out0, out1, out2};
     return tds::transport_direction_from_plans(d1, nu != 0.0 ? d2 : nullptr, u, out, nu, nx, ny,
                                                nz, sz, dir, S(stream));
+}
+
+extern "C" int tds_euler_update(const double* u, const double* rhs, double dt, double* out,
+                                long long count, void* stream) {
+    if (!u || !rhs || !out || count < 0) return set_err(TDS_ERR_INVALID, "bad argument");
+    return tds::launch_axpy_mul(u, rhs, dt, 0, out, count, S(stream));
+}
+
+extern "C" int tds_multiply(const double* a, const double* b, double* out, long long count,
+                            void* stream) {
+    if (!a || !b || !out || count < 0) return set_err(TDS_ERR_INVALID, "bad argument");
+    return tds::launch_axpy_mul(a, b, 0.0, 1, out, count, S(stream));
 }
 
 extern "C" int tds_reorder3(const double* src, double* dst, int nx, int ny, int nz, int sz,

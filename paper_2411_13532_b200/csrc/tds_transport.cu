@@ -1247,6 +1247,22 @@ __global__ void k_transport_combine(const double* __restrict__ uj, const double*
     out[idx] = accumulate ? out[idx] + v : v;
 }
 
+// out = a + w * b (the Euler update of the transport demo) or, with
+// w = NaN, out = a * b (the u_j u_i product of the 3-solve fallback path)
+__global__ void k_axpy_mul(const double* __restrict__ a, const double* __restrict__ b, double w,
+                           int mul, double* __restrict__ out, long long count) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    out[i] = mul ? a[i] * b[i] : fma(w, b[i], a[i]);
+}
+
+int launch_axpy_mul(const double* a, const double* b, double w, int mul, double* out,
+                    long long count, cudaStream_t s) {
+    if (count == 0) return TDS_OK;
+    k_axpy_mul<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(a, b, w, mul, out, count);
+    return cuda_check(cudaGetLastError(), "k_axpy_mul launch");
+}
+
 int launch_transport_combine(const double* uj, const double* du, const double* dp,
                              const double* d2u, double nu, double* out, long long count,
                              int accumulate, cudaStream_t s) {

@@ -107,6 +107,21 @@ def _operator(order, h, n):
     return hit
 
 
+def _product(a, b):
+    """a * b elementwise on the device (k_axpy_mul)."""
+    out = _torch().empty_like(a)
+    N.check(N.lib().tds_multiply(_vp(a), _vp(b), _vp(out), out.numel(), _stream_handle()))
+    return out
+
+
+def _euler(u, rhs, dt):
+    """u + dt * rhs elementwise on the device (k_axpy_mul)."""
+    out = _torch().empty_like(u)
+    N.check(N.lib().tds_euler_update(_vp(u), _vp(rhs), float(dt), _vp(out), out.numel(),
+                                     _stream_handle()))
+    return out
+
+
 def _component_index(i):
     return _COMPONENTS.index(i) if isinstance(i, str) else int(i)
 
@@ -152,7 +167,7 @@ def _contribution_into(ci, dj, fields, out, accumulate, rank_count):
         return
     # general path: three DistD2 solves (any size, emulated ranks) + combine
     d_comp = run_distd2(s1, comp, stencil=st1, rank_count=rank_count)
-    d_prod = run_distd2(s1, advect * comp, stencil=st1, rank_count=rank_count)
+    d_prod = run_distd2(s1, _product(advect, comp), stencil=st1, rank_count=rank_count)
     d2 = (run_distd2(s2, comp, stencil=st2, rank_count=rank_count)
           if fields.nu != 0.0 else None)
     N.check(N.lib().tds_transport_combine(
@@ -338,7 +353,7 @@ def _local_contribution(comp, advect, out, n, h, nu, accumulate):
     s1, st1 = _operator(1, h, n)
     s2, st2 = _operator(2, h, n)
     d_comp = run_distd2(s1, comp, stencil=st1)
-    d_prod = run_distd2(s1, torch.mul(advect, comp), stencil=st1)
+    d_prod = run_distd2(s1, _product(advect, comp), stencil=st1)
     d2 = run_distd2(s2, comp, stencil=st2) if nu != 0.0 else None
     N.check(N.lib().tds_transport_combine(
         _vp(advect), _vp(d_comp), _vp(d_prod), None if d2 is None else _vp(d2),
@@ -545,7 +560,7 @@ class SlabTransport:
             return
         r1, r2 = self._rank
         d_comp = r1.solve(comp)
-        d_prod = r1.solve(torch.mul(advect, comp))
+        d_prod = r1.solve(_product(advect, comp))
         d2 = r2.solve(comp) if r2 is not None else None
         N.check(N.lib().tds_transport_combine(
             _vp(advect), _vp(d_comp), _vp(d_prod), None if d2 is None else _vp(d2),
@@ -613,7 +628,7 @@ class SlabTransport:
     def euler_step(self, u, v, w, dt):
         """u <- u + dt * RHS(u) on this rank's slab (momentum.py:216-222)."""
         rhs = self.rhs(u, v, w)
-        return tuple(c + dt * r for c, r in zip((u, v, w), rhs))
+        return tuple(_euler(c, r, dt) for c, r in zip((u, v, w), rhs))
 
     def check(self):
         """Wait for the last fused kernels' status; TimeoutError if a rank's
@@ -642,6 +657,6 @@ class SlabTransport:
 def euler_step(fields, dt, rank_count=1):
     """u <- u + dt * RHS(u) (momentum.py:216-222)."""
     rhs = evaluate_transport_rhs(fields, rank_count=rank_count)
-    comps = [GroupedField(fields.layout, fields.component(i).data + dt * rhs[i].data)
+    comps = [GroupedField(fields.layout, _euler(fields.component(i).data, rhs[i].data, dt))
              for i in range(3)]
     return VelocityField(comps[0], comps[1], comps[2], fields.nu, fields.h)
