@@ -3,13 +3,17 @@ consumer of the DistD2 path in the reference (momentum.py:1-222).
 
     RHS_j of u_i = -1/2 (u_j d(u_i)/dx_j + d(u_j u_i)/dx_j) + nu d2(u_i)/dx_j2
 
-Work is grouped by direction j exactly like the reference: the components
-are re-laid out for j (one-pass `k_reorder`), the three contributions of
-direction j are computed while the fields sit in the j layout, and they fold
-back into the x-layout accumulators (`k_reorder` with accumulate). Each
-(i, j) contribution is ONE fused kernel (`k_transport`): it reads u_i and u_j
-once and runs the three compact solves of every chunk in registers. Field
-data stays on the device (CUDA tensors) for the whole pipeline.
+Work is grouped by direction j like the reference, but nothing is re-laid
+out: one `k_transport_dir` launch per direction reads u, v, w once (the y / z
+lines in place from the x layout), runs the nine compact solves of that
+direction and writes (x) or adds (y, z: TMA reduce-add) all three
+components' contributions -- 192 B per grid point for the whole RHS.
+`SlabTransport` splits the box into z-slabs over the ranks; its z pass is
+`k_dd_transport_dir`, the same nine solves with the DistD2 neighbour rounds
+in-kernel. Shapes these kernels cannot tile fall back, direction by
+direction, to one fused kernel per (i, j) term (`k_transport_tma`) and the
+reference-shaped reorder pipeline. Field data stays on the device (CUDA
+tensors) for the whole pipeline.
 """
 
 import ctypes
