@@ -49,7 +49,7 @@ def build(force=False, verbose_ptxas=False):
         objs.append(o)
         if force or _stale(o, [s] + headers):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-c", s, "-o", o]
+                   *os.environ.get("TDS_NVCC_EXTRA", "").split(), "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)

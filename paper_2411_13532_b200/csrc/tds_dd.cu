@@ -87,10 +87,22 @@ __device__ __forceinline__ unsigned long long ld_sys_u64(const double* p) {
 }
 // wait for a neighbour's value in my mailbox slot, consume it, re-arm the slot
 // (v: the slot's value if already loaded, else SENTINEL)
+#ifdef TDS_WAIT_PROF
+// debug builds (TDS_NVCC_EXTRA=-DTDS_WAIT_PROF, tools/wait_prof.py): ns spent
+// in take_v per call site (0: halo rows, 1: boundary rows), summed over threads
+__device__ unsigned long long g_wait_ns[2];
+__device__ unsigned long long g_wait_n[2];
+#endif
 template <class Args>
 __device__ double take_v(double* slot, unsigned long long v, const Args& A,
-                         unsigned long long* err) {
+                         unsigned long long* err, int site = 1) {
     if (v == SENTINEL) v = ld_sys_u64(slot);
+#ifdef TDS_WAIT_PROF
+    const unsigned long long tp0 = globaltimer();
+    atomicAdd(&g_wait_n[site], 1ULL);
+#else
+    (void)site;
+#endif
     if (v == SENTINEL) {
         const unsigned long long t0 = globaltimer();
         unsigned ns = 32;
@@ -108,6 +120,9 @@ __device__ double take_v(double* slot, unsigned long long v, const Args& A,
         }
     }
     *reinterpret_cast<unsigned long long*>(slot) = SENTINEL;
+#ifdef TDS_WAIT_PROF
+    atomicAdd(&g_wait_ns[site], globaltimer() - tp0);
+#endif
     return __longlong_as_double((long long)v);
 }
 template <class Args>
@@ -252,12 +267,12 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         // halos of the rank block come from the neighbours' ROUND-1 posts
         double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
         if (hlo) {
-            h0 = take_v(hlo, a0, A, err);
-            h1 = take_v(hlo + sz, a1, A, err);
+            h0 = take_v(hlo, a0, A, err, 0);
+            h1 = take_v(hlo + sz, a1, A, err, 0);
         }
         if (hhi) {
-            h2 = take_v(hhi, b0, A, err);
-            h3 = take_v(hhi + sz, b1, A, err);
+            h2 = take_v(hhi, b0, A, err, 0);
+            h3 = take_v(hhi + sz, b1, A, err, 0);
         }
 #pragma unroll
         for (int i = 0; i < M + 4; ++i) {
@@ -597,12 +612,12 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
         double v[M + 4];
         double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
         if (hlo) {
-            h0 = take_v(hlo, a0, A, err);
-            h1 = take_v(hlo + sz, a1, A, err);
+            h0 = take_v(hlo, a0, A, err, 0);
+            h1 = take_v(hlo + sz, a1, A, err, 0);
         }
         if (hhi) {
-            h2 = take_v(hhi, b0, A, err);
-            h3 = take_v(hhi + sz, b1, A, err);
+            h2 = take_v(hhi, b0, A, err, 0);
+            h3 = take_v(hhi + sz, b1, A, err, 0);
         }
 #pragma unroll
         for (int i = 0; i < M + 4; ++i) {
@@ -1843,4 +1858,17 @@ int launch_dd_transport_dir(const FastArgs& f1, const FastArgs& f2, const double
     return set_err(TDS_ERR_UNSUPPORTED, "direction distributed transport: tile");
 }
 
+#ifdef TDS_WAIT_PROF
+// debug builds only (not in the C ABI header): [halo ns, boundary ns, halo
+// takes, boundary takes] since the last call, then reset
+extern "C" int tds_debug_wait_stats(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_wait_ns, 2 * sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out + 2, g_wait_n, 2 * sizeof(unsigned long long));
+    const unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_wait_ns, z, sizeof(z));
+    cudaMemcpyToSymbol(g_wait_n, z, sizeof(z));
+    return 0;
+}
+#endif
 }  // namespace tds
