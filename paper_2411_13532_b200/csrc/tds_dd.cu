@@ -729,6 +729,25 @@ __global__ void __launch_bounds__(512) k_dd2(const __grid_constant__ DDArgs A) {
 
 namespace {
 
+// The fused per-rank kernels wait on other CTAs of the neighbour ranks, so
+// every CTA of the persistent grid must be resident at once: launch them
+// cooperatively -- the driver then guarantees co-residency of the grid or
+// fails the launch (cudaErrorCooperativeLaunchTooLarge) instead of letting
+// an unscheduled CTA deadlock its partners. TDS_COOP=0: plain launch.
+template <class Args>
+int launch_resident(const void* fn, long long grid, int threads, size_t smem, cudaStream_t s,
+                    const Args& A, const char* what) {
+    if (const char* e = getenv("TDS_COOP"))
+        if (e[0] == '0') {
+            void* args[1] = {const_cast<Args*>(&A)};
+            return cuda_check(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, s),
+                              what);
+        }
+    void* args[1] = {const_cast<Args*>(&A)};
+    return cuda_check(
+        cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, s), what);
+}
+
 size_t dd_smem(const FastArgs& a, TileCfg c) {
     return tma_smem(a, c) + (size_t)c.tpc * 2 * c.tl * 8;
 }
@@ -769,8 +788,8 @@ int launch_dd_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     }
     if (A.query) return (int)std::min<long long>(grid, 1 << 30);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd does not fit on an SM");
-    k_dd<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
-    return cuda_check(cudaGetLastError(), "k_dd launch");
+    return launch_resident(reinterpret_cast<const void*>(k_dd<M, UNI, TLT, SZC>), grid, threads,
+                           smem, s, A, "k_dd launch");
 }
 
 size_t dd2_smem(const FastArgs& a, TileCfg c, int M) {
@@ -804,8 +823,8 @@ int launch_dd2_t(const DDArgs& A0, TileCfg cfg, cudaStream_t s) {
     }
     if (A.query) return (int)std::min<long long>(grid, 1 << 30);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd2 does not fit on an SM");
-    k_dd2<M, UNI, TLT, SZC><<<(unsigned)grid, threads, smem, s>>>(A);
-    return cuda_check(cudaGetLastError(), "k_dd2 launch");
+    return launch_resident(reinterpret_cast<const void*>(k_dd2<M, UNI, TLT, SZC>), grid, threads,
+                           smem, s, A, "k_dd2 launch");
 }
 
 bool defer_policy() {
@@ -1350,8 +1369,7 @@ int launch_dd_transport_t(const TrDDArgs& A0, cudaStream_t s) {
     // co-resident, identical on every rank (max_ctas: ranks sharing a device)
     const long long grid = persistent_grid(fn, threads, smem, A.items, A.max_ctas);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport does not fit on an SM");
-    k_dd_transport<TLT, SZC, XZ><<<(unsigned)grid, threads, smem, s>>>(A);
-    return cuda_check(cudaGetLastError(), "k_dd_transport launch");
+    return launch_resident(fn, grid, threads, smem, s, A, "k_dd_transport launch");
 }
 
 }  // namespace
@@ -1810,8 +1828,7 @@ int launch_dd_transport_dir_t(const TdArgs& A0, cudaStream_t s) {
     if ((rc = ensure_smem(fn, smem, "cudaFuncSetAttribute(k_dd_transport_dir)"))) return rc;
     const long long grid = persistent_grid(fn, threads, smem, A.items, A.max_ctas);
     if (grid < 1) return set_err(TDS_ERR_UNSUPPORTED, "k_dd_transport_dir does not fit on an SM");
-    k_dd_transport_dir<TLT><<<(unsigned)grid, threads, smem, s>>>(A);
-    return cuda_check(cudaGetLastError(), "k_dd_transport_dir launch");
+    return launch_resident(fn, grid, threads, smem, s, A, "k_dd_transport_dir launch");
 }
 
 }  // namespace
