@@ -642,22 +642,23 @@ int launch_transport_tma(const TransportArgs& a, cudaStream_t s) {
 //
 // A component phase is the two passes of k_transport_tma: d/dx and d2/dx2
 // of u_i from one read of the window (one barrier for both reduced
-// systems), then d/dx of u_j u_i. Its product sweeps are the phase's last
-// reads of u_i, so right after the second barrier thread 0 re-arms that
-// tile for the next item. Components run in the order a, b, j (j = the
-// advecting one, read by every phase): u_a loads during phases b and j, u_b
-// during j and the next item's a, u_j during the next item's first sweeps
-// (it is first needed by the a combine). 16-line tiles: one CTA of 512
+// systems), then d/dx of u_j u_i. Components run in the order a, b, j (j =
+// the advecting one, read by every phase). The x pass re-arms a tile right
+// after the phase's last read of it (its second barrier). The y / z passes
+// stage the phase's contribution in the freed tile, in its load layout, and
+// add it into the accumulator by TMA reduce-add; tiles a and b are re-armed
+// at the next phase's first barrier (once the TMA engine has read them), u_j
+// at once (the next item needs it early). 16-line tiles: one CTA of 512
 // threads and 3 x 64 KB of tiles per SM at n = 512.
 //
 // Instruction diet (the kernel is issue / latency bound, not HBM bound):
 // per-row coefficients of both operators sit in shared memory as 16-byte
-// pairs (DirRow, one LDS.128 per pair); and the periodic P = 1 reduced map
-// is block-circulant, so every chunk's band row is the same nb values --
-// they travel in the kernel-parameter bank and enter the bounds as
-// constant DFMA operands (no loads), fully unrolled.
+// pairs (DirRow, one LDS.128 per pair); the periodic P = 1 reduced map is
+// block-circulant, so every chunk's band row is the same nb values -- they
+// travel in the kernel-parameter bank and, with the band lengths as
+// template constants (NB1 / NB2), enter the bounds as uniform-register DFMA
+// operands; the x / y passes take the stencil weights the same way.
 constexpr int NBC_MAX = 24;
-
 
 struct TransportDirArgs {
     TransportArgs p;          // geometry, tables and reduced maps (ui/uj/out unused)
@@ -674,9 +675,7 @@ struct TransportDirArgs {
     double2 hc1[NBC_MAX], hc2[NBC_MAX];
 };
 
-
 namespace {
-
 
 // (F, L) of a chunk from a circulant band row held in the parameter bank:
 // the same terms and association as band_bounds (even columns into F0 / L0,
