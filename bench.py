@@ -491,28 +491,47 @@ def run_multi_e2e(args, torch, dist, solver, fields, n, world, dev):
     dev_in = {d: torch.empty_like(fields[d]) for d in "xyz"}
     dev_out = {d: torch.empty_like(fields[d]) for d in "xyz"}
     steps = max(2, min(args.steps, args.e2e_steps))
+    # pipelined like run_distd2's host path: host -> device copies on one
+    # stream, the solves on the current stream (the same order on every
+    # rank), device -> host copies on a third, so the copies of one
+    # direction overlap the solve of another
+    s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    comp = torch.cuda.current_stream()
 
     def step():
+        arrived = {}
         for d in "xyz":
-            dev_in[d].copy_(host_in[d], non_blocking=True)
+            with torch.cuda.stream(s_in):
+                dev_in[d].copy_(host_in[d], non_blocking=True)
+                arrived[d] = torch.cuda.Event()
+                arrived[d].record(s_in)
+        for d in "xyz":
+            comp.wait_event(arrived[d])
             solver.solve(dev_in[d], dev_out[d])
-            host_out[d].copy_(dev_out[d], non_blocking=True)
+            solved = torch.cuda.Event()
+            solved.record(comp)
+            s_out.wait_event(solved)
+            with torch.cuda.stream(s_out):
+                host_out[d].copy_(dev_out[d], non_blocking=True)
         torch.cuda.synchronize()
 
     step()
-    dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
-    dist.barrier()
-    dt = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
-    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-    dt = float(dt.item())
+    dt = 1e30
+    for _ in range(2):                                  # best of two blocks (see run_e2e)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            step()
+        dist.barrier()
+        t = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = min(dt, float(t.item()))
     nbytes = sum(h.numel() * 8 for h in host_in.values())
     return {"value": round(3 * BYTES_PER_POINT * n ** 3 / dt / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
-            "ms_per_step": round(dt * 1e3, 3), "steps": steps,
-            "api": "per rank: pinned host slab -> DistD2Rank.solve -> pinned host slab, x3"}
+            "ms_per_step": round(dt * 1e3, 3), "steps": steps, "blocks": 2, "of": "best block",
+            "api": "per rank: pinned host slab -> DistD2Rank.solve -> pinned host slab, x3 "
+                   "(copies and solves on three streams)"}
 
 
 # ------------------------------------------------------------ CPU legs
