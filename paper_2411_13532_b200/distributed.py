@@ -464,7 +464,9 @@ def _pipelined_host_solve(plan, u_host, out_host, groups, sz):
     if pipe is None:
         pipe = _PIPES[dev] = _HostPipe(dev)
     per_group = u_host[0].numel()
-    gchunk = max(1, min(groups, PIPE_CHUNK_BYTES // (8 * per_group)))
+    import os
+    chunk_bytes = int(os.environ.get("TDS_PIPE_MB", "0")) << 20 or PIPE_CHUNK_BYTES
+    gchunk = max(1, min(groups, chunk_bytes // (8 * per_group)))
     bufs = pipe.buffers(gchunk * per_group)
     uf = u_host.view(groups, per_group)
     of = out_host.view(groups, per_group)
