@@ -128,6 +128,9 @@ int tds_preprocess(const double* a, const double* b, const double* c, int m,
  * reference's truncation at the partition's rank boundaries
  * (run_distd2, distributed.py:399-449). u, out: (groups, n, sz) device,
  * distinct (non-aliasing) buffers -- the reference returns fresh arrays.
+ * The persistent kernels take their work items from schedule counters held
+ * in the plan (reset by each launch's last CTA): up to 64 launches of one
+ * plan may be in flight at once on different streams.
  */
 int tds_solve(const tds_plan* plan, const double* u, double* out,
               long long groups, int sz, void* stream);
