@@ -244,9 +244,8 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
         const bool valid = line < p.lines;
         nvalid += valid ? 1u : 0u;
         const long long nxt = s_q[(it + 1) % 3];
-        // halo slots of this item: loads in flight across the TMA wait, and
-        // issued before the next item's halo posts, whose HBM reads the posts
-        // wait for (the two latencies overlap instead of adding up)
+        // halo slots of this item: loads in flight across the TMA wait (the
+        // next item's halo posts come later, during ROUND 2)
         const long long hb = valid ? halo_base_t<SZC>(line, p.sz) : 0;
         double* hlo = (valid && first_chunk && A.mail_prev) ? A.mail + par + mb.h_lo() + hb : nullptr;
         double* hhi = (valid && last_chunk && A.mail_next) ? A.mail + par + mb.h_hi() + hb : nullptr;
@@ -259,7 +258,6 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
             b0 = ld_sys_u64(hhi);
             b1 = ld_sys_u64(hhi + sz);
         }
-        if (nxt < p.items) publish_halo(nxt);          // one item ahead
 
         while (!mbar_try_wait(bar, phase)) {
         }
@@ -322,6 +320,11 @@ __global__ void __launch_bounds__(512) k_dd(const __grid_constant__ DDArgs A) {
                 post(A.mail_next + par + mb.d_from_prev() + line, g1y);
             }
         }
+        // ROUND 1 of the next item while the boundary rows travel: the HBM
+        // reads of its halo rows overlap the neighbour round trip (half an
+        // item ahead of use; deadlock-free as above: a post depends only on
+        // earlier items and on same-item posts that precede their waits)
+        if (nxt < p.items) publish_halo(nxt);
         double F, L;
         if (A.t.band)   // banded reduced map, pin columns excluded (TDS_BAND=0: full row)
             band_bounds_nopins<TLT>(p.Hb + (size_t)chunk * p.nb, __ldg(p.bq0 + chunk), p.nb, Y,
